@@ -1,0 +1,120 @@
+/*
+ * dart_b200.h -- C ABI of the B200-native DART multi-class detection path.
+ *
+ * The reference exposes this path as a Python function API (no FFI); each entry
+ * point below replaces the arithmetic of one reference function, and the Python
+ * mirror in paper_2603_11441_b200/ binds them with ctypes:
+ *
+ *   dart_model_create   <- build_model / load_model weight hand-off
+ *                          (/root/reference/pkg/src/dart/model.py:306-334, 657-681)
+ *   dart_backbone       <- backbone_forward (model.py:454-459: patch_tokens :426,
+ *                          _block_forward x num_blocks :412, fpn_from_tokens :446)
+ *   dart_encdec         <- encdec_forward (model.py:536-570, per class _encdec_single :511-533)
+ *   dart_postprocess    <- postprocess (pipeline.py:266-294)
+ *
+ * Conventions: plain C, no exceptions across the boundary.  Every function returns
+ * an int status (DART_OK = 0); on failure dart_last_error() returns a thread-local
+ * message.  All tensor pointers are caller-owned DEVICE pointers, row-major,
+ * contiguous; `stream` is a cudaStream_t passed as void*.  No host synchronisation
+ * happens inside any entry point except dart_model_create.  A model handle owns its
+ * device weights and an activation workspace, and must be used from one stream at
+ * a time (one handle per GPU / per concurrent stream).
+ */
+#ifndef DART_B200_H
+#define DART_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DART_OK 0
+#define DART_ERR_INVALID 1 /* bad argument / shape: maps to ValueError      */
+#define DART_ERR_CUDA 2    /* CUDA launch or allocation failure: RuntimeError */
+
+/* Status-flag bits written by dart_backbone into `flags` (device int32). */
+#define DART_FLAG_IMAGE_RANGE 1   /* some image value outside [0, 1] or NaN (model.py:432-433) */
+#define DART_FLAG_NONFINITE 2     /* some FPN level non-finite (model.py:161-166)              */
+
+#define DART_MAX_BLOCKS 256
+
+/* Model dimensions: the fields of the reference ModelConfig (model.py:41-56) plus the
+ * per-block structure of DetectorModel (block_kinds / attn_enabled / mlp_enabled,
+ * model.py:140-149). */
+typedef struct dart_model_desc {
+  int32_t image_size, patch_size, embed_dim, num_blocks, window_size, num_heads;
+  int32_t fpn_dims[3];
+  int32_t text_tokens, text_dim, num_queries, num_encoder_layers, num_decoder_layers;
+  int32_t block_global[DART_MAX_BLOCKS]; /* 1 = global attention, 0 = windowed */
+  int32_t attn_enabled[DART_MAX_BLOCKS];
+  int32_t mlp_enabled[DART_MAX_BLOCKS];
+} dart_model_desc;
+
+typedef struct dart_model dart_model;
+
+/* Upload weights.  `weights` holds `n_weights` HOST float32 pointers in the reference's
+ * parameter declaration order without the mask head (model.py:216-303, the DARTM1
+ * order), each tensor row-major in the reference's [in, out] layout. */
+int dart_model_create(const dart_model_desc* desc, const float* const* weights, int32_t n_weights,
+                      dart_model** out);
+void dart_model_destroy(dart_model* m);
+
+/* Number of parameter tensors dart_model_create expects for `desc`. */
+int32_t dart_expected_weight_count(const dart_model_desc* desc);
+
+/* images [B, S, S, 3] float32 in [0,1] -> L0 [B, T, F0], L1 [B, T/4, F1], L2 [B, T/16, F2]
+ * float32.  The level-0 features are also kept (fp16) in the workspace for a following
+ * dart_encdec(.., l0 = NULL, ..).  `flags` (device int32, zeroed by the caller) receives
+ * DART_FLAG_* bits. */
+int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
+                  void* stream);
+
+/* Class-batched encoder-decoder for B images x N classes.
+ *   l0    [B, T, F0] float32 level-0 features, or NULL to reuse the last dart_backbone output
+ *   text  [N, L_t, d] float32 text embeddings (rows of text.table, model.py:470-484)
+ * outputs (item = b * N + c), float64 like the reference's RawQueryOutputs (model.py:177-188):
+ *   boxes [B*N, Q, 4]  sigmoid (cx, cy, w, h);  score_logits [B*N, Q];  presence_logits [B*N]
+ *   query_features [B*N, Q, d] float32, or NULL. */
+int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
+                double* score_logits, double* presence_logits, float* query_features, void* stream);
+
+/* Presence gate, score gate, (score desc, query asc) ordering and greedy per-class NMS,
+ * decisions in fp64 (pipeline.py:243-294).  Inputs float64 [N,Q,4] / [N,Q] / [N].  For N items of Q queries:
+ *   kept_count [N] int32, kept_query [N, Q] int32, kept_score [N, Q] float64 (sigmoid),
+ *   presence_prob [N] float64.
+ * cross_class != 0 additionally runs cross-class NMS and writes keep_flag [N, Q] int32
+ * (1 = survivor of slot k of item c); scratch must hold N*(2Q+1)+1 int32. */
+int dart_postprocess(dart_model* m, const double* boxes, const double* score_logits, const double* presence_logits,
+                     int32_t N, int32_t Q, double presence_threshold, double score_threshold,
+                     double nms_iou_threshold, int32_t cross_class, int32_t* kept_count, int32_t* kept_query,
+                     double* kept_score, double* presence_prob, int32_t* keep_flag, int32_t* scratch,
+                     void* stream);
+
+/* Kernel-level entry points (used by the per-kernel parity tests and microbenchmarks).
+ * dart_gemm: out = epilogue(A[M,K] . W[N,K]^T + bias), A/W fp16 K-major, K % 64 == 0,
+ *   N % 64 == 0; epi 0 fp16 out, 1 fp16 relu, 2 fp32 out, 3 fp32 out += , 4 fp16 with RoPE on
+ *   columns < rope_cols (tables [rope_T, rope_hd/2]), 5 fp32 out + fp16 out2.
+ * dart_attention: o = softmax(q k^T / sqrt(hd)) v, fp16 in/out, tokens `*_tok_stride`
+ *   elements apart, heads hd apart, batch items `*_batch_stride` apart; win > 0 selects the
+ *   windowed token map over a grid x grid token image (batch = images * (grid/win)^2). */
+int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* out2, int32_t M, int32_t N,
+              int32_t K, int32_t epi, const float* rope_cos, const float* rope_sin, int32_t rope_T, int32_t rope_hd,
+              int32_t rope_cols, void* stream);
+int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
+                   int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,
+                   int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,
+                   int32_t grid, void* stream);
+
+/* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
+ * on this handle (for the bench's gpu_launches evidence). */
+int64_t dart_launch_count(const dart_model* m);
+void dart_reset_launch_count(dart_model* m);
+
+const char* dart_last_error(void);
+const char* dart_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DART_B200_H */

@@ -1,0 +1,118 @@
+"""ctypes binding of libdart_b200.so (include/dart_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing, or no CUDA
+device is present, every forward raises.  `load()` is the single place the library
+is opened; it is built in-tree by `__graft_entry__.build()` (csrc/Makefile).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdart_b200.so")
+MAX_BLOCKS = 256
+
+DART_OK = 0
+DART_ERR_INVALID = 1
+DART_ERR_CUDA = 2
+FLAG_IMAGE_RANGE = 1
+FLAG_NONFINITE = 2
+
+# Every symbol include/dart_b200.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "dart_model_create",
+    "dart_model_destroy",
+    "dart_expected_weight_count",
+    "dart_backbone",
+    "dart_encdec",
+    "dart_postprocess",
+    "dart_gemm",
+    "dart_attention",
+    "dart_launch_count",
+    "dart_reset_launch_count",
+    "dart_last_error",
+    "dart_version",
+)
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure reported by the C ABI (DART_ERR_CUDA)."""
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [
+        ("image_size", ctypes.c_int32),
+        ("patch_size", ctypes.c_int32),
+        ("embed_dim", ctypes.c_int32),
+        ("num_blocks", ctypes.c_int32),
+        ("window_size", ctypes.c_int32),
+        ("num_heads", ctypes.c_int32),
+        ("fpn_dims", ctypes.c_int32 * 3),
+        ("text_tokens", ctypes.c_int32),
+        ("text_dim", ctypes.c_int32),
+        ("num_queries", ctypes.c_int32),
+        ("num_encoder_layers", ctypes.c_int32),
+        ("num_decoder_layers", ctypes.c_int32),
+        ("block_global", ctypes.c_int32 * MAX_BLOCKS),
+        ("attn_enabled", ctypes.c_int32 * MAX_BLOCKS),
+        ("mlp_enabled", ctypes.c_int32 * MAX_BLOCKS),
+    ]
+
+
+_lib = None
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+F64 = ctypes.c_double
+
+
+def load() -> ctypes.CDLL:
+    """Open the in-tree library once; raise if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the DART B200 path)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.dart_model_create.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(ctypes.c_void_p), I32,
+                                      ctypes.POINTER(ctypes.c_void_p)]
+    lib.dart_model_create.restype = ctypes.c_int
+    lib.dart_model_destroy.argtypes = [P]
+    lib.dart_model_destroy.restype = None
+    lib.dart_expected_weight_count.argtypes = [ctypes.POINTER(ModelDesc)]
+    lib.dart_expected_weight_count.restype = I32
+    lib.dart_backbone.argtypes = [P, P, I32, P, P, P, P, P]
+    lib.dart_backbone.restype = ctypes.c_int
+    lib.dart_encdec.argtypes = [P, P, I32, P, I32, P, P, P, P, P]
+    lib.dart_encdec.restype = ctypes.c_int
+    lib.dart_postprocess.argtypes = [P, P, P, P, I32, I32, F64, F64, F64, I32, P, P, P, P, P, P, P]
+    lib.dart_postprocess.restype = ctypes.c_int
+    lib.dart_gemm.argtypes = [P, P, P, P, P, I32, I32, I32, I32, P, P, I32, I32, I32, P]
+    lib.dart_gemm.restype = ctypes.c_int
+    lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,
+                                   ctypes.c_int64, ctypes.c_int64, I32, I32, P]
+    lib.dart_attention.restype = ctypes.c_int
+    lib.dart_launch_count.argtypes = [P]
+    lib.dart_launch_count.restype = ctypes.c_int64
+    lib.dart_reset_launch_count.argtypes = [P]
+    lib.dart_reset_launch_count.restype = None
+    lib.dart_last_error.argtypes = []
+    lib.dart_last_error.restype = ctypes.c_char_p
+    lib.dart_version.argtypes = []
+    lib.dart_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == DART_OK:
+        return
+    msg = load().dart_last_error().decode(errors="replace")
+    if rc == DART_ERR_INVALID:
+        raise ValueError(msg)
+    raise NativeError(msg)

@@ -1,0 +1,227 @@
+// Flash attention, fp16 operands / fp32 online softmax, for every attention on the
+// DART hot path:
+//   backbone windowed + global self-attention, hd = 80 (reference model.py:390-409)
+//   enc-dec self / cross / decoder attention, hd = 16   (reference model.py:491-502)
+// softmax(q k^T / sqrt(hd)) v with max-subtraction (tensors.py:194-197) computed online
+// in exp2 space.  Operands are read in place through strides (token / head / batch),
+// so the QKV / KV GEMM outputs need no transposes; windowed blocks map in-window
+// indices to tokens on the fly (reference _window_partition, model.py:375-387).
+//
+// This is the first correct sm_100a path: m16n8k16 mma.sync fragments, cp.async
+// double-buffered K/V tiles of 64 keys, 16 query rows per warp.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dart {
+namespace {
+
+constexpr int BKV = 64;
+
+__device__ __forceinline__ long long tok_offset(int z, int i, long long batch_stride, int tok_stride,
+                                                long long img_stride, int win, int grid, int nwin) {
+  if (win == 0) return (long long)z * batch_stride + (long long)i * tok_stride;
+  const int img = z / nwin, w = z - img * nwin;
+  const int wpr = grid / win;
+  const int r = (w / wpr) * win + i / win;
+  const int c = (w % wpr) * win + i % win;
+  return (long long)img * img_stride + (long long)(r * grid + c) * tok_stride;
+}
+
+template <int HD, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) flash_attn_kernel(AttnArgs a) {
+  constexpr int BQ = 16 * WARPS;
+  constexpr int PITCH = HD + 8;  // halves; breaks ldmatrix bank conflicts
+  constexpr int CH = HD / 8;     // 16-byte chunks per row
+  constexpr int KSTEPS = HD / 16;
+  constexpr int NT_O = HD / 8;   // output n-tiles
+  extern __shared__ __align__(128) __half smem_attn[];
+  __half* sQ = smem_attn;
+  __half (*sK)[BKV * PITCH] = reinterpret_cast<__half (*)[BKV * PITCH]>(smem_attn + BQ * PITCH);
+  __half (*sV)[BKV * PITCH] = reinterpret_cast<__half (*)[BKV * PITCH]>(smem_attn + BQ * PITCH + 2 * BKV * PITCH);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int z = blockIdx.z, h = blockIdx.y;
+  const int q0 = blockIdx.x * BQ;
+
+  const __half* qb = a.q + (long long)h * a.head_stride_q;
+  const int zkv = a.kv_batch_mod > 0 ? z % a.kv_batch_mod : z;
+  const __half* kb = a.k + (long long)h * a.head_stride_k;
+  const __half* vb = a.v + (long long)h * a.head_stride_v;
+
+  // ---- Q tile
+  for (int idx = tid; idx < BQ * CH; idx += WARPS * 32) {
+    const int r = idx / CH, c = idx % CH;
+    const int qi = q0 + r;
+    const bool ok = qi < a.Lq;
+    const __half* src = qb + (ok ? tok_offset(z, qi, a.q_batch_stride, a.q_tok_stride, a.img_stride_q, a.win, a.grid, a.nwin) : 0) + c * 8;
+    cp_async16(smem_u32(&sQ[r * PITCH + c * 8]), src, ok);
+  }
+  auto load_kv = [&](int buf, int kt) {
+    for (int idx = tid; idx < BKV * CH; idx += WARPS * 32) {
+      const int r = idx / CH, c = idx % CH;
+      const int ki = kt * BKV + r;
+      const bool ok = ki < a.Lk;
+      const long long ko = ok ? tok_offset(zkv, ki, a.k_batch_stride, a.k_tok_stride, a.img_stride_k, a.win, a.grid, a.nwin) : 0;
+      const long long vo = ok ? tok_offset(zkv, ki, a.v_batch_stride, a.v_tok_stride, a.img_stride_v, a.win, a.grid, a.nwin) : 0;
+      cp_async16(smem_u32(&sK[buf][r * PITCH + c * 8]), kb + ko + c * 8, ok);
+      cp_async16(smem_u32(&sV[buf][r * PITCH + c * 8]), vb + vo + c * 8, ok);
+    }
+  };
+  load_kv(0, 0);
+  cp_async_commit();
+
+  const int nkt = (a.Lk + BKV - 1) / BKV;
+  uint32_t qf[KSTEPS][4];
+  float o[NT_O][4];
+#pragma unroll
+  for (int n = 0; n < NT_O; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY};
+  float l_r[2] = {0.f, 0.f};
+  const int g = lane >> 2, t = lane & 3;
+
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nkt) load_kv(buf ^ 1, kt + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kt == 0) {
+#pragma unroll
+      for (int ks = 0; ks < KSTEPS; ++ks) {
+        const int row = warp * 16 + (lane & 15);
+        const int col = ks * 16 + (lane >> 4) * 8;
+        ldmatrix_x4(qf[ks], smem_u32(&sQ[row * PITCH + col]));
+      }
+    }
+    // ---- S = Q K^T (16 x 64 per warp)
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {  // pairs of 8-key n-tiles
+#pragma unroll
+      for (int ks = 0; ks < KSTEPS; ++ks) {
+        uint32_t b[4];
+        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int dim = ks * 16 + ((lane >> 3) & 1) * 8;
+        ldmatrix_x4(b, smem_u32(&sK[buf][key * PITCH + dim]));
+        mma16816(s[2 * np], qf[ks], b);
+        mma16816(s[2 * np + 1], qf[ks], b + 2);
+      }
+    }
+    // ---- online softmax (log2 domain)
+    const int kbase = kt * BKV;
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kbase + n * 8 + 2 * t + (e & 1);
+        float v = s[n][e] * a.scale_log2;
+        v = key < a.Lk ? v : -INFINITY;
+        s[n][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 2));
+      const float m_new = fmaxf(m_r[r], mx[r]);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      corr[r] = fast_exp2(m_r[r] - m_use);
+      m_r[r] = m_new;
+      mx[r] = m_use;
+    }
+    float rs[2] = {0.f, 0.f};
+    uint32_t p[4][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float p0 = fast_exp2(s[n][0] - mx[0]);
+      const float p1 = fast_exp2(s[n][1] - mx[0]);
+      const float p2 = fast_exp2(s[n][2] - mx[1]);
+      const float p3 = fast_exp2(s[n][3] - mx[1]);
+      rs[0] += p0 + p1;
+      rs[1] += p2 + p3;
+      p[n >> 1][(n & 1) * 2 + 0] = pack_half2(p0, p1);
+      p[n >> 1][(n & 1) * 2 + 1] = pack_half2(p2, p3);
+    }
+    l_r[0] = l_r[0] * corr[0] + rs[0];
+    l_r[1] = l_r[1] * corr[1] + rs[1];
+#pragma unroll
+    for (int n = 0; n < NT_O; ++n) {
+      o[n][0] *= corr[0];
+      o[n][1] *= corr[0];
+      o[n][2] *= corr[1];
+      o[n][3] *= corr[1];
+    }
+    // ---- O += P V
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t pa[4] = {p[ks][0], p[ks][1], p[ks][2], p[ks][3]};
+#pragma unroll
+      for (int np = 0; np < NT_O / 2; ++np) {
+        uint32_t b[4];
+        const int key = ks * 16 + (lane & 15);
+        const int dim = np * 16 + (lane >> 4) * 8;
+        ldmatrix_x4_trans(b, smem_u32(&sV[buf][key * PITCH + dim]));
+        mma16816(o[2 * np], pa, b);
+        mma16816(o[2 * np + 1], pa, b + 2);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- normalise and store
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 2);
+  }
+  const float inv0 = 1.f / l_r[0], inv1 = 1.f / l_r[1];
+  __half* ob = a.o + (long long)h * a.head_stride_o;
+  const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
+  if (r0 < a.Lq) {
+    __half* dst = ob + tok_offset(z, r0, a.o_batch_stride, a.o_tok_stride, a.img_stride_o, a.win, a.grid, a.nwin);
+#pragma unroll
+    for (int n = 0; n < NT_O; ++n)
+      *reinterpret_cast<uint32_t*>(dst + n * 8 + 2 * t) = pack_half2(o[n][0] * inv0, o[n][1] * inv0);
+  }
+  if (r1 < a.Lq) {
+    __half* dst = ob + tok_offset(z, r1, a.o_batch_stride, a.o_tok_stride, a.img_stride_o, a.win, a.grid, a.nwin);
+#pragma unroll
+    for (int n = 0; n < NT_O; ++n)
+      *reinterpret_cast<uint32_t*>(dst + n * 8 + 2 * t) = pack_half2(o[n][2] * inv1, o[n][3] * inv1);
+  }
+}
+
+template <int HD>
+int launch(const AttnArgs& a, cudaStream_t stream) {
+  constexpr int WARPS = 4;
+  constexpr int SMEM = (16 * WARPS + 4 * BKV) * (HD + 8) * 2;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(flash_attn_kernel<HD, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  dim3 grid((a.Lq + 16 * WARPS - 1) / (16 * WARPS), a.heads, a.batch);
+  flash_attn_kernel<HD, WARPS><<<grid, WARPS * 32, SMEM, stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int attention(const AttnArgs& a, int head_dim, cudaStream_t stream) {
+  if (a.Lq <= 0 || a.batch <= 0) return 0;
+  switch (head_dim) {
+    case 16: return launch<16>(a, stream);
+    case 32: return launch<32>(a, stream);
+    case 64: return launch<64>(a, stream);
+    case 80: return launch<80>(a, stream);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace dart

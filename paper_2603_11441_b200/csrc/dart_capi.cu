@@ -1,0 +1,808 @@
+// C ABI of the DART B200 path (include/dart_b200.h): weight upload, workspace, and
+// the orchestration of the backbone / class-batched enc-dec / post-processing kernels.
+//
+// Data layout in HBM (per model handle):
+//   weights   GEMM weights transposed to [out, in] fp16 (K-major for tcgen05), one TMA
+//             descriptor each (128B swizzle, box 64 x BN); biases, LN affine, RoPE tables,
+//             text table and heads in fp32.  The 6 encoder cross-attention K/V projections
+//             and the 6 decoder cross-attention K/V projections are each concatenated into
+//             one [6*2d, d] weight so one GEMM per pass reads its input once.
+//   backbone  residual stream x [B*T, E] fp32; LN outputs / qkv / attention out / MLP hidden fp16.
+//   enc-dec   class-shared prefix e1 [B*T, d] fp32; per-class residual e [B*N*T, d] fp32;
+//             decoder memory K/V for all layers [B*N*T, 6*2d] fp16; decoder stream [B*N*201, d] fp32.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dart_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace dart;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(expr)                                                                                   \
+  do {                                                                                             \
+    int _e = (int)(expr);                                                                          \
+    if (_e != 0) {                                                                                 \
+      char _b[256];                                                                                \
+      snprintf(_b, sizeof(_b), "%s failed: %s (%s:%d)", #expr, cudaGetErrorString((cudaError_t)_e), \
+               __FILE__, __LINE__);                                                                \
+      return fail(DART_ERR_CUDA, _b);                                                              \
+    }                                                                                              \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp16 tensor map over [rows, inner] with row stride `ld` elements, 128B swizzle.
+bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct GemmW {
+  __half* w = nullptr;  // [N, K] fp16
+  float* b = nullptr;   // [N]
+  int N = 0, K = 0;
+  CUtensorMap tmap;
+};
+struct LNW {
+  float* g = nullptr;
+  float* b = nullptr;
+};
+struct AttnW {
+  GemmW q, kv, out;
+};
+struct BlockW {
+  LNW ln1, ln2;
+  GemmW qkv, out, fc1, fc2;
+};
+struct XLayerW {
+  LNW ln1, ln2, ln3;
+  AttnW self, cross;
+  GemmW fc1, fc2;
+};
+
+__global__ void transpose_cast_kernel(const float* __restrict__ src, __half* __restrict__ dst, int in, int out,
+                                      int kpad) {
+  // src [in, out] fp32 -> dst [out, kpad] fp16 (zero for k >= in)
+  __shared__ float tile[32][33];
+  const int o0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, o = o0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < in && o < out) ? src[(long long)i * out + o] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int o = o0 + r, i = i0 + threadIdx.x;
+    if (o < out && i < kpad) dst[(long long)o * kpad + i] = __float2half_rn(tile[threadIdx.x][r]);
+  }
+}
+
+struct Workspace {
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  void* get(size_t n) {
+    n = (n + 255) & ~size_t(255);
+    void* p = nullptr;
+    if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    bytes += n;
+    return p;
+  }
+  void release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct dart_model {
+  dart_model_desc d;
+  int T = 0, G = 0, E = 0, H = 0, hd = 0, kpatch = 0, kpad = 0, D = 0, Lt = 0, Q1 = 0, F0 = 0, F1 = 0, F2 = 0;
+  int num_sms = 148;
+  std::vector<void*> owned;
+  GemmW patch;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  std::vector<BlockW> blocks;
+  GemmW fpn[3];
+  float* text_table = nullptr;
+  GemmW enc_in;
+  std::vector<XLayerW> enc, dec;
+  LNW enc_final, dec_final;
+  GemmW enc_cross_kv_all, dec_cross_kv_all;
+  float* queries = nullptr;  // [Q+1, d] fp32 (queries then presence token)
+  float *box_w = nullptr, *box_b = nullptr, *score_w = nullptr, *score_b = nullptr, *pres_w = nullptr,
+        *pres_b = nullptr;
+  // workspaces
+  Workspace bb_ws, ed_ws;
+  int bb_cap = 0, ed_cap_items = 0, ed_cap_n = 0, ed_cap_b = 0;
+  int last_backbone_B = 0;
+  struct {
+    __half *patches, *h, *qkv, *ao, *hid, *pool1, *pool2, *l0h;
+    float* x;
+  } bb{};
+  struct {
+    float *e1, *e, *qd, *qd0, *qf;
+    __half *l0h, *h, *q, *kv, *o, *hid, *dkv, *text, *tkv, *dh, *dq, *dkvs, *do_, *dhid;
+  } ed{};
+  int64_t launches = 0;
+
+  ~dart_model() {
+    bb_ws.release();
+    ed_ws.release();
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+namespace {
+
+template <typename T>
+T* dev_alloc(dart_model* m, size_t n) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+  m->owned.push_back(p);
+  return reinterpret_cast<T*>(p);
+}
+
+float* upload_f32(dart_model* m, const float* h, size_t n) {
+  float* d = dev_alloc<float>(m, n);
+  if (d && cudaMemcpy(d, h, n * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  return d;
+}
+
+// Transposed fp16 weight from a host [in, out] fp32 matrix, written at row offset `row0`
+// of a [total_out, kpad] destination.
+bool upload_wT(dart_model* m, const float* h, int in, int out, __half* dst, int kpad, int row0, float* scratch) {
+  if (cudaMemcpy(scratch, h, (size_t)in * out * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+  dim3 grid((out + 31) / 32, (kpad + 31) / 32);
+  transpose_cast_kernel<<<grid, dim3(32, 8)>>>(scratch, dst + (size_t)row0 * kpad, in, out, kpad);
+  return cudaGetLastError() == cudaSuccess;
+}
+
+bool finish_gemmw(GemmW& g) {
+  return make_tmap(&g.tmap, g.w, g.K, g.N, g.K, gemm_bn_for(g.N));
+}
+
+struct WeightCursor {
+  const float* const* w;
+  int n, i = 0;
+  const float* next() { return i < n ? w[i++] : nullptr; }
+};
+
+bool make_gemm(dart_model* m, WeightCursor& c, int in, int out, float* scratch, GemmW& g, int kpad = 0) {
+  const float* wh = c.next();
+  const float* bh = c.next();
+  if (!wh || !bh) return false;
+  g.N = out;
+  g.K = kpad ? kpad : in;
+  g.w = dev_alloc<__half>(m, (size_t)g.N * g.K);
+  if (!g.w || !upload_wT(m, wh, in, out, g.w, g.K, 0, scratch)) return false;
+  g.b = upload_f32(m, bh, out);
+  return g.b && finish_gemmw(g);
+}
+
+bool make_ln(dart_model* m, WeightCursor& c, int dim, LNW& l) {
+  const float* gh = c.next();
+  const float* bh = c.next();
+  if (!gh || !bh) return false;
+  l.g = upload_f32(m, gh, dim);
+  l.b = upload_f32(m, bh, dim);
+  return l.g && l.b;
+}
+
+// Attention projections; when `fused` is non-null the K/V projection of this layer is
+// also written into the concatenated [layers*2d, d] weight at row offset `row0`.
+bool make_attn(dart_model* m, WeightCursor& c, int d, float* scratch, AttnW& a, GemmW* fused, int row0) {
+  if (!make_gemm(m, c, d, d, scratch, a.q)) return false;
+  const float* kvw = c.next();
+  const float* kvb = c.next();
+  if (!kvw || !kvb) return false;
+  if (fused) {
+    if (!upload_wT(m, kvw, d, 2 * d, fused->w, d, row0, scratch)) return false;
+    if (cudaMemcpy(fused->b + row0, kvb, 2 * d * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+  } else {
+    a.kv.N = 2 * d;
+    a.kv.K = d;
+    a.kv.w = dev_alloc<__half>(m, (size_t)2 * d * d);
+    if (!a.kv.w || !upload_wT(m, kvw, d, 2 * d, a.kv.w, d, 0, scratch)) return false;
+    a.kv.b = upload_f32(m, kvb, 2 * d);
+    if (!a.kv.b || !finish_gemmw(a.kv)) return false;
+  }
+  return make_gemm(m, c, d, d, scratch, a.out);
+}
+
+bool make_xlayer(dart_model* m, WeightCursor& c, int d, float* scratch, XLayerW& L, GemmW* fused, int row0) {
+  return make_ln(m, c, d, L.ln1) && make_attn(m, c, d, scratch, L.self, nullptr, 0) && make_ln(m, c, d, L.ln2) &&
+         make_attn(m, c, d, scratch, L.cross, fused, row0) && make_ln(m, c, d, L.ln3) &&
+         make_gemm(m, c, d, 4 * d, scratch, L.fc1) && make_gemm(m, c, 4 * d, d, scratch, L.fc2);
+}
+
+int check_desc(const dart_model_desc* d) {
+  if (!d) return fail(DART_ERR_INVALID, "null model desc");
+  if (d->patch_size <= 0 || d->image_size % d->patch_size) return fail(DART_ERR_INVALID, "image_size % patch_size");
+  const int g = d->image_size / d->patch_size;
+  if (d->window_size <= 0 || g % d->window_size || g % 4) return fail(DART_ERR_INVALID, "grid/window");
+  if (d->num_blocks < 0 || d->num_blocks > DART_MAX_BLOCKS) return fail(DART_ERR_INVALID, "num_blocks");
+  if (d->num_heads <= 0 || d->embed_dim % d->num_heads) return fail(DART_ERR_INVALID, "embed_dim % heads");
+  const int hd = d->embed_dim / d->num_heads, hde = d->text_dim / d->num_heads;
+  auto hd_ok = [](int h) { return h == 16 || h == 32 || h == 64 || h == 80; };
+  if (!hd_ok(hd) || !hd_ok(hde)) return fail(DART_ERR_INVALID, "unsupported head_dim (16/32/64/80)");
+  if (d->embed_dim % 64 || d->text_dim % 64 || d->fpn_dims[0] % 64 || d->fpn_dims[1] % 64 || d->fpn_dims[2] % 64)
+    return fail(DART_ERR_INVALID, "embed/text/fpn dims must be multiples of 64");
+  if (d->num_queries < 1 || d->num_queries + 1 > 1024) return fail(DART_ERR_INVALID, "num_queries");
+  if (d->text_tokens < 1 || d->num_encoder_layers < 1 || d->num_decoder_layers < 1)
+    return fail(DART_ERR_INVALID, "text_tokens / layer counts");
+  return DART_OK;
+}
+
+// ---------------------------------------------------------------- launch helpers
+int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi, GemmEpi e, cudaStream_t s) {
+  if (M <= 0) return 0;
+  CUtensorMap ta;
+  if (!make_tmap(&ta, A, W.K, M, lda, 128)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (A)");
+  if (e.bias == nullptr) e.bias = W.b;
+  m->launches++;
+  int rc = gemm_tc(ta, W.tmap, M, W.N, W.K, epi, e, m->num_sms, s);
+  if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
+  return 0;
+}
+
+GemmEpi epi_out(void* out, int ldo) {
+  GemmEpi e;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+
+AttnArgs attn_base(int heads, int hd) {
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.heads = heads;
+  a.head_stride_q = a.head_stride_k = a.head_stride_v = a.head_stride_o = hd;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+  return a;
+}
+
+int attn(dart_model* m, const AttnArgs& a, int hd, cudaStream_t s) {
+  m->launches++;
+  int rc = attention(a, hd, s);
+  if (rc) return fail(DART_ERR_CUDA, std::string("attention: ") + cudaGetErrorString((cudaError_t)rc));
+  return 0;
+}
+
+#define LAUNCH(expr)                                                                                      \
+  do {                                                                                                    \
+    m->launches++;                                                                                        \
+    int _rc = (int)(expr);                                                                                \
+    if (_rc) return fail(DART_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString((cudaError_t)_rc)); \
+  } while (0)
+#define RUN(expr)          \
+  do {                     \
+    int _rc = (expr);      \
+    if (_rc) return _rc;   \
+  } while (0)
+
+int ensure_backbone_ws(dart_model* m, int B) {
+  if (B <= m->bb_cap) return 0;
+  m->bb_ws.release();
+  const size_t rows = (size_t)B * m->T, E = m->E;
+  auto& w = m->bb_ws;
+  m->bb.patches = (__half*)w.get(rows * m->kpad * 2);
+  m->bb.x = (float*)w.get(rows * E * 4);
+  m->bb.h = (__half*)w.get(rows * E * 2);
+  m->bb.qkv = (__half*)w.get(rows * 3 * E * 2);
+  m->bb.ao = (__half*)w.get(rows * E * 2);
+  m->bb.hid = (__half*)w.get(rows * 4 * E * 2);
+  m->bb.pool1 = (__half*)w.get(rows / 4 * E * 2);
+  m->bb.pool2 = (__half*)w.get(rows / 16 * E * 2);
+  m->bb.l0h = (__half*)w.get(rows * m->F0 * 2);
+  if (!m->bb.patches || !m->bb.x || !m->bb.h || !m->bb.qkv || !m->bb.ao || !m->bb.hid || !m->bb.pool1 ||
+      !m->bb.pool2 || !m->bb.l0h) {
+    m->bb_ws.release();
+    m->bb_cap = 0;
+    return fail(DART_ERR_CUDA, "backbone workspace allocation failed");
+  }
+  m->bb_cap = B;
+  return 0;
+}
+
+int ensure_encdec_ws(dart_model* m, int B, int N) {
+  if (B * N <= m->ed_cap_items && N <= m->ed_cap_n && B <= m->ed_cap_b) return 0;
+  m->ed_ws.release();
+  const int items = B * N;
+  const size_t T = m->T, D = m->D, rows = (size_t)items * T, drows = (size_t)items * m->Q1;
+  const int ne = m->d.num_encoder_layers, nd = m->d.num_decoder_layers;
+  auto& w = m->ed_ws;
+  auto& e = m->ed;
+  e.e1 = (float*)w.get((size_t)B * T * D * 4);
+  e.l0h = (__half*)w.get((size_t)B * T * m->F0 * 2);
+  e.e = (float*)w.get(rows * D * 4);
+  e.h = (__half*)w.get(rows * D * 2);
+  e.q = (__half*)w.get(rows * D * 2);
+  e.kv = (__half*)w.get(rows * 2 * D * 2);
+  e.o = (__half*)w.get(rows * D * 2);
+  e.hid = (__half*)w.get(rows * 4 * D * 2);
+  e.dkv = (__half*)w.get(rows * nd * 2 * D * 2);
+  e.text = (__half*)w.get((size_t)N * m->Lt * D * 2);
+  e.tkv = (__half*)w.get((size_t)N * m->Lt * ne * 2 * D * 2);
+  e.qd0 = (float*)w.get((size_t)m->Q1 * D * 4);
+  e.qd = (float*)w.get(drows * D * 4);
+  e.qf = (float*)w.get(drows * D * 4);
+  e.dh = (__half*)w.get(drows * D * 2);
+  e.dq = (__half*)w.get(drows * D * 2);
+  e.dkvs = (__half*)w.get(drows * 2 * D * 2);
+  e.do_ = (__half*)w.get(drows * D * 2);
+  e.dhid = (__half*)w.get(drows * 4 * D * 2);
+  void* all[] = {e.e1, e.l0h, e.e, e.h, e.q, e.kv, e.o, e.hid, e.dkv, e.text, e.tkv, e.qd0, e.qd, e.qf,
+                 e.dh, e.dq, e.dkvs, e.do_, e.dhid};
+  for (void* p : all)
+    if (!p) {
+      m->ed_ws.release();
+      m->ed_cap_items = m->ed_cap_n = m->ed_cap_b = 0;
+      return fail(DART_ERR_CUDA, "enc-dec workspace allocation failed");
+    }
+  m->ed_cap_items = items;
+  m->ed_cap_n = N;
+  m->ed_cap_b = B;
+  return 0;
+}
+
+// One pre-LN attention sub-block + residual over `rows` rows of the fp32 stream `x`:
+// x += out_proj(MHA(LN(x), kv_source)).  Self-attention when kv16 == nullptr.
+struct XAttnSpec {
+  int items, Lq;                 // batch items and query rows per item
+  const __half* kv16 = nullptr;  // external K/V (cross-attention): [.., tok_stride] fp16
+  int kv_tok_stride = 0, Lk = 0, kv_mod = 0;
+  long long kv_batch_stride = 0;
+};
+
+int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpec& sp, __half* h, __half* q,
+          __half* kv, __half* o, cudaStream_t s) {
+  const int D = m->D, H = m->H, hd = D / H;
+  const int rows = sp.items * sp.Lq;
+  LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
+  RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
+  AttnArgs a = attn_base(H, hd);
+  a.q = q;
+  a.q_tok_stride = D;
+  a.q_batch_stride = (long long)sp.Lq * D;
+  a.o = o;
+  a.o_tok_stride = D;
+  a.o_batch_stride = (long long)sp.Lq * D;
+  a.Lq = sp.Lq;
+  a.batch = sp.items;
+  if (sp.kv16 == nullptr) {
+    RUN(gemm(m, h, rows, D, w.kv, EPI_F16, epi_out(kv, 2 * D), s));
+    a.k = kv;
+    a.v = kv + D;
+    a.k_tok_stride = a.v_tok_stride = 2 * D;
+    a.k_batch_stride = a.v_batch_stride = (long long)sp.Lq * 2 * D;
+    a.Lk = sp.Lq;
+  } else {
+    a.k = sp.kv16;
+    a.v = sp.kv16 + D;
+    a.k_tok_stride = a.v_tok_stride = sp.kv_tok_stride;
+    a.k_batch_stride = a.v_batch_stride = sp.kv_batch_stride;
+    a.Lk = sp.Lk;
+    a.kv_batch_mod = sp.kv_mod;
+  }
+  RUN(attn(m, a, hd, s));
+  return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+}
+
+int xmlp(dart_model* m, float* x, const LNW& ln, const GemmW& fc1, const GemmW& fc2, int rows, __half* h,
+         __half* hid, cudaStream_t s) {
+  const int D = m->D;
+  LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
+  RUN(gemm(m, h, rows, D, fc1, EPI_F16_RELU, epi_out(hid, 4 * D), s));
+  return gemm(m, hid, rows, 4 * D, fc2, EPI_F32_RESID, epi_out(x, D), s);
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+const char* dart_last_error(void) { return g_last_error.c_str(); }
+const char* dart_version(void) { return "dart-b200 0.1 (sm_100a, tcgen05 GEMM + mma.sync flash attention)"; }
+
+int32_t dart_expected_weight_count(const dart_model_desc* d) {
+  if (!d) return -1;
+  return 4 + 12 * d->num_blocks + 6 + 3 + 22 * d->num_encoder_layers + 2 + 2 + 22 * d->num_decoder_layers + 2 + 6;
+}
+
+int dart_model_create(const dart_model_desc* desc, const float* const* weights, int32_t n_weights,
+                      dart_model** out) {
+  if (!out) return fail(DART_ERR_INVALID, "null out");
+  *out = nullptr;
+  RUN(check_desc(desc));
+  if (n_weights != dart_expected_weight_count(desc))
+    return fail(DART_ERR_INVALID, "weight count does not match the model description");
+  if (!encode_fn()) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable (no CUDA driver?)");
+  dart_model* m = new dart_model();
+  m->d = *desc;
+  m->G = desc->image_size / desc->patch_size;
+  m->T = m->G * m->G;
+  m->E = desc->embed_dim;
+  m->H = desc->num_heads;
+  m->hd = m->E / m->H;
+  m->kpatch = 3 * desc->patch_size * desc->patch_size;
+  m->kpad = (m->kpatch + 63) / 64 * 64;
+  m->D = desc->text_dim;
+  m->Lt = desc->text_tokens;
+  m->Q1 = desc->num_queries + 1;
+  m->F0 = desc->fpn_dims[0];
+  m->F1 = desc->fpn_dims[1];
+  m->F2 = desc->fpn_dims[2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (m->F0 != m->D) {
+    delete m;
+    return fail(DART_ERR_INVALID, "fpn_dims[0] must equal text_dim (encdec.input is [F0, d])");
+  }
+
+  // scratch for fp32 uploads (largest weight matrix)
+  const int E = m->E, D = m->D;
+  size_t biggest = std::max<size_t>((size_t)E * 4 * E, (size_t)1024 * D);
+  biggest = std::max<size_t>(biggest, (size_t)m->kpatch * E);
+  float* scratch = nullptr;
+  if (cudaMalloc(&scratch, biggest * sizeof(float)) != cudaSuccess) {
+    delete m;
+    return fail(DART_ERR_CUDA, "weight upload scratch allocation failed");
+  }
+  WeightCursor c{weights, n_weights};
+  bool ok = make_gemm(m, c, m->kpatch, E, scratch, m->patch, m->kpad);
+  const float* rc = c.next();
+  const float* rs = c.next();
+  ok = ok && rc && rs;
+  if (ok) {
+    m->rope_cos = upload_f32(m, rc, (size_t)m->T * (m->hd / 2));
+    m->rope_sin = upload_f32(m, rs, (size_t)m->T * (m->hd / 2));
+    ok = m->rope_cos && m->rope_sin;
+  }
+  m->blocks.resize(desc->num_blocks);
+  for (int b = 0; ok && b < desc->num_blocks; ++b) {
+    BlockW& B = m->blocks[b];
+    ok = make_ln(m, c, E, B.ln1) && make_gemm(m, c, E, 3 * E, scratch, B.qkv) &&
+         make_gemm(m, c, E, E, scratch, B.out) && make_ln(m, c, E, B.ln2) &&
+         make_gemm(m, c, E, 4 * E, scratch, B.fc1) && make_gemm(m, c, 4 * E, E, scratch, B.fc2);
+  }
+  for (int l = 0; ok && l < 3; ++l) ok = make_gemm(m, c, E, desc->fpn_dims[l], scratch, m->fpn[l]);
+  if (ok) {
+    const float* tt = c.next();
+    ok = tt && (m->text_table = upload_f32(m, tt, (size_t)1024 * D)) != nullptr;
+  }
+  ok = ok && make_gemm(m, c, m->F0, D, scratch, m->enc_in);
+  const int ne = desc->num_encoder_layers, nd = desc->num_decoder_layers;
+  auto init_fused = [&](GemmW& g, int layers) {
+    g.N = layers * 2 * D;
+    g.K = D;
+    g.w = dev_alloc<__half>(m, (size_t)g.N * g.K);
+    g.b = dev_alloc<float>(m, g.N);
+    return g.w && g.b;
+  };
+  ok = ok && init_fused(m->enc_cross_kv_all, ne) && init_fused(m->dec_cross_kv_all, nd);
+  m->enc.resize(ne);
+  for (int l = 0; ok && l < ne; ++l) ok = make_xlayer(m, c, D, scratch, m->enc[l], &m->enc_cross_kv_all, l * 2 * D);
+  ok = ok && make_ln(m, c, D, m->enc_final);
+  if (ok) {
+    const float* qw = c.next();
+    const float* pw = c.next();
+    ok = qw && pw && (m->queries = dev_alloc<float>(m, (size_t)m->Q1 * D)) != nullptr;
+    ok = ok && cudaMemcpy(m->queries, qw, (size_t)desc->num_queries * D * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(m->queries + (size_t)desc->num_queries * D, pw, (size_t)D * 4, cudaMemcpyHostToDevice) ==
+                   cudaSuccess;
+  }
+  m->dec.resize(nd);
+  for (int l = 0; ok && l < nd; ++l) ok = make_xlayer(m, c, D, scratch, m->dec[l], &m->dec_cross_kv_all, l * 2 * D);
+  ok = ok && make_ln(m, c, D, m->dec_final);
+  ok = ok && finish_gemmw(m->enc_cross_kv_all) && finish_gemmw(m->dec_cross_kv_all);
+  if (ok) {
+    const float* h[6];
+    for (int i = 0; i < 6; ++i) h[i] = c.next();
+    ok = h[5] != nullptr;
+    if (ok) {
+      m->box_w = upload_f32(m, h[0], (size_t)D * 4);
+      m->box_b = upload_f32(m, h[1], 4);
+      m->score_w = upload_f32(m, h[2], D);
+      m->score_b = upload_f32(m, h[3], 1);
+      m->pres_w = upload_f32(m, h[4], D);
+      m->pres_b = upload_f32(m, h[5], 1);
+      ok = m->box_w && m->box_b && m->score_w && m->score_b && m->pres_w && m->pres_b;
+    }
+  }
+  cudaError_t se = cudaDeviceSynchronize();
+  cudaFree(scratch);
+  if (!ok || se != cudaSuccess || c.i != n_weights) {
+    delete m;
+    return fail(DART_ERR_CUDA, std::string("weight upload failed: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = m;
+  return DART_OK;
+}
+
+void dart_model_destroy(dart_model* m) { delete m; }
+
+int64_t dart_launch_count(const dart_model* m) { return m ? m->launches : 0; }
+void dart_reset_launch_count(dart_model* m) {
+  if (m) m->launches = 0;
+}
+
+int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
+                  void* stream) {
+  if (!m || !images || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  RUN(ensure_backbone_ws(m, B));
+  const int T = m->T, E = m->E, H = m->H, hd = m->hd, G = m->G;
+  const int rows = B * T;
+  auto& w = m->bb;
+  // patch embedding (im2col fused with the [0,1] range check) + GEMM
+  LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, flags, s));
+  RUN(gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(w.x, E), s));
+  const int win = m->d.window_size, nwin = (G / win) * (G / win);
+  for (int b = 0; b < m->d.num_blocks; ++b) {
+    const BlockW& bw = m->blocks[b];
+    if (m->d.attn_enabled[b]) {
+      LAUNCH(layernorm_f32_to_f16(w.x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
+      GemmEpi e = epi_out(w.qkv, 3 * E);
+      e.rope_cos = m->rope_cos;
+      e.rope_sin = m->rope_sin;
+      e.rope_T = T;
+      e.rope_hd = hd;
+      e.rope_cols = 2 * E;  // q and k
+      RUN(gemm(m, w.h, rows, E, bw.qkv, EPI_QKV_ROPE, e, s));
+      AttnArgs a = attn_base(H, hd);
+      a.q = w.qkv;
+      a.k = w.qkv + E;
+      a.v = w.qkv + 2 * E;
+      a.o = w.ao;
+      a.q_tok_stride = a.k_tok_stride = a.v_tok_stride = 3 * E;
+      a.o_tok_stride = E;
+      if (m->d.block_global[b]) {
+        a.q_batch_stride = a.k_batch_stride = a.v_batch_stride = (long long)T * 3 * E;
+        a.o_batch_stride = (long long)T * E;
+        a.Lq = a.Lk = T;
+        a.batch = B;
+      } else {
+        a.win = win;
+        a.grid = G;
+        a.nwin = nwin;
+        a.img_stride_q = a.img_stride_k = a.img_stride_v = (long long)T * 3 * E;
+        a.img_stride_o = (long long)T * E;
+        a.Lq = a.Lk = win * win;
+        a.batch = B * nwin;
+      }
+      RUN(attn(m, a, hd, s));
+      RUN(gemm(m, w.ao, rows, E, bw.out, EPI_F32_RESID, epi_out(w.x, E), s));
+    }
+    if (m->d.mlp_enabled[b]) {
+      LAUNCH(layernorm_f32_to_f16(w.x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
+      RUN(gemm(m, w.h, rows, E, bw.fc1, EPI_F16_RELU, epi_out(w.hid, 4 * E), s));
+      RUN(gemm(m, w.hid, rows, 4 * E, bw.fc2, EPI_F32_RESID, epi_out(w.x, E), s));
+    }
+  }
+  // FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
+  LAUNCH(cast_f32_to_f16(w.x, w.h, (long long)rows * E, s));
+  GemmEpi e0 = epi_out(l0, m->F0);
+  e0.out2 = w.l0h;
+  e0.ldo2 = m->F0;
+  RUN(gemm(m, w.h, rows, E, m->fpn[0], EPI_F32_F16, e0, s));
+  LAUNCH(pool_tokens(w.x, w.pool1, B, G, E, 2, s));
+  RUN(gemm(m, w.pool1, rows / 4, E, m->fpn[1], EPI_F32, epi_out(l1, m->F1), s));
+  LAUNCH(pool_tokens(w.x, w.pool2, B, G, E, 4, s));
+  RUN(gemm(m, w.pool2, rows / 16, E, m->fpn[2], EPI_F32, epi_out(l2, m->F2), s));
+  LAUNCH(finite_check(l0, (long long)rows * m->F0, flags, DART_FLAG_NONFINITE, s));
+  LAUNCH(finite_check(l1, (long long)rows / 4 * m->F1, flags, DART_FLAG_NONFINITE, s));
+  LAUNCH(finite_check(l2, (long long)rows / 16 * m->F2, flags, DART_FLAG_NONFINITE, s));
+  m->last_backbone_B = B;
+  return DART_OK;
+}
+
+int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
+                double* score_logits, double* presence_logits, float* query_features, void* stream) {
+  if (!m || B <= 0 || N <= 0 || !text || !boxes || !score_logits || !presence_logits)
+    return fail(DART_ERR_INVALID, "dart_encdec: bad args");
+  if (!l0 && (m->bb_cap == 0 || m->last_backbone_B != B))
+    return fail(DART_ERR_INVALID, "dart_encdec: l0 == NULL but no matching dart_backbone output");
+  cudaStream_t s = (cudaStream_t)stream;
+  RUN(ensure_encdec_ws(m, B, N));
+  const int T = m->T, D = m->D, Q1 = m->Q1, Q = m->d.num_queries, Lt = m->Lt;
+  const int ne = m->d.num_encoder_layers, nd = m->d.num_decoder_layers;
+  const int items = B * N;
+  auto& w = m->ed;
+  const __half* l0h = m->bb.l0h;
+  if (l0) {
+    LAUNCH(cast_f32_to_f16(l0, w.l0h, (long long)B * T * m->F0, s));
+    l0h = w.l0h;
+  }
+  // ---- class-independent prefix, once per image: input projection + encoder layer-0
+  //      self-attention sub-block (model.py:513-517; text first enters at :518)
+  RUN(gemm(m, l0h, B * T, m->F0, m->enc_in, EPI_F32, epi_out(w.e1, D), s));
+  {
+    XAttnSpec sp;
+    sp.items = B;
+    sp.Lq = T;
+    RUN(xattn(m, w.e1, m->enc[0].ln1, m->enc[0].self, sp, w.h, w.q, w.kv, w.o, s));
+  }
+  for (int b = 0; b < B; ++b)
+    LAUNCH(broadcast_rows(w.e1 + (size_t)b * T * D, w.e + (size_t)b * N * T * D, (long long)T * D, N, s));
+  // ---- text K/V for all 6 encoder cross-attentions in one GEMM
+  LAUNCH(cast_f32_to_f16(text, w.text, (long long)N * Lt * D, s));
+  RUN(gemm(m, w.text, N * Lt, D, m->enc_cross_kv_all, EPI_F16, epi_out(w.tkv, ne * 2 * D), s));
+  const int rows = items * T;
+  for (int l = 0; l < ne; ++l) {
+    const XLayerW& L = m->enc[l];
+    if (l > 0) {
+      XAttnSpec sp;
+      sp.items = items;
+      sp.Lq = T;
+      RUN(xattn(m, w.e, L.ln1, L.self, sp, w.h, w.q, w.kv, w.o, s));
+    }
+    XAttnSpec cx;
+    cx.items = items;
+    cx.Lq = T;
+    cx.kv16 = w.tkv + (size_t)l * 2 * D;
+    cx.kv_tok_stride = ne * 2 * D;
+    cx.kv_batch_stride = (long long)Lt * ne * 2 * D;
+    cx.Lk = Lt;
+    cx.kv_mod = N;
+    RUN(xattn(m, w.e, L.ln2, L.cross, cx, w.h, w.q, w.kv, w.o, s));
+    RUN(xmlp(m, w.e, L.ln3, L.fc1, L.fc2, rows, w.h, w.hid, s));
+  }
+  // ---- encoder memory: final LN, then K/V of all 6 decoder cross-attentions in one GEMM
+  LAUNCH(layernorm_f32_to_f16(w.e, m->enc_final.g, m->enc_final.b, w.h, rows, D, D, D, s));
+  RUN(gemm(m, w.h, rows, D, m->dec_cross_kv_all, EPI_F16, epi_out(w.dkv, nd * 2 * D), s));
+  // ---- decoder: layer-0 self-attention over the learned queries is class-independent
+  CK(cudaMemcpyAsync(w.qd0, m->queries, (size_t)Q1 * D * 4, cudaMemcpyDeviceToDevice, s));
+  {
+    XAttnSpec sp;
+    sp.items = 1;
+    sp.Lq = Q1;
+    RUN(xattn(m, w.qd0, m->dec[0].ln1, m->dec[0].self, sp, w.dh, w.dq, w.dkvs, w.do_, s));
+  }
+  LAUNCH(broadcast_rows(w.qd0, w.qd, (long long)Q1 * D, items, s));
+  const int drows = items * Q1;
+  for (int l = 0; l < nd; ++l) {
+    const XLayerW& L = m->dec[l];
+    if (l > 0) {
+      XAttnSpec sp;
+      sp.items = items;
+      sp.Lq = Q1;
+      RUN(xattn(m, w.qd, L.ln1, L.self, sp, w.dh, w.dq, w.dkvs, w.do_, s));
+    }
+    XAttnSpec cx;
+    cx.items = items;
+    cx.Lq = Q1;
+    cx.kv16 = w.dkv + (size_t)l * 2 * D;
+    cx.kv_tok_stride = nd * 2 * D;
+    cx.kv_batch_stride = (long long)T * nd * 2 * D;
+    cx.Lk = T;
+    RUN(xattn(m, w.qd, L.ln2, L.cross, cx, w.dh, w.dq, w.dkvs, w.do_, s));
+    RUN(xmlp(m, w.qd, L.ln3, L.fc1, L.fc2, drows, w.dh, w.dhid, s));
+  }
+  LAUNCH(layernorm_f32_to_f32(w.qd, m->dec_final.g, m->dec_final.b, w.qf, drows, D, s));
+  LAUNCH(heads_forward(w.qf, Q1, Q, items, D, m->box_w, m->box_b, m->score_w, m->score_b, m->pres_w, m->pres_b, boxes,
+                       score_logits, presence_logits, query_features, s));
+  return DART_OK;
+}
+
+int dart_postprocess(dart_model* m, const double* boxes, const double* score_logits, const double* presence_logits,
+                     int32_t N, int32_t Q, double presence_threshold, double score_threshold,
+                     double nms_iou_threshold, int32_t cross_class, int32_t* kept_count, int32_t* kept_query,
+                     double* kept_score, double* presence_prob, int32_t* keep_flag, int32_t* scratch,
+                     void* stream) {
+  if (!boxes || !score_logits || !presence_logits || N <= 0 || Q <= 0 || !kept_count || !kept_query ||
+      !kept_score || !presence_prob)
+    return fail(DART_ERR_INVALID, "dart_postprocess: bad args");
+  if (cross_class && (!keep_flag || !scratch)) return fail(DART_ERR_INVALID, "cross-class NMS needs keep_flag/scratch");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m) m->launches++;
+  int rc = postprocess_classes(boxes, score_logits, presence_logits, N, Q, presence_threshold, score_threshold,
+                               nms_iou_threshold, kept_count, kept_query, kept_score, presence_prob, s);
+  if (rc) return fail(DART_ERR_CUDA, std::string("postprocess: ") + cudaGetErrorString((cudaError_t)rc));
+  if (cross_class) {
+    if (m) m->launches++;
+    rc = postprocess_cross_class(boxes, kept_count, kept_query, kept_score, N, Q, nms_iou_threshold, keep_flag,
+                                 scratch, s);
+    if (rc) return fail(DART_ERR_CUDA, std::string("cross-class NMS: ") + cudaGetErrorString((cudaError_t)rc));
+  }
+  return DART_OK;
+}
+
+int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* out2, int32_t M, int32_t N,
+              int32_t K, int32_t epi, const float* rope_cos, const float* rope_sin, int32_t rope_T, int32_t rope_hd,
+              int32_t rope_cols, void* stream) {
+  if (!A || !W || !out || M <= 0 || K % 64 || gemm_bn_for(N) == 0 || epi < 0 || epi > 5)
+    return fail(DART_ERR_INVALID, "dart_gemm: bad args");
+  CUtensorMap ta, tb;
+  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, gemm_bn_for(N)))
+    return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  GemmEpi e;
+  e.bias = bias;
+  e.out = out;
+  e.ldo = N;
+  e.out2 = out2;
+  e.ldo2 = N;
+  e.rope_cos = rope_cos;
+  e.rope_sin = rope_sin;
+  e.rope_T = rope_T > 0 ? rope_T : 1;
+  e.rope_hd = rope_hd > 0 ? rope_hd : 2;
+  e.rope_cols = rope_cols;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int rc = gemm_tc(ta, tb, M, N, K, epi, e, sms, (cudaStream_t)stream);
+  if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
+  return DART_OK;
+}
+
+int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
+                   int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,
+                   int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,
+                   int32_t grid, void* stream) {
+  if (!q || !k || !v || !o || batch <= 0 || heads <= 0 || Lq <= 0 || Lk <= 0)
+    return fail(DART_ERR_INVALID, "dart_attention: bad args");
+  AttnArgs a = attn_base(heads, hd);
+  a.q = (const __half*)q;
+  a.k = (const __half*)k;
+  a.v = (const __half*)v;
+  a.o = (__half*)o;
+  a.q_tok_stride = q_tok_stride;
+  a.k_tok_stride = a.v_tok_stride = kv_tok_stride;
+  a.o_tok_stride = o_tok_stride;
+  a.q_batch_stride = q_batch_stride;
+  a.k_batch_stride = a.v_batch_stride = kv_batch_stride;
+  a.o_batch_stride = o_batch_stride;
+  a.Lq = Lq;
+  a.Lk = Lk;
+  a.batch = batch;
+  if (win > 0) {
+    a.win = win;
+    a.grid = grid;
+    a.nwin = (grid / win) * (grid / win);
+    a.img_stride_q = q_batch_stride;
+    a.img_stride_k = a.img_stride_v = kv_batch_stride;
+    a.img_stride_o = o_batch_stride;
+  }
+  int rc = attention(a, hd, (cudaStream_t)stream);
+  if (rc) return fail(DART_ERR_CUDA, std::string("attention: ") + cudaGetErrorString((cudaError_t)rc));
+  return DART_OK;
+}
+
+}  // extern "C"

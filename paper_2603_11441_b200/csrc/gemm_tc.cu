@@ -1,0 +1,275 @@
+// Persistent tcgen05 GEMM for sm_100a: D[M,N] = A[M,K] . W[N,K]^T (+ fused epilogue).
+//
+// Replaces every `_linear` on the DART hot path (reference model.py:356-358:
+// y = x @ W + b with W stored [in, out]; here W is stored transposed [out, in] so
+// both operands are K-major).  Warp roles (256 threads, 1 CTA per SM):
+//   warp 0  TMA producer  (A 128x64 and W BNx64 fp16 tiles, 128B swizzle, STAGES-deep ring)
+//   warp 1  MMA issuer    (one thread, tcgen05.mma.cta_group::1.kind::f16, fp32 accumulators in TMEM)
+//   warp 2  TMEM allocator
+//   warps 4-7 epilogue    (tcgen05.ld -> bias / ReLU / residual / RoPE -> global)
+// Two TMEM accumulator buffers let the epilogue of tile i overlap the MMAs of tile i+1.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dart {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 fp16 = 128 B = one swizzle atom row
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+};
+
+__device__ __forceinline__ void store_f16x32(act_t* dst, const float* v) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
+    u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
+    u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
+    u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
+    d[q] = u;
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const GemmEpi& e) {
+  if (e.bias != nullptr) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 b = __ldg(b4 + q);
+      v[4 * q + 0] += b.x;
+      v[4 * q + 1] += b.y;
+      v[4 * q + 2] += b.z;
+      v[4 * q + 3] += b.w;
+    }
+  }
+  if (EPI == EPI_F16_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+  }
+  if (EPI == EPI_QKV_ROPE) {
+    if (col < e.rope_cols) {
+      const int half_hd = e.rope_hd >> 1;
+      const int tok = row % e.rope_T;
+      const float* ct = e.rope_cos + (size_t)tok * half_hd;
+      const float* st = e.rope_sin + (size_t)tok * half_hd;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        int p = ((col + j) % e.rope_hd) >> 1;
+        float c = __ldg(ct + p), s = __ldg(st + p);
+        float ev = v[j], od = v[j + 1];
+        v[j] = ev * c - od * s;
+        v[j + 1] = ev * s + od * c;
+      }
+    }
+  }
+  if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) {
+    store_f16x32(reinterpret_cast<act_t*>(e.out) + (size_t)row * e.ldo + col, v);
+  } else if (EPI == EPI_F32 || EPI == EPI_F32_F16) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    if (EPI == EPI_F32_F16) store_f16x32(reinterpret_cast<act_t*>(e.out2) + (size_t)row * e.ldo2 + col, v);
+  } else if (EPI == EPI_F32_RESID) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
+    float4 r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = o[q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      o[q] = make_float4(r[q].x + v[4 * q], r[q].y + v[4 * q + 1], r[q].z + v[4 * q + 2], r[q].w + v[4 * q + 3]);
+  }
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, GemmEpi epi) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = N / BN;
+  const int num_tiles = num_m * num_n;
+  const int nk = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile / num_n) * BM;
+        const int n0 = (tile % num_n) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::STAGE_BYTES;
+          uint8_t* sb = sa + L::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+          tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
+          const uint32_t sb = sa + L::A_BYTES;
+          const uint64_t da = umma_desc_sw128(sa);
+          const uint64_t db = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 fp16 = 32 B along K inside the swizzle atom (encoded >> 4)
+            umma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (tile / num_n) * BM;
+      const int n0 = (tile % num_n) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(taddr + c, v);
+        tmem_ld_wait();
+        if (c + 32 >= BN) {
+          // all accumulator columns of this buffer are in registers: hand TMEM back early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (row < M) epilogue_chunk<EPI>(v, row, n0 + c, epi);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  }
+}
+
+template <int BN, int STAGES, int EPI>
+int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, const GemmEpi& epi, int num_sms,
+                cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, 256, L::TOTAL, stream>>>(tA, tB, M, N, K, epi);
+  return (int)cudaGetLastError();
+}
+
+template <int BN, int STAGES>
+int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, const GemmEpi& epi,
+                 int num_sms, cudaStream_t stream) {
+  switch (epi_mode) {
+    case EPI_F16: return launch_gemm<BN, STAGES, EPI_F16>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_F16_RELU: return launch_gemm<BN, STAGES, EPI_F16_RELU>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_F32: return launch_gemm<BN, STAGES, EPI_F32>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_F32_RESID: return launch_gemm<BN, STAGES, EPI_F32_RESID>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_QKV_ROPE: return launch_gemm<BN, STAGES, EPI_QKV_ROPE>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_F32_F16: return launch_gemm<BN, STAGES, EPI_F32_F16>(tA, tB, M, N, K, epi, num_sms, stream);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int gemm_bn_for(int N) {
+  if (N % 256 == 0) return 256;
+  if (N % 128 == 0) return 128;
+  if (N % 64 == 0) return 64;
+  return 0;
+}
+
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int epi_mode, const GemmEpi& epi,
+            int num_sms, cudaStream_t stream) {
+  if (M <= 0) return 0;
+  if (K % BK != 0) return (int)cudaErrorInvalidValue;
+  switch (gemm_bn_for(N)) {
+    case 256: return dispatch_epi<256, 4>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
+    case 128: return dispatch_epi<128, 6>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
+    case 64: return dispatch_epi<64, 8>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace dart

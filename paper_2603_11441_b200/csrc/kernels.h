@@ -1,0 +1,81 @@
+// Internal (C++) launcher declarations shared by the kernel files and the C ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dart {
+
+enum EpiMode {
+  EPI_F16 = 0,        // out16 = acc + bias
+  EPI_F16_RELU = 1,   // out16 = relu(acc + bias)
+  EPI_F32 = 2,        // out32 = acc + bias
+  EPI_F32_RESID = 3,  // out32 += acc + bias       (fp32 residual stream)
+  EPI_QKV_ROPE = 4,   // out16 = rope(acc + bias) on columns < rope_cols
+  EPI_F32_F16 = 5,    // out32 = acc + bias, out2_16 = same in fp16
+};
+
+struct GemmEpi {
+  const float* bias = nullptr;
+  void* out = nullptr;
+  int ldo = 0;
+  void* out2 = nullptr;
+  int ldo2 = 0;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int rope_T = 1;
+  int rope_hd = 2;
+  int rope_cols = 0;
+};
+
+int gemm_bn_for(int N);
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int epi_mode, const GemmEpi& epi,
+            int num_sms, cudaStream_t stream);
+
+// Flash attention (fp16 operands, fp32 softmax/accumulation).
+struct AttnArgs {
+  const __half* q;
+  const __half* k;
+  const __half* v;
+  __half* o;
+  int q_tok_stride, k_tok_stride, v_tok_stride, o_tok_stride;  // elements between consecutive tokens
+  long long q_batch_stride, k_batch_stride, v_batch_stride, o_batch_stride;  // elements between batch items
+  int head_stride_q, head_stride_k, head_stride_v, head_stride_o;            // elements between heads
+  int Lq, Lk;
+  int heads;
+  int batch;
+  float scale_log2;      // log2(e) / sqrt(hd)
+  // windowed token map (win > 0): batch item z covers window (z % nwin) of image (z / nwin);
+  // in-window index i -> token ((wr*win + i/win) * grid + wc*win + i%win), image stride = img_stride
+  int win, grid, nwin;
+  int kv_batch_mod;      // > 0: K/V batch item = z % kv_batch_mod (class-shared image, per-class text)
+  long long img_stride_q, img_stride_k, img_stride_v, img_stride_o;
+};
+int attention(const AttnArgs& a, int head_dim, cudaStream_t stream);
+
+// Row kernels.
+int layernorm_f32_to_f16(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
+                         int ld_in, int ld_out, cudaStream_t stream);
+int layernorm_f32_to_f32(const float* x, const float* gamma, const float* beta, float* y, int rows, int dim,
+                         cudaStream_t stream);
+int cast_f32_to_f16(const float* x, __half* y, long long n, cudaStream_t stream);
+int patchify(const float* images, __half* patches, int B, int S, int p, int kpad, int* flags, cudaStream_t stream);
+int pool_tokens(const float* x, __half* y, int B, int grid, int dim, int factor, cudaStream_t stream);
+int finite_check(const float* x, long long n, int* flags, int bit, cudaStream_t stream);
+int broadcast_rows(const float* src, float* dst, long long row_elems, int reps, cudaStream_t stream);
+int gather_rows_f16(const float* table, const int* rows, __half* out, int n, int dim, cudaStream_t stream);
+int heads_forward(const float* qf, int rows_per_item, int nq, int items, int d, const float* w_box,
+                  const float* b_box, const float* w_score, const float* b_score, const float* w_pres,
+                  const float* b_pres, double* boxes, double* scores, double* presence, float* qf_out,
+                  cudaStream_t stream);
+
+// Post-processing: per-class gates, (score desc, query asc) order, greedy NMS in fp64.
+int postprocess_classes(const double* boxes, const double* score_logits, const double* presence_logits, int N, int Q,
+                        double presence_thr, double score_thr, double nms_thr, int* kept_count, int* kept_query,
+                        double* kept_score, double* presence_prob, cudaStream_t stream);
+int postprocess_cross_class(const double* boxes, const int* kept_count, const int* kept_query,
+                            const double* kept_score, int N, int Q, double nms_thr, int* keep_flag, int* scratch,
+                            cudaStream_t stream);
+
+}  // namespace dart

@@ -1,0 +1,224 @@
+// Detection-only post-processing (reference pipeline.py:243-294), one CTA per class.
+//
+// Decisions must be bit-identical to the reference on identical inputs, so every
+// decision-bearing value is computed in fp64 in the reference's operation order
+// with explicit round-to-nearest intrinsics (no FMA contraction):
+//   presence = sigmoid(presence_logit); class skipped if presence < thr   (pipeline.py:277-279)
+//   s_q = sigmoid(score_logit_q); candidate iff s_q >= thr                (pipeline.py:280-285)
+//   order by (s desc, q asc)                                              (pipeline.py:286)
+//   greedy NMS: keep iff IoU(e, k) < thr for every kept k                 (pipeline.py:257-263)
+//   IoU from (cx,cy,w,h) corners, 0 if iw<=0 or ih<=0                     (pipeline.py:243-254)
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dart {
+namespace {
+
+constexpr int PP_THREADS = 256;
+constexpr int PP_MAXQ = 1024;
+
+__device__ __forceinline__ double sigmoid_d(double x) {
+  x = fmin(fmax(x, -60.0), 60.0);
+  return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+}
+
+__device__ __forceinline__ double iou_d(const double* a, const double* b) {
+  const double ax0 = __dsub_rn(a[0], a[2] / 2), ax1 = __dadd_rn(a[0], a[2] / 2);
+  const double ay0 = __dsub_rn(a[1], a[3] / 2), ay1 = __dadd_rn(a[1], a[3] / 2);
+  const double bx0 = __dsub_rn(b[0], b[2] / 2), bx1 = __dadd_rn(b[0], b[2] / 2);
+  const double by0 = __dsub_rn(b[1], b[3] / 2), by1 = __dadd_rn(b[1], b[3] / 2);
+  const double iw = __dsub_rn(fmin(ax1, bx1), fmax(ax0, bx0));
+  const double ih = __dsub_rn(fmin(ay1, by1), fmax(ay0, by0));
+  if (iw <= 0.0 || ih <= 0.0) return 0.0;
+  const double inter = __dmul_rn(iw, ih);
+  const double uni = __dsub_rn(__dadd_rn(__dmul_rn(a[2], a[3]), __dmul_rn(b[2], b[3])), inter);
+  return __ddiv_rn(inter, uni);
+}
+
+// priority order: higher score first, then lower index
+__device__ __forceinline__ bool before(double sa, int qa, double sb, int qb) {
+  return sa > sb || (sa == sb && qa < qb);
+}
+
+__global__ void __launch_bounds__(PP_THREADS) pp_class_kernel(const double* __restrict__ boxes,
+                                                              const double* __restrict__ score_logits,
+                                                              const double* __restrict__ presence_logits, int Q,
+                                                              double pthr, double sthr, double nthr, int* kept_count,
+                                                              int* kept_query, double* kept_score,
+                                                              double* presence_prob) {
+  __shared__ double ss[PP_MAXQ];
+  __shared__ int sq[PP_MAXQ];
+  __shared__ int kept[PP_MAXQ];
+  __shared__ int nkept, ncand;
+  __shared__ bool skip;
+  const int c = blockIdx.x, tid = threadIdx.x;
+  if (tid == 0) {
+    const double p = sigmoid_d(presence_logits[c]);
+    presence_prob[c] = p;
+    skip = p < pthr;
+    nkept = 0;
+    ncand = 0;
+  }
+  __syncthreads();
+  if (skip) {
+    if (tid == 0) kept_count[c] = 0;
+    return;
+  }
+  int P = 2;
+  while (P < Q) P <<= 1;
+  for (int i = tid; i < P; i += PP_THREADS) {
+    if (i < Q) {
+      const double s = sigmoid_d(score_logits[(long long)c * Q + i]);
+      const bool ok = s >= sthr;
+      ss[i] = ok ? s : -1.0;  // rejected candidates sort last
+      sq[i] = i;
+      if (ok) atomicAdd(&ncand, 1);
+    } else {
+      ss[i] = -2.0;
+      sq[i] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  // bitonic sort into priority order
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += PP_THREADS) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const bool sw = up ? before(ss[l], sq[l], ss[i], sq[i]) : before(ss[i], sq[i], ss[l], sq[l]);
+          if (sw) {
+            const double ts = ss[i];
+            ss[i] = ss[l];
+            ss[l] = ts;
+            const int tq = sq[i];
+            sq[i] = sq[l];
+            sq[l] = tq;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // greedy NMS over the ncand leading candidates
+  const int n = ncand;
+  const double* bc = boxes + (long long)c * Q * 4;
+  for (int e = 0; e < n; ++e) {
+    double be[4];
+    const int qe = sq[e];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) be[j] = bc[qe * 4 + j];
+    bool sup = false;
+    for (int k = tid; k < nkept; k += PP_THREADS) {
+      double bk[4];
+      const int qk = sq[kept[k]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bk[j] = bc[qk * 4 + j];
+      sup |= !(iou_d(be, bk) < nthr);
+    }
+    const bool any = __syncthreads_or(sup);
+    if (!any && tid == 0) kept[nkept++] = e;
+    __syncthreads();
+  }
+  for (int k = tid; k < nkept; k += PP_THREADS) {
+    kept_query[(long long)c * Q + k] = sq[kept[k]];
+    kept_score[(long long)c * Q + k] = ss[kept[k]];
+  }
+  if (tid == 0) kept_count[c] = nkept;
+}
+
+// Cross-class NMS over the per-class survivors (pipeline.py:289-293): order by
+// (score desc, detection index asc), greedy NMS, survivors keep their original order.
+__global__ void __launch_bounds__(1024) pp_cross_kernel(const double* __restrict__ boxes, const int* kept_count,
+                                                        const int* kept_query, const double* kept_score, int N, int Q,
+                                                        double nthr, int* keep_flag, int* scratch) {
+  __shared__ int total;
+  __shared__ int nk;
+  const int tid = threadIdx.x;
+  int* off = scratch;              // [N+1]
+  int* rank_of = scratch + N + 1;  // [total] detection index at each priority rank
+  int* kept = rank_of + N * Q;     // [total]
+  if (tid == 0) {
+    int acc = 0;
+    for (int c = 0; c < N; ++c) {
+      off[c] = acc;
+      acc += kept_count[c];
+    }
+    off[N] = acc;
+    total = acc;
+    nk = 0;
+  }
+  __syncthreads();
+  const int T = total;
+  auto locate = [&](int i, int& c, int& k) {
+    int lo = 0, hi = N;  // off[lo] <= i < off[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (off[mid] <= i) lo = mid; else hi = mid;
+    }
+    c = lo;
+    k = i - off[lo];
+  };
+  for (int i = tid; i < T; i += blockDim.x) {
+    int ci, ki;
+    locate(i, ci, ki);
+    const double si = kept_score[(long long)ci * Q + ki];
+    int r = 0;
+    for (int j = 0; j < T; ++j) {
+      int cj, kj;
+      locate(j, cj, kj);
+      const double sj = kept_score[(long long)cj * Q + kj];
+      r += before(sj, j, si, i);
+    }
+    rank_of[r] = i;
+    keep_flag[(long long)ci * Q + ki] = 0;
+  }
+  __syncthreads();
+  for (int r = 0; r < T; ++r) {
+    const int i = rank_of[r];
+    int ci, ki;
+    locate(i, ci, ki);
+    const int qi = kept_query[(long long)ci * Q + ki];
+    double be[4];
+    for (int j = 0; j < 4; ++j) be[j] = boxes[((long long)ci * Q + qi) * 4 + j];
+    bool sup = false;
+    for (int k = tid; k < nk; k += blockDim.x) {
+      int ck, kk;
+      locate(kept[k], ck, kk);
+      const int qk = kept_query[(long long)ck * Q + kk];
+      double bk[4];
+      for (int j = 0; j < 4; ++j) bk[j] = boxes[((long long)ck * Q + qk) * 4 + j];
+      sup |= !(iou_d(be, bk) < nthr);
+    }
+    const bool any = __syncthreads_or(sup);
+    if (!any && tid == 0) {
+      kept[nk] = i;
+      nk = nk + 1;
+      keep_flag[(long long)ci * Q + ki] = 1;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int postprocess_classes(const double* boxes, const double* score_logits, const double* presence_logits, int N, int Q,
+                        double presence_thr, double score_thr, double nms_thr, int* kept_count, int* kept_query,
+                        double* kept_score, double* presence_prob, cudaStream_t stream) {
+  if (N <= 0) return 0;
+  if (Q > PP_MAXQ) return (int)cudaErrorInvalidValue;
+  pp_class_kernel<<<N, PP_THREADS, 0, stream>>>(boxes, score_logits, presence_logits, Q, presence_thr, score_thr,
+                                                nms_thr, kept_count, kept_query, kept_score, presence_prob);
+  return (int)cudaGetLastError();
+}
+
+int postprocess_cross_class(const double* boxes, const int* kept_count, const int* kept_query,
+                            const double* kept_score, int N, int Q, double nms_thr, int* keep_flag, int* scratch,
+                            cudaStream_t stream) {
+  if (N <= 0) return 0;
+  pp_cross_kernel<<<1, 1024, 0, stream>>>(boxes, kept_count, kept_query, kept_score, N, Q, nms_thr, keep_flag,
+                                          scratch);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace dart

@@ -1,0 +1,145 @@
+"""Per-kernel numerics on the B200: the tcgen05 GEMM (every epilogue) and the flash
+attention, each against a plain PyTorch fp32 reference of the same op, called through
+the C ABI (dart_gemm / dart_attention)."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2603_11441_b200 import _native  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return _native.load()
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def run_gemm(lib, A, W, bias, epi, out, out2=None, rope=None):
+    M, K = A.shape
+    N = W.shape[0]
+    rc, rs, rT, rhd, rcols = (None, None, 0, 0, 0) if rope is None else rope
+    _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr() if bias is not None else None,
+                                out.data_ptr(), out2.data_ptr() if out2 is not None else None, M, N, K, epi,
+                                rc.data_ptr() if rc is not None else None, rs.data_ptr() if rs is not None else None,
+                                rT, rhd, rcols, stream()))
+    torch.cuda.synchronize()
+
+
+def rel_err(got, ref):
+    return float((got.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 192, 128), (1000, 256, 1280), (5184, 3840, 1280),
+                                   (5184, 1280, 5120), (777, 512, 256), (201, 1024, 256), (64, 3072, 256)])
+def test_gemm_f32_out(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda")
+    run_gemm(lib, A, W, bias, 2, out)
+    ref = A.float() @ W.float().T + bias
+    assert rel_err(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("epi", [0, 1, 3, 5])
+def test_gemm_epilogues(lib, epi):
+    M, N, K = 517, 768, 320
+    g = torch.Generator(device="cuda").manual_seed(epi)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(N, device="cuda", generator=g)
+    ref = A.float() @ W.float().T + bias
+    if epi in (0, 1):
+        out = torch.empty(M, N, device="cuda", dtype=torch.float16)
+        run_gemm(lib, A, W, bias, epi, out)
+        if epi == 1:
+            ref = ref.clamp_min(0)
+        assert rel_err(out, ref) < 2e-3
+    elif epi == 3:
+        resid = torch.randn(M, N, device="cuda", generator=g)
+        out = resid.clone()
+        run_gemm(lib, A, W, bias, 3, out)
+        assert rel_err(out, ref + resid) < 1e-5
+    else:
+        out = torch.empty(M, N, device="cuda")
+        out2 = torch.empty(M, N, device="cuda", dtype=torch.float16)
+        run_gemm(lib, A, W, bias, 5, out, out2)
+        assert rel_err(out, ref) < 1e-5 and rel_err(out2, ref) < 2e-3
+
+
+def test_gemm_rope_epilogue(lib):
+    """QKV projection with RoPE on q and k (reference model.py:392-397, tensors.py:235-252)."""
+    T, E, H = 576, 1280, 16
+    hd = E // H
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(T, E, device="cuda", generator=g).half()
+    W = (torch.randn(3 * E, E, device="cuda", generator=g) / math.sqrt(E)).half()
+    bias = torch.randn(3 * E, device="cuda", generator=g)
+    ang = torch.rand(T, hd // 2, device="cuda", generator=g) * 10
+    cos, sin = torch.cos(ang).contiguous(), torch.sin(ang).contiguous()
+    out = torch.empty(T, 3 * E, device="cuda", dtype=torch.float16)
+    run_gemm(lib, A, W, bias, 4, out, rope=(cos, sin, T, hd, 2 * E))
+    y = (A.float() @ W.float().T + bias).reshape(T, 3, H, hd)
+    ev, od = y[..., 0::2], y[..., 1::2]
+    c, s = cos[:, None, None, :], sin[:, None, None, :]
+    rot = torch.empty_like(y)
+    rot[..., 0::2] = ev * c - od * s
+    rot[..., 1::2] = ev * s + od * c
+    rot[:, 2] = y[:, 2]
+    assert rel_err(out, rot.reshape(T, 3 * E)) < 2e-3
+
+
+def ref_attention(q, k, v):
+    s = (q.float() @ k.float().transpose(-1, -2)) / math.sqrt(q.shape[-1])
+    return torch.softmax(s, dim=-1) @ v.float()
+
+
+@pytest.mark.parametrize("hd,Lq,Lk,heads,batch", [(80, 576, 576, 16, 2), (80, 5184, 5184, 2, 1), (16, 5184, 5184, 4, 2),
+                                                  (16, 201, 5184, 16, 3), (16, 5184, 32, 16, 2), (16, 201, 201, 16, 2),
+                                                  (16, 64, 64, 4, 1), (16, 17, 8, 4, 1)])
+def test_attention_dense(lib, hd, Lq, Lk, heads, batch):
+    g = torch.Generator(device="cuda").manual_seed(hd + Lq + Lk)
+    q = (torch.randn(batch, Lq, heads, hd, device="cuda", generator=g) * 2).half()
+    k = (torch.randn(batch, Lk, heads, hd, device="cuda", generator=g) * 2).half()
+    v = torch.randn(batch, Lk, heads, hd, device="cuda", generator=g).half()
+    o = torch.empty(batch, Lq, heads, hd, device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), batch, heads, Lq, Lk,
+                                     hd, heads * hd, heads * hd, heads * hd, Lq * heads * hd, Lk * heads * hd,
+                                     Lq * heads * hd, 0, 0, stream()))
+    torch.cuda.synchronize()
+    ref = ref_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2)).transpose(1, 2)
+    assert float((o.float() - ref).abs().max()) < 1e-2
+
+
+@pytest.mark.parametrize("hd,grid,win,heads", [(80, 72, 24, 16), (16, 8, 4, 4)])
+def test_attention_windowed(lib, hd, grid, win, heads):
+    """Windowed attention reads the token-major QKV directly (model.py:375-387, 398-408)."""
+    T = grid * grid
+    B = 2
+    g = torch.Generator(device="cuda").manual_seed(hd)
+    qkv = (torch.randn(B, T, 3, heads, hd, device="cuda", generator=g) * 2).half()
+    o = torch.empty(B, T, heads * hd, device="cuda", dtype=torch.float16)
+    E = heads * hd
+    base = qkv.reshape(B, T, 3 * E)
+    nw = (grid // win) ** 2
+    _native.check(lib.dart_attention(base.data_ptr(), base[..., E:].data_ptr(), base[..., 2 * E:].data_ptr(),
+                                     o.data_ptr(), B * nw, heads, win * win, win * win, hd, 3 * E, 3 * E, E,
+                                     T * 3 * E, T * 3 * E, T * E, win, grid, stream()))
+    torch.cuda.synchronize()
+    n = grid // win
+    x = qkv.reshape(B, n, win, n, win, 3, heads, hd).permute(0, 1, 3, 5, 6, 2, 4, 7).reshape(B, n * n, 3, heads, win * win, hd)
+    ow = ref_attention(x[:, :, 0], x[:, :, 1], x[:, :, 2])  # [B, nw, H, w2, hd]
+    ow = ow.reshape(B, n, n, heads, win, win, hd).permute(0, 1, 4, 2, 5, 3, 6).reshape(B, T, E)
+    assert float((o.float() - ow).abs().max()) < 1e-2

@@ -1,0 +1,223 @@
+"""End-to-end parity of the CUDA path against the reference's float64 outputs
+(tests/golden/*.npz, written by oracle/make_golden.py from the real reference).
+
+Contract:
+  (1) tensor parity: fp16-operand / fp32-accumulate device path vs float64 reference,
+      tolerances below are stated per tensor;
+  (2) post-processing decisions bit-exact on identical inputs (the reference's raw
+      outputs fed to the device kernel);
+  (3) end-to-end decisions: labels and per-class kept counts exact; kept query index
+      exact whenever the oracle's top-1/top-2 score-logit gap exceeds delta = measured
+      max |score-logit error|, otherwise inside the oracle's delta-tie set.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2603_11441_b200 as D  # noqa: E402
+
+
+def model_for(g):
+    cfg = D.ModelConfig.from_dict(json.loads(str(g["config_json"])))
+    m = D.build_model(cfg, with_mask_head=False)
+    assert D.weights_checksum(m) == str(g["weights_checksum"])
+    return m
+
+
+def scene_for(name, cfg):
+    seed, ncls = {"A": (1, 3), "A2": (5, 4), "B": (1, 3), "C": (1, 4)}[name]
+    img, _ = D.generate_scene(D.SceneSpec(seed=seed, image_size=cfg.image_size, num_classes=ncls))
+    return img
+
+
+def cosine(a, b):
+    a, b = np.ravel(a), np.ravel(b)
+    return float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+
+
+class _Raw:
+    def __init__(self, boxes, scores, pres):
+        self.boxes, self.score_logits, self.presence_logits = boxes, scores, pres
+        self.batch = scores.shape[0]
+
+
+def dets_rows(dets):
+    return np.array([[d.class_id, d.query, *d.box, d.score, d.presence] for d in dets], dtype=np.float64).reshape(-1, 8)
+
+
+def check_decisions(g, raw, delta):
+    """Contract (3) with gates open: one detection per class survives when all boxes overlap;
+    compare labels, counts and the kept query index under the margin rule."""
+    names = [str(n) for n in g["names"]]
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    got = D.postprocess(raw, names, cfg)
+    ref = g["dets_open"]
+    assert [d.class_id for d in got] == [int(r[0]) for r in ref]
+    decided = 0
+    for d, r in zip(got, ref):
+        c, q_ref = int(r[0]), int(r[1])
+        s = g["score_logits"][c]
+        if d.query == q_ref:
+            decided += 1
+            continue
+        # undecidable pick: the device winner must be inside the oracle's delta-tie set
+        assert s[q_ref] - s[d.query] <= 2 * delta, (c, q_ref, d.query, s[q_ref] - s[d.query], delta)
+    return decided / max(1, len(ref))
+
+
+@pytest.mark.parametrize("name", ["A", "A2"])
+def test_toy_end_to_end(name):
+    g = load_golden(name)
+    model = model_for(g)
+    image = scene_for(name, model.config)
+    fpn = D.backbone_forward(model, image)
+    l0 = fpn.levels[0]
+    assert cosine(l0, g["L0"]) > 0.9999
+    assert np.abs(l0 - g["L0"]).max() / np.abs(g["L0"]).max() < 1e-2
+    assert cosine(fpn.levels[1][g["L1_rows"]], g["L1"]) > 0.9999
+    assert cosine(fpn.levels[2][g["L2_rows"]], g["L2"]) > 0.9999
+    names = [str(n) for n in g["names"]]
+    raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
+    err_b = np.abs(raw.boxes - g["boxes"]).max()
+    err_s = np.abs(raw.score_logits - g["score_logits"]).max()
+    err_p = np.abs(raw.presence_logits - g["presence_logits"]).max()
+    print(f"{name}: box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}")
+    # toy bf16 emulation bounds are 5.2e-3 / 1.46e-2 / 1.12e-2; gate at 2x
+    assert err_b < 1.04e-2 and err_s < 2.9e-2 and err_p < 2.2e-2
+    check_decisions(g, raw, err_s)
+
+
+@pytest.mark.parametrize("name", ["A", "A2", "B", "C"])
+def test_postprocess_bit_exact_on_reference_raw(name):
+    """Contract (2): the reference's own raw outputs through the device kernel give the
+    reference's detections exactly (order, class, query, box, score, presence)."""
+    g = load_golden(name)
+    names = [str(n) for n in g["names"]]
+    raw = _Raw(g["boxes"], g["score_logits"], g["presence_logits"])
+    for key in [k for k in g if k.startswith("dets_") and not k.endswith("_cfg")]:
+        kw = json.loads(str(g[key + "_cfg"]))
+        cfg = D.PipelineConfig(cross_class_nms=key.endswith("_xc"), **kw)
+        got = dets_rows(D.postprocess(raw, names, cfg))
+        ref = g[key]
+        assert got.shape == ref.shape, key
+        np.testing.assert_array_equal(got[:, :6], ref[:, :6])
+        np.testing.assert_allclose(got[:, 6:], ref[:, 6:], rtol=1e-15, atol=0)
+
+
+def test_postprocess_kats():
+    """The reference's postprocess known-answer tests (tests/test_pipeline.py:177-213) on the GPU."""
+    lg = lambda p: float(np.log(p / (1 - p)))
+    cfg = D.PipelineConfig()
+    box = [0.5, 0.5, 0.2, 0.2]
+    d = D.postprocess(_Raw(np.array([[box, box]]), np.array([[lg(0.9), lg(0.8)]]), np.array([10.0])), ["car"], cfg)
+    assert len(d) == 1 and abs(d[0].score - 0.9) < 1e-12
+    assert D.postprocess(_Raw(np.array([[box]]), np.array([[lg(0.99)]]), np.array([-np.inf])), ["car"], cfg) == []
+    two = np.array([[[0.2, 0.2, 0.1, 0.1], [0.8, 0.8, 0.1, 0.1]]])
+    assert len(D.postprocess(_Raw(two, np.array([[lg(0.9), lg(0.8)]]), np.array([10.0])), ["car"], cfg)) == 2
+    assert D.postprocess(_Raw(np.array([[box]]), np.array([[lg(0.3)]]), np.array([10.0])), ["car"], cfg) == []
+    a, b = [0.3, 0.3, 0.2, 0.2], [0.31, 0.3, 0.2, 0.2]
+    d = D.postprocess(_Raw(np.array([[b, a]]), np.array([[lg(0.8), lg(0.8)]]), np.array([10.0])), ["car"], cfg)
+    assert len(d) == 1 and d[0].box == tuple(b)
+    bb, sc = np.array([[box], [box]]), np.array([[lg(0.9)], [lg(0.8)]])
+    assert len(D.postprocess(_Raw(bb, sc, np.array([10.0, 10.0])), ["car", "person"], cfg)) == 2
+    d = D.postprocess(_Raw(bb, sc, np.array([10.0, 10.0])), ["car", "person"],
+                      D.PipelineConfig(cross_class_nms=True))
+    assert len(d) == 1 and d[0].class_name == "car"
+    with pytest.raises(ValueError):
+        D.postprocess(_Raw(np.array([[box]]), np.array([[lg(0.9)]]), np.array([10.0])), ["car", "person"], cfg)
+
+
+def test_nms_survivors_random():
+    """Hypothesis-style property (tests/test_pipeline.py:225-239) on the device kernel,
+    checked against the oracle decision-for-decision."""
+    from oracle import dart_oracle as O
+
+    cfg = D.PipelineConfig(score_threshold=0.0)
+    for seed in range(40):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(1, 64))
+        boxes = np.column_stack([rng.uniform(0.2, 0.8, n), rng.uniform(0.2, 0.8, n), rng.uniform(0.05, 0.4, n),
+                                 rng.uniform(0.05, 0.4, n)])[None]
+        scores = rng.uniform(-3, 3, (1, n))
+        if seed % 5 == 0:
+            scores[0, : n // 2] = scores[0, 0]  # ties -> query order
+        got = D.postprocess(_Raw(boxes, scores, np.array([10.0])), ["car"], cfg)
+        ref = O.postprocess(boxes, scores, np.array([10.0]), presence_thr=cfg.presence_threshold,
+                            score_thr=cfg.score_threshold)
+        assert [d.query for d in got] == [r[1] for r in ref]
+        for i, d1 in enumerate(got):
+            for d2 in got[i + 1:]:
+                assert D.box_iou(d1.box, d2.box) < cfg.nms_iou_threshold
+
+
+def test_bad_image_rejected():
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    with pytest.raises(ValueError):
+        D.backbone_forward(model, np.full((64, 64, 3), 1.5))
+    with pytest.raises(ValueError):
+        D.backbone_forward(model, np.zeros((32, 32, 3)))
+
+
+def test_batch_independence_and_chunking():
+    """Row i of a batched run equals the N=1 run bitwise (classes never mix), and n_max
+    chunking does not change outputs (reference tests/test_model.py:176-201,
+    tests/test_acceptance.py:299-314)."""
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    image, _ = D.generate_scene(D.SceneSpec(seed=1, num_classes=3))
+    fpn = D.backbone_forward(model, image)
+    names = ["car", "person", "dog", "cat"]
+    emb = D.text_encode(model, names)
+    full = D.encdec_forward(model, fpn, emb.stack(names))
+    sub = D.encdec_forward(model, fpn, emb.stack(["person", "cat"]))
+    np.testing.assert_array_equal(sub.boxes[0], full.boxes[1])
+    np.testing.assert_array_equal(sub.score_logits[1], full.score_logits[3])
+    rev = D.encdec_forward(model, fpn, emb.stack(names[::-1]))
+    np.testing.assert_array_equal(rev.boxes, full.boxes[::-1])
+    dup = D.encdec_forward(model, fpn, emb.stack(["car", "car"]))
+    np.testing.assert_array_equal(dup.boxes[0], dup.boxes[1])
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    ref = D.run_batched(model, image, names, cfg)
+    for n_max in (1, 2, 3):
+        assert D.run_batched(model, image, names, D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0,
+                                                                      n_max=n_max)) == ref
+    assert D.run_naive(model, image, names, cfg) == ref
+    assert D.run_shared(model, image, names, cfg) == ref
+
+
+@pytest.mark.parametrize("name", ["B", "C"])
+def test_full_width_parity(name):
+    """Full-size kernels (hd 80, window 24, T 5184, d 256, hd 16, Q 200) against the reference.
+    B: 4 blocks + 6+6 enc-dec, 3 classes; C: full ViT-H/14, 4 classes."""
+    g = load_golden(name)
+    model = model_for(g)
+    image = scene_for(name, model.config)
+    assert hashlib_image(image) == str(g["image_checksum"])
+    fpn = D.backbone_forward(model, image)
+    rows = g["rows"]
+    l0 = fpn.levels[0][rows]
+    c0 = cosine(l0, g["L0"])
+    e0 = np.abs(l0 - g["L0"]).max() / np.abs(g["L0"]).max()
+    names = [str(n) for n in g["names"]]
+    raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
+    err_b = np.abs(raw.boxes - g["boxes"]).max()
+    err_s = np.abs(raw.score_logits - g["score_logits"]).max()
+    err_p = np.abs(raw.presence_logits - g["presence_logits"]).max()
+    frac = check_decisions(g, raw, err_s)
+    print(f"{name}: L0 cos {c0:.6f} rel {e0:.2e}; box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}; "
+          f"decided {frac:.2f}")
+    # SURVEY 8(c)(1) full-size bf16 emulation: cos 0.99992, |dbox| 5.1e-3, |dscore| 2.0e-2; gate at 2x
+    assert c0 > 0.9998 and e0 < 3.2e-2
+    assert err_b < 1.02e-2 and err_s < 4.0e-2 and err_p < 4.0e-2
+
+
+def hashlib_image(img):
+    import hashlib
+
+    return hashlib.blake2b(img.tobytes(), digest_size=16).hexdigest()
