@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""DART multi-class detection throughput on B200 (BASELINE.json metric: images/sec at
+1008^2 ViT-H/14 DART, N classes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--classes 4] [--batch 1] [--impl ours|reference]
+
+A step = one detection of one batch of synthetic 1008^2 scenes (SceneSpec(seed=1000+i,
+num_rects=3, noise=0.05)) against N class prompts: backbone, class-batched enc-dec,
+post-processing with gates open (presence 0, score 0: worst-case NMS work).  Weights
+are the deterministic random init of the full ViT-H/14 model (seed 0).
+
+value  = images/s over exactly K device-timed steps (CUDA events on the launch stream,
+         max over ranks), inputs resident in HBM.
+e2e    = the same through Detector.detect() with pinned host images: H2D of the images,
+         the whole path, D2H of the kept detections, inside the timed region.
+Multi-GPU (torchrun): image-batch data parallelism, one process per GPU, no collective
+on the data path ("scaling": "weak"); timing is the max over ranks.
+--impl reference: the CPU reference path (the float64 NumPy oracle port of the
+reference's algorithm) on the host cores, timed on bounded per-unit samples and
+composed additively (the reference's per-block / per-class loops are additive).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec at 1008^2 ViT-H/14 DART (N classes), 1 image per step"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def gflops_per_image(cfg, n_classes: int) -> float:
+    """Algorithmic FLOPs (2 per MAC, reference math) with the
+    class-independent prefix counted once: F(N) = F_bb + F_prefix + N * F_class."""
+    T, E, L, G, H = cfg.tokens, cfg.embed_dim, cfg.num_blocks, len(cfg.global_block_indices), cfg.num_heads
+    hd, w2, p, F = cfg.head_dim, cfg.window_size ** 2, cfg.patch_size, cfg.fpn_dims[0]
+    nw = T // w2
+    d, H2, Lt, q1, ne, nd = cfg.text_dim, cfg.num_heads, cfg.text_tokens, cfg.num_queries + 1, \
+        cfg.num_encoder_layers, cfg.num_decoder_layers
+    dh = d // H2
+    fb = 2 * T * 3 * p * p * E + L * 24 * T * E * E + (L - G) * 4 * H * nw * w2 * w2 * hd + G * 4 * H * T * T * hd
+    fb += 2 * E * F * (T + T / 4 + T / 16)
+    prefix = 2 * T * F * d + 8 * T * d * d + 4 * H2 * T * T * dh + 8 * q1 * d * d + 4 * H2 * q1 * q1 * dh
+    enc = ne * (4 * T * d * d + 4 * Lt * d * d + 4 * H2 * T * Lt * dh + 16 * T * d * d) + (ne - 1) * (
+        8 * T * d * d + 4 * H2 * T * T * dh)
+    dec = nd * (4 * q1 * d * d + 4 * T * d * d + 4 * H2 * q1 * T * dh + 16 * q1 * d * d) + (nd - 1) * (
+        8 * q1 * d * d + 4 * H2 * q1 * q1 * dh)
+    heads = 2 * cfg.num_queries * d * 5 + 2 * d
+    return (fb + prefix + n_classes * (enc + dec + heads)) / 1e9
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def coco80():
+    return ["person", "bicycle", "car", "motorcycle", "airplane", "bus", "train", "truck", "boat", "traffic light",
+            "fire hydrant", "stop sign", "parking meter", "bench", "bird", "cat", "dog", "horse", "sheep", "cow",
+            "elephant", "bear", "zebra", "giraffe", "backpack", "umbrella", "handbag", "tie", "suitcase", "frisbee",
+            "skis", "snowboard", "sports ball", "kite", "baseball bat", "baseball glove", "skateboard", "surfboard",
+            "tennis racket", "bottle", "wine glass", "cup", "fork", "knife", "spoon", "bowl", "banana", "apple",
+            "sandwich", "orange", "broccoli", "carrot", "hot dog", "pizza", "donut", "cake", "chair", "couch",
+            "potted plant", "bed", "dining table", "toilet", "tv", "laptop", "mouse", "remote", "keyboard",
+            "cell phone", "microwave", "oven", "toaster", "sink", "refrigerator", "book", "clock", "vase",
+            "scissors", "teddy bear", "hair drier", "toothbrush"]
+
+
+def class_names(n: int):
+    base = ["person", "car", "dog", "bicycle"]
+    if n <= 4:
+        return base[:n]
+    return coco80()[:n] if n <= 80 else [f"class{i:02d}" for i in range(n)]
+
+
+# ============================================================================ CPU reference arm
+
+def cpu_reference_units(cfg, n_classes: int, budget_s: float, log=None):
+    """Time the oracle port (float64 NumPy, all BLAS threads) per additive unit of the
+    reference's loops and compose seconds/image:
+        t = t_patch + (L-G) t_windowed_block + G t_global_block + t_fpn + t_prefix
+            + N (t_enc_layer * ne + t_dec_layer * nd)
+    Each unit is measured once (the global block and encoder layer dominate)."""
+    from oracle import dart_oracle as O
+
+    ocfg = O.full_config()
+    rng = np.random.default_rng(0)
+    units = {}
+
+    def timed(name, fn):
+        t0 = time.perf_counter()
+        fn()
+        units[name] = time.perf_counter() - t0
+        if log:
+            log(f"[cpu] {name}: {units[name]:.2f}s")
+
+    # weights only for the blocks/layers sampled (same shapes and init as the full model)
+    decl = {p: (s, i) for p, s, i in O.param_declaration(ocfg)}
+    P = {}
+
+    def need(prefix):
+        for p, (s, i) in decl.items():
+            if p.startswith(prefix) and p not in P:
+                if i == "ones":
+                    P[p] = np.ones(s)
+                elif i == "zeros":
+                    P[p] = np.zeros(s)
+                elif i in ("rope_cos", "rope_sin"):
+                    c, sn = O.rope_tables(ocfg)
+                    P["rope.cos"], P["rope.sin"] = c, sn
+                else:
+                    P[p] = O.philox_uniform(0, p, s, int(i))
+
+    need("rope")
+    need("patch_embed")
+    image, _ = O.scene(1000, 1008, num_classes=4)
+    x = None
+
+    def patch():
+        nonlocal x
+        x = O.linear(P, O.patchify(ocfg, image), "patch_embed")
+
+    timed("patch_embed", patch)
+    need("backbone.block0.")
+    timed("windowed_block", lambda: O.backbone_block(P, ocfg, x, 0))
+    need("backbone.block7.")
+    timed("global_block", lambda: O.backbone_block(P, ocfg, x, 7))
+    need("fpn.")
+    timed("fpn", lambda: O.fpn(P, ocfg, x))
+    need("encdec.")
+    need("encoder.")
+    need("decoder.")
+    need("text.")
+    l0 = rng.standard_normal((ocfg.tokens, 256)) * 0.5
+    e = None
+
+    def prefix():
+        nonlocal e
+        e = O.encoder_prefix(P, ocfg, l0)
+
+    timed("encdec_prefix", prefix)
+    text = O.text_embedding(P, ocfg, "person")
+
+    def enc_layer():
+        p = "encoder.layer1"
+        h = O._ln(P, e, f"{p}.ln1")
+        e2 = e + O.mha(P, ocfg, h, h, f"{p}.self")
+        e2 = e2 + O.mha(P, ocfg, O._ln(P, e2, f"{p}.ln2"), text, f"{p}.cross")
+        return e2 + O.mlp(P, O._ln(P, e2, f"{p}.ln3"), f"{p}.mlp")
+
+    timed("encoder_layer", enc_layer)
+
+    def dec_layer():
+        q = np.concatenate([P["decoder.queries"], P["decoder.presence_token"]])
+        p = "decoder.layer1"
+        h = O._ln(P, q, f"{p}.ln1")
+        q = q + O.mha(P, ocfg, h, h, f"{p}.self")
+        q = q + O.mha(P, ocfg, O._ln(P, q, f"{p}.ln2"), e, f"{p}.cross")
+        return q + O.mlp(P, O._ln(P, q, f"{p}.ln3"), f"{p}.mlp")
+
+    timed("decoder_layer", dec_layer)
+    L, G = cfg.num_blocks, len(cfg.global_block_indices)
+    per_image = (units["patch_embed"] + (L - G) * units["windowed_block"] + G * units["global_block"] + units["fpn"]
+                 + units["encdec_prefix"] + n_classes * (cfg.num_encoder_layers * units["encoder_layer"]
+                                                          + cfg.num_decoder_layers * units["decoder_layer"]))
+    sample = ("oracle port (float64 NumPy) timed per unit at full size: patch-embed, 1 windowed block, 1 global "
+              "block, FPN, enc-dec prefix, 1 encoder layer + 1 decoder layer for 1 class; composed additively as "
+              f"(L-G)*win + G*glob + N*(6*enc + 6*dec) for L={L}, G={G}, N={n_classes}")
+    return per_image, units, sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2603_11441_b200 as D
+
+    cfg = D.vit_h_config()
+    t0 = time.perf_counter()
+    per_image, units, sample = cpu_reference_units(cfg, args.classes, budget_s=240,
+                                                   log=lambda s: print(s, file=sys.stderr))
+    value = 1.0 / per_image
+    line = {
+        "impl": "reference", "metric": METRIC.replace("N classes", f"N={args.classes} classes"), "value": value,
+        "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_image * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SceneSpec seed 1000, random-init ViT-H/14 weights seed 0)",
+        "config": {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {args.batch}",
+                   "classes": args.classes, "batch": args.batch},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": sample, "units_s": units},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ============================================================================ B200 arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_11441_b200 as D
+    from paper_2603_11441_b200 import _native
+    from paper_2603_11441_b200.detector import Detector
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    log = (lambda s: print(s, file=sys.stderr, flush=True)) if rank == 0 else (lambda s: None)
+
+    cfg = D.vit_h_config(seed=0)
+    t0 = time.perf_counter()
+    model = D.build_model(cfg, with_mask_head=False)
+    log(f"[bench] build_model {time.perf_counter() - t0:.1f}s")
+    names = class_names(args.classes)
+    pcfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    t0 = time.perf_counter()
+    det = Detector(model, names, pcfg, device=dev)
+    log(f"[bench] weight upload {time.perf_counter() - t0:.1f}s")
+
+    B = args.batch
+    n_imgs = max(2, min(8, args.steps + args.warmup))
+    pool = [np.stack([D.generate_scene(D.SceneSpec(seed=1000 + rank * 100000 + i * B + j, image_size=1008,
+                                                   num_rects=3, noise=0.05, num_classes=4))[0]
+                      for j in range(B)]).astype(np.float32) for i in range(n_imgs)]
+    dev_pool = [torch.from_numpy(p).to(dev) for p in pool]
+    host_pool = [torch.from_numpy(p).pin_memory() for p in pool]
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident throughput (value)
+    for i in range(args.warmup):
+        det.detect_device(dev_pool[i % n_imgs])
+    barrier()
+    det.reset_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            det.detect_device(dev_pool[i % n_imgs])
+        ev1.record(stream)
+        barrier()
+    launches = det.launch_count()
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms)
+    imgs = args.steps * B * world
+    value = imgs / (ms / 1000.0)
+    res = det.result_tensors(det._buffers(B))
+    kept = int(res["kc"].sum().item())
+
+    # ---------------- end to end through Detector.detect (pinned host images, D2H results)
+    for i in range(max(1, args.warmup)):
+        det.detect(host_pool[i % n_imgs])
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        out = det.detect(host_pool[i % n_imgs])
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = imgs / (e2e_ms / 1000.0)
+    h2d = B * cfg.image_size * cfg.image_size * 3 * 4
+    d2h = det.d2h_bytes(B)
+
+    # ---------------- dominant-kernel roofline: backbone MLP fc1 GEMM (tcgen05), live CUDA events
+    roof = kernel_roofline(det, model, cfg, dev, args)
+
+    pk, pk_kind = load_peaks()
+    gf = gflops_per_image(cfg, args.classes)
+    step_tflops = gf * imgs / (ms / 1000.0) / 1000.0 / world
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            per_image, units, sample = cpu_reference_units(cfg, args.classes, budget_s=60, log=log)
+            cpu = {"value": 1.0 / per_image, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": sample, "units_s": units}
+        line = {
+            "metric": METRIC.replace("N classes", f"N={args.classes} classes"), "value": value, "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp16 operands, fp32 accumulate/residual, fp64 post-processing",
+            "data": "synthetic (SceneSpec seed 1000+i, random-init ViT-H/14 weights seed 0)",
+            "config": {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {B} per GPU",
+                       "classes": args.classes, "batch_per_gpu": B, "parallelism": f"image-dp{world}",
+                       "thresholds": "presence 0, score 0 (gates open)",
+                       "l2": "working set > L2 (1.29 GB fp16 weights streamed per step; 8-image input pool)"},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "step_roofline": {"bound": "tensor", "gflop_per_image": gf, "achieved_tflops": step_tflops,
+                              "peak_tflops": pk["bf16_tflops_sustained"], "peak_kind": f"{pk_kind} sustained",
+                              "frac": step_tflops / pk["bf16_tflops_sustained"]},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "kept_detections_last_step": kept,
+            "detections_e2e_last": len(out),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def kernel_roofline(det, model, cfg, dev, args):
+    """Time the backbone MLP fc1 GEMM ([B*T, E] x [E, 4E], the largest single tcgen05 launch
+    shape) on the launching stream with CUDA events; achieved = 2*M*N*K / mean duration."""
+    import torch
+    from paper_2603_11441_b200 import _native
+
+    pk, pk_kind = load_peaks()
+    lib = _native.load()
+    M, K, N = args.batch * cfg.tokens, cfg.embed_dim, 4 * cfg.embed_dim
+    A = torch.randn(M, K, device=dev).half()
+    W = (torch.randn(N, K, device=dev) / K ** 0.5).half()
+    bias = torch.zeros(N, device=dev)
+    out = torch.empty(M, N, device=dev, dtype=torch.float16)
+    st = torch.cuda.current_stream(dev)
+    call = lambda: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None,
+                                               M, N, K, 1, None, None, 0, 0, 0, st.cuda_stream))
+    for _ in range(5):
+        call()
+    torch.cuda.synchronize(dev)
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        call()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / reps / 1000.0
+    achieved = 2.0 * M * N * K / t / 1e12
+    peak = pk["bf16_tflops"]
+    return {"kernel": "gemm_tc_kernel<256,4,EPI_F16_RELU> (backbone mlp.fc1)", "bound": "tensor",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_kind": f"{pk_kind} burst bf16/fp16 dense", "flop_per_launch": 2.0 * M * N * K,
+            "us_per_launch": t * 1e6, "traffic": None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--classes", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

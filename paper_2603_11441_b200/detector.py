@@ -1,0 +1,184 @@
+"""High-throughput detector: the `detect(images, class_names) -> boxes/scores/labels`
+entry point of the north_star, built on the same C ABI as the drop-in functions.
+
+One `Detector` binds a model, a fixed class list and a post-processing config to one
+GPU.  Device buffers for the backbone levels, the raw enc-dec outputs and the
+post-processing results are allocated once per batch size; text embeddings of the class
+list are resident on the device.  `detect_device` is fully asynchronous (no host sync);
+`detect` adds the pinned host->device image copy, one synchronisation and the
+device->host copy of the kept detections.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .model import DetectorModel, _device, _stream_ptr, native_handle, raise_for_flags, text_encode
+from .pipeline import Detection, PipelineConfig, _require_classes
+
+
+class Detector:
+    def __init__(self, model: DetectorModel, class_names: list[str], cfg: PipelineConfig | None = None,
+                 device=None):
+        import torch
+
+        _require_classes(class_names)
+        self.model = model
+        self.cfg = cfg or PipelineConfig()
+        if self.cfg.n_max is not None and self.cfg.n_max < len(class_names):
+            self.chunks = [class_names[i: i + self.cfg.n_max] for i in range(0, len(class_names), self.cfg.n_max)]
+        else:
+            self.chunks = [list(class_names)]
+        self.class_names = list(class_names)
+        self.device = device or _device()
+        self.handle = native_handle(model, self.device)
+        self.lib = self.handle.lib
+        emb = text_encode(model, self.class_names)
+        self.text = [torch.from_numpy(np.stack(emb.stack(ch)).astype(np.float32)).to(self.device)
+                     for ch in self.chunks]
+        self._bufs = {}
+
+    # ------------------------------------------------------------------ buffers
+    def _buffers(self, B: int):
+        import torch
+
+        b = self._bufs.get(B)
+        if b is not None:
+            return b
+        cfg, dev = self.model.config, self.device
+        T, g, Q, N = cfg.tokens, cfg.grid, cfg.num_queries, len(self.class_names)
+        f64, f32, i32 = torch.float64, torch.float32, torch.int32
+        b = {
+            "l0": torch.empty((B, T, cfg.fpn_dims[0]), device=dev, dtype=f32),
+            "l1": torch.empty((B, (g // 2) ** 2, cfg.fpn_dims[1]), device=dev, dtype=f32),
+            "l2": torch.empty((B, (g // 4) ** 2, cfg.fpn_dims[2]), device=dev, dtype=f32),
+            "flags": torch.zeros((1,), device=dev, dtype=i32),
+            "boxes": torch.empty((B, N, Q, 4), device=dev, dtype=f64),
+            "scores": torch.empty((B, N, Q), device=dev, dtype=f64),
+            "presence": torch.empty((B, N), device=dev, dtype=f64),
+            # post-processing outputs, packed so one D2H copy brings everything back
+            "kc": torch.empty((B * N,), device=dev, dtype=i32),
+            "kq": torch.empty((B * N, Q), device=dev, dtype=i32),
+            "ks": torch.empty((B * N, Q), device=dev, dtype=f64),
+            "pp": torch.empty((B * N,), device=dev, dtype=f64),
+            "kf": torch.zeros((B * N, Q), device=dev, dtype=i32),
+            "scratch": torch.empty((N * (2 * Q + 1) + 1,), device=dev, dtype=i32),
+            "img": torch.empty((B, cfg.image_size, cfg.image_size, 3), device=dev, dtype=f32),
+        }
+        b["host_img"] = torch.empty((B, cfg.image_size, cfg.image_size, 3), dtype=f32, pin_memory=True)
+        self._bufs[B] = b
+        return b
+
+    # ------------------------------------------------------------------ device path
+    def detect_device(self, images):
+        """images: device float32 [B, S, S, 3].  Enqueues backbone, class-batched enc-dec and
+        post-processing on the current stream; returns the buffer dict (no sync)."""
+        B = int(images.shape[0])
+        b = self._buffers(B)
+        h, lib, st = self.handle, self.lib, _stream_ptr(self.device)
+        N, Q = len(self.class_names), self.model.config.num_queries
+        b["flags"].zero_()
+        _native.check(lib.dart_backbone(h.ptr, images.data_ptr(), B, b["l0"].data_ptr(), b["l1"].data_ptr(),
+                                        b["l2"].data_ptr(), b["flags"].data_ptr(), st))
+        off = 0
+        for ci, ch in enumerate(self.chunks):
+            n = len(ch)
+            if len(self.chunks) == 1:
+                bx, sc, pr = b["boxes"], b["scores"], b["presence"]
+            else:  # chunked: decode into per-chunk slices of a [B, N] layout via a temp
+                bx = b.setdefault(f"boxes{ci}", b["boxes"].new_empty((B, n, Q, 4)))
+                sc = b.setdefault(f"scores{ci}", b["scores"].new_empty((B, n, Q)))
+                pr = b.setdefault(f"presence{ci}", b["presence"].new_empty((B, n)))
+            _native.check(lib.dart_encdec(h.ptr, None, B, self.text[ci].data_ptr(), n, bx.data_ptr(), sc.data_ptr(),
+                                          pr.data_ptr(), None, st))
+            if len(self.chunks) > 1:
+                b["boxes"][:, off: off + n].copy_(bx)
+                b["scores"][:, off: off + n].copy_(sc)
+                b["presence"][:, off: off + n].copy_(pr)
+            off += n
+        c = self.cfg
+        xc = int(c.cross_class_nms)
+        if xc and B > 1:
+            for i in range(B):  # cross-class NMS is per image
+                sl = slice(i * N, (i + 1) * N)
+                _native.check(lib.dart_postprocess(
+                    h.ptr, b["boxes"][i].data_ptr(), b["scores"][i].data_ptr(), b["presence"][i].data_ptr(), N, Q,
+                    c.presence_threshold, c.score_threshold, c.nms_iou_threshold, 1, b["kc"][sl].data_ptr(),
+                    b["kq"][sl].data_ptr(), b["ks"][sl].data_ptr(), b["pp"][sl].data_ptr(), b["kf"][sl].data_ptr(),
+                    b["scratch"].data_ptr(), st))
+        else:
+            _native.check(lib.dart_postprocess(
+                h.ptr, b["boxes"].data_ptr(), b["scores"].data_ptr(), b["presence"].data_ptr(), B * N, Q,
+                c.presence_threshold, c.score_threshold, c.nms_iou_threshold, xc, b["kc"].data_ptr(),
+                b["kq"].data_ptr(), b["ks"].data_ptr(), b["pp"].data_ptr(), b["kf"].data_ptr(),
+                b["scratch"].data_ptr(), st))
+        return b
+
+    def result_tensors(self, b):
+        keys = ["flags", "kc", "kq", "ks", "pp", "boxes"] + (["kf"] if self.cfg.cross_class_nms else [])
+        return {k: b[k] for k in keys}
+
+    def d2h_bytes(self, B: int) -> int:
+        b = self._buffers(B)
+        return sum(t.numel() * t.element_size() for t in self.result_tensors(b).values())
+
+    # ------------------------------------------------------------------ host API
+    def detect(self, images) -> list[list[Detection]]:
+        """images: [B, S, S, 3] or [S, S, 3] in [0, 1] (NumPy or pinned/host torch).  Returns
+        one detection list per image, in the reference's order (class order, then NMS order)."""
+        import torch
+
+        arr = images
+        single = False
+        if isinstance(arr, np.ndarray):
+            if arr.ndim == 3:
+                arr, single = arr[None], True
+        elif arr.ndim == 3:
+            arr, single = arr.unsqueeze(0), True
+        S = self.model.config.image_size
+        if tuple(arr.shape[1:]) != (S, S, 3):
+            raise ValueError(f"image shape {tuple(arr.shape)} does not match {(S, S, 3)}")
+        B = int(arr.shape[0])
+        b = self._buffers(B)
+        if isinstance(arr, np.ndarray):
+            b["host_img"].numpy()[...] = arr
+            src = b["host_img"]
+        else:
+            src = arr
+        if src.is_cuda:
+            b["img"].copy_(src)
+        else:
+            b["img"].copy_(src, non_blocking=True)
+        self.detect_device(b["img"])
+        host = {k: v.cpu() for k, v in self.result_tensors(b).items()}  # synchronises
+        raise_for_flags(int(host["flags"][0]))
+        out = self.unpack(host, B)
+        return out[0] if single else out
+
+    def unpack(self, host, B: int) -> list[list[Detection]]:
+        N = len(self.class_names)
+        kc, kq, ks, pp = (host[k].numpy() for k in ("kc", "kq", "ks", "pp"))
+        boxes = host["boxes"].numpy().reshape(B * N, -1, 4)
+        kf = host["kf"].numpy() if "kf" in host else None
+        res = []
+        for i in range(B):
+            dets = []
+            for c, name in enumerate(self.class_names):
+                it = i * N + c
+                for k in range(int(kc[it])):
+                    if kf is not None and not kf[it, k]:
+                        continue
+                    q = int(kq[it, k])
+                    dets.append(Detection(c, name, tuple(float(v) for v in boxes[it, q]), float(ks[it, k]),
+                                          float(pp[it]), q))
+            res.append(dets)
+        return res
+
+    def launch_count(self) -> int:
+        return int(self.lib.dart_launch_count(self.handle.ptr))
+
+    def reset_launch_count(self) -> None:
+        self.lib.dart_reset_launch_count(self.handle.ptr)
