@@ -71,14 +71,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) flash_attn_kernel(AttnArgs a) {
   load_kv(0, 0);
   cp_async_commit();
 
+  // V pad columns [HD, HD+8) hold ones: the extra PV n-tile then accumulates the softmax
+  // row sum on the tensor core (no per-element FADD), consistent with the fp16 P used for O.
+  for (int idx = tid; idx < 2 * BKV; idx += WARPS * 32) {
+    const int b = idx / BKV, r = idx % BKV;
+    *reinterpret_cast<uint4*>(&sV[b][r * PITCH + HD]) = make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
+  }
+
   const int nkt = (a.Lk + BKV - 1) / BKV;
   uint32_t qf[KSTEPS][4];
-  float o[NT_O][4];
+  float o[NT_O + 1][4];
 #pragma unroll
-  for (int n = 0; n < NT_O; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY};
-  float l_r[2] = {0.f, 0.f};
-  const int g = lane >> 2, t = lane & 3;
+  for (int n = 0; n <= NT_O; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY};  // running max of raw scores
+  const float c = a.scale_log2;            // exp(s/sqrt(hd) - m) = exp2(s*c - m*c)
+  const int t = lane & 3;
 
   for (int kt = 0; kt < nkt; ++kt) {
     const int buf = kt & 1;
@@ -94,7 +101,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) flash_attn_kernel(AttnArgs a) {
         ldmatrix_x4(qf[ks], smem_u32(&sQ[row * PITCH + col]));
       }
     }
-    // ---- S = Q K^T (16 x 64 per warp)
+    // ---- S = Q K^T (16 x 64 per warp, raw scores)
     float s[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
@@ -110,76 +117,70 @@ __global__ void __launch_bounds__(WARPS * 32, 1) flash_attn_kernel(AttnArgs a) {
         mma16816(s[2 * np + 1], qf[ks], b + 2);
       }
     }
-    // ---- online softmax (log2 domain)
     const int kbase = kt * BKV;
-    float mx[2] = {-INFINITY, -INFINITY};
+    if (kbase + BKV > a.Lk) {  // partial tile only
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
+      for (int n = 0; n < 8; ++n)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kbase + n * 8 + 2 * t + (e & 1);
-        float v = s[n][e] * a.scale_log2;
-        v = key < a.Lk ? v : -INFINITY;
-        s[n][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
+        for (int e = 0; e < 4; ++e)
+          if (kbase + n * 8 + 2 * t + (e & 1) >= a.Lk) s[n][e] = -INFINITY;
     }
-    float corr[2];
+    // ---- online softmax
+    float mx0 = fmax3f(s[0][0], s[0][1], m_r[0]);
+    float mx1 = fmax3f(s[0][2], s[0][3], m_r[1]);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 2));
-      const float m_new = fmaxf(m_r[r], mx[r]);
-      const float m_use = m_new == -INFINITY ? 0.f : m_new;
-      corr[r] = fast_exp2(m_r[r] - m_use);
-      m_r[r] = m_new;
-      mx[r] = m_use;
+    for (int n = 1; n < 8; ++n) {
+      mx0 = fmax3f(mx0, s[n][0], s[n][1]);
+      mx1 = fmax3f(mx1, s[n][2], s[n][3]);
     }
-    float rs[2] = {0.f, 0.f};
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, 2));
+    const float corr0 = fast_exp2((m_r[0] - mx0) * c);
+    const float corr1 = fast_exp2((m_r[1] - mx1) * c);
+    m_r[0] = mx0;
+    m_r[1] = mx1;
+    const float nb0 = -mx0 * c, nb1 = -mx1 * c;
     uint32_t p[4][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-      const float p0 = fast_exp2(s[n][0] - mx[0]);
-      const float p1 = fast_exp2(s[n][1] - mx[0]);
-      const float p2 = fast_exp2(s[n][2] - mx[1]);
-      const float p3 = fast_exp2(s[n][3] - mx[1]);
-      rs[0] += p0 + p1;
-      rs[1] += p2 + p3;
+      const float p0 = fast_exp2(fmaf(s[n][0], c, nb0));
+      const float p1 = fast_exp2(fmaf(s[n][1], c, nb0));
+      const float p2 = fast_exp2(fmaf(s[n][2], c, nb1));
+      const float p3 = fast_exp2(fmaf(s[n][3], c, nb1));
       p[n >> 1][(n & 1) * 2 + 0] = pack_half2(p0, p1);
       p[n >> 1][(n & 1) * 2 + 1] = pack_half2(p2, p3);
     }
-    l_r[0] = l_r[0] * corr[0] + rs[0];
-    l_r[1] = l_r[1] * corr[1] + rs[1];
 #pragma unroll
-    for (int n = 0; n < NT_O; ++n) {
-      o[n][0] *= corr[0];
-      o[n][1] *= corr[0];
-      o[n][2] *= corr[1];
-      o[n][3] *= corr[1];
+    for (int n = 0; n <= NT_O; ++n) {
+      o[n][0] *= corr0;
+      o[n][1] *= corr0;
+      o[n][2] *= corr1;
+      o[n][3] *= corr1;
     }
-    // ---- O += P V
+    // ---- O += P [V | 1]
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       uint32_t pa[4] = {p[ks][0], p[ks][1], p[ks][2], p[ks][3]};
+      const int key = ks * 16 + (lane & 15);
 #pragma unroll
       for (int np = 0; np < NT_O / 2; ++np) {
         uint32_t b[4];
-        const int key = ks * 16 + (lane & 15);
         const int dim = np * 16 + (lane >> 4) * 8;
         ldmatrix_x4_trans(b, smem_u32(&sV[buf][key * PITCH + dim]));
         mma16816(o[2 * np], pa, b);
         mma16816(o[2 * np + 1], pa, b + 2);
       }
+      uint32_t b1[2];
+      ldmatrix_x2_trans(b1, smem_u32(&sV[buf][key * PITCH + HD]));
+      mma16816(o[NT_O], pa, b1);
     }
     __syncthreads();
   }
-  // ---- normalise and store
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 1);
-    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 2);
-  }
-  const float inv0 = 1.f / l_r[0], inv1 = 1.f / l_r[1];
+  // ---- normalise by the tensor-core row sum and store
+  const int g = lane >> 2;
+  const float inv0 = 1.f / o[NT_O][0], inv1 = 1.f / o[NT_O][2];
   __half* ob = a.o + (long long)h * a.head_stride_o;
   const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
   if (r0 < a.Lq) {

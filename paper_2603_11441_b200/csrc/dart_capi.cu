@@ -74,8 +74,9 @@ struct GemmW {
   __half* w = nullptr;  // [N, K] fp16
   float* b = nullptr;   // [N]
   int N = 0, K = 0;
-  CUtensorMap tmap;
+  CUtensorMap tmap[3];  // box rows 256 / 128 / 64 (index = bn_slot(BN)), built where N allows
 };
+inline int bn_slot(int bn) { return bn == 256 ? 0 : bn == 128 ? 1 : 2; }
 struct LNW {
   float* g = nullptr;
   float* b = nullptr;
@@ -194,7 +195,13 @@ bool upload_wT(dart_model* m, const float* h, int in, int out, __half* dst, int 
 }
 
 bool finish_gemmw(GemmW& g) {
-  return make_tmap(&g.tmap, g.w, g.K, g.N, g.K, gemm_bn_for(g.N));
+  bool any = false;
+  for (int bn = 256; bn >= 64; bn >>= 1) {
+    if (g.N % bn) continue;
+    if (!make_tmap(&g.tmap[bn_slot(bn)], g.w, g.K, g.N, g.K, bn)) return false;
+    any = true;
+  }
+  return any;
 }
 
 struct WeightCursor {
@@ -276,7 +283,8 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
   if (!make_tmap(&ta, A, W.K, M, lda, 128)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (A)");
   if (e.bias == nullptr) e.bias = W.b;
   m->launches++;
-  int rc = gemm_tc(ta, W.tmap, M, W.N, W.K, epi, e, m->num_sms, s);
+  const int bn = gemm_pick_bn(M, W.N, m->num_sms);
+  int rc = gemm_tc(ta, W.tmap[bn_slot(bn)], M, W.N, W.K, bn, epi, e, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
 }
@@ -750,8 +758,12 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
               int32_t rope_cols, void* stream) {
   if (!A || !W || !out || M <= 0 || K % 64 || gemm_bn_for(N) == 0 || epi < 0 || epi > 5)
     return fail(DART_ERR_INVALID, "dart_gemm: bad args");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int bn = gemm_pick_bn(M, N, sms);
   CUtensorMap ta, tb;
-  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, gemm_bn_for(N)))
+  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, bn))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   GemmEpi e;
   e.bias = bias;
@@ -764,10 +776,7 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.rope_T = rope_T > 0 ? rope_T : 1;
   e.rope_hd = rope_hd > 0 ? rope_hd : 2;
   e.rope_cols = rope_cols;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int rc = gemm_tc(ta, tb, M, N, K, epi, e, sms, (cudaStream_t)stream);
+  int rc = gemm_tc(ta, tb, M, N, K, bn, epi, e, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }

@@ -260,11 +260,30 @@ int gemm_bn_for(int N) {
   return 0;
 }
 
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int epi_mode, const GemmEpi& epi,
-            int num_sms, cudaStream_t stream) {
+// Tile width minimising wave-quantised work: cost = waves(tiles / SMs) * (BN + 32), where the
+// +32 charges per-tile fixed cost (epilogue drain, A re-reads).  E.g. M=5184, N=1280 picks 128
+// (410 tiles = 2.8 waves) over 256 (205 tiles = 1.4 waves).
+int gemm_pick_bn(int M, int N, int num_sms) {
+  int best = 0;
+  long long best_cost = 0;
+  for (int bn = 256; bn >= 64; bn >>= 1) {
+    if (N % bn) continue;
+    const long long tiles = (long long)((M + BM - 1) / BM) * (N / bn);
+    const long long waves = (tiles + num_sms - 1) / num_sms;
+    const long long cost = waves * (bn + 32);
+    if (best == 0 || cost < best_cost) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int BN, int epi_mode,
+            const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (M <= 0) return 0;
-  if (K % BK != 0) return (int)cudaErrorInvalidValue;
-  switch (gemm_bn_for(N)) {
+  if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
+  switch (BN) {
     case 256: return dispatch_epi<256, 4>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
     case 128: return dispatch_epi<128, 6>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
     case 64: return dispatch_epi<64, 8>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);

@@ -30,8 +30,10 @@ struct GemmEpi {
 };
 
 int gemm_bn_for(int N);
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int epi_mode, const GemmEpi& epi,
-            int num_sms, cudaStream_t stream);
+int gemm_pick_bn(int M, int N, int num_sms);
+// tB must be a tensor map over W [N, K] with box {64, BN}.
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int BN, int epi_mode,
+            const GemmEpi& epi, int num_sms, cudaStream_t stream);
 
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {
