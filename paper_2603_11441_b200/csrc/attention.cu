@@ -28,7 +28,7 @@ __device__ __forceinline__ long long tok_offset(int z, int i, long long batch_st
 }
 
 template <int HD, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1) flash_attn_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, HD == 16 ? 6 : 1) flash_attn_kernel(AttnArgs a) {
   constexpr int BQ = 16 * WARPS;
   constexpr int PITCH = HD + 8;  // halves; breaks ldmatrix bank conflicts
   constexpr int CH = HD / 8;     // 16-byte chunks per row
