@@ -1,0 +1,111 @@
+"""World-size-2 gloo tests of the multi-GPU protocols (CPU): class sharding with the
+feature all-gather and raw-output all-gather, and image-DP result gathering.  The
+oracle stands in for the CUDA engine, so the collective flow and the merge order are
+checked against a single-process run of the same oracle."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_11441_b200.distributed import ClassShardPlan, detect_class_sharded, gather_detections, shard_images
+
+
+class OracleEngine:
+    def __init__(self):
+        from oracle import dart_oracle as O
+
+        self.O = O
+        self.cfg = O.OracleConfig()
+        self.P = O.build_params(self.cfg)
+        self.num_queries = self.cfg.num_queries
+
+    def backbone(self, images):
+        l0, _, _ = self.O.backbone(self.P, self.cfg, images[0].numpy())
+        return torch.from_numpy(l0)[None]
+
+    def decode(self, l0, names):
+        texts = [self.O.text_embedding(self.P, self.cfg, n) for n in names]
+        outs = [self.O.encdec(self.P, self.cfg, l0[w].numpy(), texts) for w in range(l0.shape[0])]
+        boxes = torch.from_numpy(np.stack([o[1] for o in outs]))
+        scores = torch.from_numpy(np.stack([o[3] for o in outs]))
+        pres = torch.from_numpy(np.stack([o[2] for o in outs]))
+        return boxes, scores, pres
+
+    def postprocess(self, boxes, scores, presence, names, cfg):
+        return self.O.postprocess(boxes.numpy(), scores.numpy(), presence.numpy(), presence_thr=cfg["p"],
+                                  score_thr=cfg["s"], cross_class=cfg["x"])
+
+
+NAMES = ["car", "person", "dog", "cat", "bus"]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import dart_oracle as O
+
+        eng = OracleEngine()
+        img, _ = O.scene(100 + rank, 64, num_classes=3)
+        res = {}
+        for xc in (False, True):
+            cfg = {"p": 0.0, "s": 0.0, "x": xc}
+            res[xc] = detect_class_sharded(eng, torch.from_numpy(img)[None], NAMES, cfg)
+        mine = {i: f"img{i}@{rank}" for i in shard_images(5, rank, world)}
+        merged = gather_detections(mine)
+        q.put((rank, res, merged))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_class_sharded_matches_single_process():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict((r, (res, merged)) for r, res, merged in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import dart_oracle as O
+
+    eng = OracleEngine()
+    for rank in range(world):
+        img, _ = O.scene(100 + rank, 64, num_classes=3)
+        for xc in (False, True):
+            ref = O.run_detect(eng.P, eng.cfg, img, NAMES, presence_thr=0.0, score_thr=0.0, cross_class=xc)
+            out = got[rank][0][xc]
+            assert [(c, q) for c, q, *_ in out] == [(c, q) for c, q, *_ in ref]
+            for a, b in zip(out, ref):
+                np.testing.assert_allclose(a[2], b[2], rtol=1e-12)
+                assert abs(a[3] - b[3]) < 1e-12
+    assert got[0][1] == {0: "img0@0", 1: "img1@1", 2: "img2@0", 3: "img3@1", 4: "img4@0"}
+    assert got[1][1] is None
+
+
+def test_shard_plan_covers_all_classes():
+    for n in (1, 3, 4, 80, 81):
+        for w in (1, 2, 3, 8):
+            plan = ClassShardPlan(n, w)
+            covered = []
+            for r in range(w):
+                s, e = plan.bounds(r)
+                assert 0 <= e - s <= plan.width
+                covered.extend(range(s, e))
+            assert covered == list(range(n))
