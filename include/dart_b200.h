@@ -106,6 +106,11 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
                    int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,
                    int32_t grid, void* stream);
 
+/* tcgen05/TMEM flash attention on a packed QKV buffer [items * L, 3 * heads * hd] fp16 (q | k | v
+ * column blocks, head-major inside each), o [items * L, heads * hd] fp16.  hd = 80, L % 192 == 0
+ * (the backbone's windowed and global attention, model.py:390-409). */
+int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd, void* stream);
+
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */
 int64_t dart_launch_count(const dart_model* m);

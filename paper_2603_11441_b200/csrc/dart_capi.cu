@@ -58,16 +58,54 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D fp16 tensor map over [rows, inner] with row stride `ld` elements, 128B swizzle.
-bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+bool make_tmap_ex(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_inner,
+                  uint32_t box_rows, CUtensorMapSwizzle swz) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, rows};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  return make_tmap_ex(m, ptr, inner, rows, ld, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Attention implementation switch for A/B tests: DART_ATTN_IMPL=mma forces the mma.sync kernel.
+bool tc_attention_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DART_ATTN_IMPL");
+    v = (e && strcmp(e, "mma") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Backbone self-attention on a packed QKV buffer [items * L, 3E] (q | k | v column blocks,
+// head-major), tcgen05 kernel.
+int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, int hd, int E, int num_sms,
+                   cudaStream_t s) {
+  CUtensorMap tq, tkv;
+  const uint64_t rows = (uint64_t)items * L;
+  if (!make_tmap_ex(&tq, qkv, 3 * E, rows, 3 * E, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !make_tmap_ex(&tkv, qkv, 3 * E, rows, 3 * E, 16, 192, CU_TENSOR_MAP_SWIZZLE_32B))
+    return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (attention)");
+  AttnTcArgs a;
+  a.L = L;
+  a.heads = heads;
+  a.items = items;
+  a.q_col = 0;
+  a.k_col = E;
+  a.v_col = 2 * E;
+  a.o = o;
+  a.o_ld = E;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+  int rc = attention_tc(tq, tkv, a, num_sms, s);
+  if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
+  return 0;
 }
 
 struct GemmW {
@@ -581,9 +619,12 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
   const int rows = B * T;
   auto& w = m->bb;
   // patch embedding (im2col fused with the [0,1] range check) + GEMM
-  LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, flags, s));
-  RUN(gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(w.x, E), s));
+  // The residual stream is kept in window-major row order (windows = contiguous 576-row
+  // blocks); global attention, LayerNorm and the MLP are order-invariant, RoPE and the
+  // FPN map rows back to true tokens.
   const int win = m->d.window_size, nwin = (G / win) * (G / win);
+  LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, win, flags, s));
+  RUN(gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(w.x, E), s));
   for (int b = 0; b < m->d.num_blocks; ++b) {
     const BlockW& bw = m->blocks[b];
     if (m->d.attn_enabled[b]) {
@@ -594,6 +635,8 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
       e.rope_T = T;
       e.rope_hd = hd;
       e.rope_cols = 2 * E;  // q and k
+      e.wm_grid = G;
+      e.wm_win = win;
       RUN(gemm(m, w.h, rows, E, bw.qkv, EPI_QKV_ROPE, e, s));
       AttnArgs a = attn_base(H, hd);
       a.q = w.qkv;
@@ -607,16 +650,18 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
         a.o_batch_stride = (long long)T * E;
         a.Lq = a.Lk = T;
         a.batch = B;
-      } else {
-        a.win = win;
-        a.grid = G;
-        a.nwin = nwin;
-        a.img_stride_q = a.img_stride_k = a.img_stride_v = (long long)T * 3 * E;
-        a.img_stride_o = (long long)T * E;
+      } else {  // windows are contiguous blocks of win*win rows
+        a.q_batch_stride = a.k_batch_stride = a.v_batch_stride = (long long)win * win * 3 * E;
+        a.o_batch_stride = (long long)win * win * E;
         a.Lq = a.Lk = win * win;
         a.batch = B * nwin;
       }
-      RUN(attn(m, a, hd, s));
+      if (tc_attention_enabled() && attention_tc_supported(hd, a.Lq)) {
+        m->launches++;
+        RUN(attn_tc_packed(w.qkv, w.ao, a.batch, H, a.Lq, hd, E, m->num_sms, s));
+      } else {
+        RUN(attn(m, a, hd, s));
+      }
       RUN(gemm(m, w.ao, rows, E, bw.out, EPI_F32_RESID, epi_out(w.x, E), s));
     }
     if (m->d.mlp_enabled[b]) {
@@ -627,13 +672,16 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
   }
   // FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
   LAUNCH(cast_f32_to_f16(w.x, w.h, (long long)rows * E, s));
-  GemmEpi e0 = epi_out(l0, m->F0);
+  GemmEpi e0 = epi_out(l0, m->F0);  // rows scattered back to token-major order
   e0.out2 = w.l0h;
   e0.ldo2 = m->F0;
+  e0.wm_grid = G;
+  e0.wm_win = win;
+  e0.wm_scatter = 1;
   RUN(gemm(m, w.h, rows, E, m->fpn[0], EPI_F32_F16, e0, s));
-  LAUNCH(pool_tokens(w.x, w.pool1, B, G, E, 2, s));
+  LAUNCH(pool_tokens(w.x, w.pool1, B, G, E, 2, win, s));
   RUN(gemm(m, w.pool1, rows / 4, E, m->fpn[1], EPI_F32, epi_out(l1, m->F1), s));
-  LAUNCH(pool_tokens(w.x, w.pool2, B, G, E, 4, s));
+  LAUNCH(pool_tokens(w.x, w.pool2, B, G, E, 4, win, s));
   RUN(gemm(m, w.pool2, rows / 16, E, m->fpn[2], EPI_F32, epi_out(l2, m->F2), s));
   LAUNCH(finite_check(l0, (long long)rows * m->F0, flags, DART_FLAG_NONFINITE, s));
   LAUNCH(finite_check(l1, (long long)rows / 4 * m->F1, flags, DART_FLAG_NONFINITE, s));
@@ -815,3 +863,13 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 }
 
 }  // extern "C"
+
+extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
+                                  void* stream) {
+  if (!qkv || !o || items <= 0 || heads <= 0 || L <= 0) return fail(DART_ERR_INVALID, "dart_attention_qkv: bad args");
+  if (!attention_tc_supported(hd, L)) return fail(DART_ERR_INVALID, "dart_attention_qkv: unsupported hd / L");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return attn_tc_packed((const __half*)qkv, (__half*)o, items, heads, L, hd, heads * hd, sms, (cudaStream_t)stream);
+}

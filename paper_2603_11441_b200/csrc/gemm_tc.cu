@@ -61,7 +61,8 @@ __device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const
   if (EPI == EPI_QKV_ROPE) {
     if (col < e.rope_cols) {
       const int half_hd = e.rope_hd >> 1;
-      const int tok = row % e.rope_T;
+      int tok = row % e.rope_T;
+      if (e.wm_grid > 0) tok = wm_to_token(tok, e.wm_grid, e.wm_win);
       const float* ct = e.rope_cos + (size_t)tok * half_hd;
       const float* st = e.rope_sin + (size_t)tok * half_hd;
 #pragma unroll
@@ -77,6 +78,10 @@ __device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const
   if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) {
     store_f16x32(reinterpret_cast<act_t*>(e.out) + (size_t)row * e.ldo + col, v);
   } else if (EPI == EPI_F32 || EPI == EPI_F32_F16) {
+    if (e.wm_scatter) {
+      const int T = e.wm_grid * e.wm_grid;
+      row = (row / T) * T + wm_to_token(row % T, e.wm_grid, e.wm_win);
+    }
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
 #pragma unroll
     for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);

@@ -27,7 +27,24 @@ struct GemmEpi {
   int rope_T = 1;
   int rope_hd = 2;
   int rope_cols = 0;
+  // Window-major row order (grid x grid tokens, win x win windows): rows are stored window by
+  // window.  wm_grid > 0 makes the RoPE epilogue look up the true token of a row, and
+  // wm_scatter additionally writes output rows back in token-major order (FPN level 0).
+  int wm_grid = 0;
+  int wm_win = 0;
+  int wm_scatter = 0;
 };
+
+// window-major row index <-> token index within one image
+__host__ __device__ inline int wm_to_token(int r, int grid, int win) {
+  const int w2 = win * win, nw = grid / win;
+  const int w = r / w2, i = r - w * w2;
+  return ((w / nw) * win + i / win) * grid + (w % nw) * win + i % win;
+}
+__host__ __device__ inline int token_to_wm(int t, int grid, int win) {
+  const int r = t / grid, c = t - r * grid, nw = grid / win;
+  return (((r / win) * nw + c / win) * win + r % win) * win + c % win;
+}
 
 int gemm_bn_for(int N);
 int gemm_pick_bn(int M, int N, int num_sms);
@@ -56,14 +73,29 @@ struct AttnArgs {
 };
 int attention(const AttnArgs& a, int head_dim, cudaStream_t stream);
 
+// tcgen05 flash attention over contiguous row blocks of a token-major QKV buffer.
+struct AttnTcArgs {
+  int L;                       // rows per item (window or image); multiple of 192
+  int heads, items;
+  int q_col, k_col, v_col;     // column offsets of q / k / v in the QKV buffer
+  __half* o;                   // [items * L, o_ld]
+  int o_ld;
+  float scale_log2;
+};
+bool attention_tc_supported(int head_dim, int L);
+// tmQ: 2-D map over QKV [rows, cols] fp16, box {16, 128}, 32B swizzle; tmKV: same, box {16, 192}.
+int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms,
+                 cudaStream_t stream);
+
 // Row kernels.
 int layernorm_f32_to_f16(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
                          int ld_in, int ld_out, cudaStream_t stream);
 int layernorm_f32_to_f32(const float* x, const float* gamma, const float* beta, float* y, int rows, int dim,
                          cudaStream_t stream);
 int cast_f32_to_f16(const float* x, __half* y, long long n, cudaStream_t stream);
-int patchify(const float* images, __half* patches, int B, int S, int p, int kpad, int* flags, cudaStream_t stream);
-int pool_tokens(const float* x, __half* y, int B, int grid, int dim, int factor, cudaStream_t stream);
+int patchify(const float* images, __half* patches, int B, int S, int p, int kpad, int win, int* flags,
+             cudaStream_t stream);
+int pool_tokens(const float* x, __half* y, int B, int grid, int dim, int factor, int win, cudaStream_t stream);
 int finite_check(const float* x, long long n, int* flags, int bit, cudaStream_t stream);
 int broadcast_rows(const float* src, float* dst, long long row_elems, int reps, cudaStream_t stream);
 int gather_rows_f16(const float* table, const int* rows, __half* out, int n, int dim, cudaStream_t stream);

@@ -83,8 +83,9 @@ __global__ void cast_kernel(const float* __restrict__ x, __half* __restrict__ y,
 }
 
 // patches[b*T + t][k] for k < 3p^2 in (py, px, ch) order, zero for k in [3p^2, kpad).
+// Output rows are window-major (win > 0) so every attention window is a contiguous block.
 __global__ void patchify_kernel(const float* __restrict__ img, __half* __restrict__ out, int B, int S, int p,
-                                int kpad, int* flags) {
+                                int kpad, int win, int* flags) {
   const int g = S / p;
   const long long total = (long long)B * g * g * kpad;
   const int kdim = 3 * p * p;
@@ -96,7 +97,8 @@ __global__ void patchify_kernel(const float* __restrict__ img, __half* __restric
     float val = 0.f;
     if (k < kdim) {
       const int b = (int)(tokb / (g * g));
-      const int t = (int)(tokb % (g * g));
+      int t = (int)(tokb % (g * g));
+      if (win > 0) t = wm_to_token(t, g, win);
       const int r = t / g, c = t % g;
       const int py = k / (3 * p), rem = k % (3 * p), px = rem / 3, ch = rem % 3;
       val = img[(((long long)b * S + r * p + py) * S + c * p + px) * 3 + ch];
@@ -108,7 +110,7 @@ __global__ void patchify_kernel(const float* __restrict__ img, __half* __restric
 }
 
 __global__ void pool_kernel(const float* __restrict__ x, __half* __restrict__ y, int B, int grid, int dim,
-                            int f) {
+                            int f, int win) {
   const int g2 = grid / f;
   const long long total = (long long)B * g2 * g2 * dim;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -120,8 +122,11 @@ __global__ void pool_kernel(const float* __restrict__ x, __half* __restrict__ y,
     const int r = t / g2, c = t % g2;
     float s = 0.f;
     for (int i = 0; i < f; ++i)
-      for (int j = 0; j < f; ++j)
-        s += x[((long long)b * grid * grid + (long long)(r * f + i) * grid + c * f + j) * dim + e];
+      for (int j = 0; j < f; ++j) {
+        int t = (r * f + i) * grid + c * f + j;
+        if (win > 0) t = token_to_wm(t, grid, win);
+        s += x[((long long)b * grid * grid + t) * dim + e];
+      }
     y[idx] = __float2half_rn(s / (float)(f * f));
   }
 }
@@ -213,14 +218,15 @@ int cast_f32_to_f16(const float* x, __half* y, long long n, cudaStream_t stream)
   cast_kernel<<<(int)((threads + 255) / 256), 256, 0, stream>>>(x, y, n);
   return (int)cudaGetLastError();
 }
-int patchify(const float* images, __half* patches, int B, int S, int p, int kpad, int* flags, cudaStream_t stream) {
+int patchify(const float* images, __half* patches, int B, int S, int p, int kpad, int win, int* flags,
+             cudaStream_t stream) {
   const long long total = (long long)B * (S / p) * (S / p) * kpad;
-  patchify_kernel<<<grid_for(total), 256, 0, stream>>>(images, patches, B, S, p, kpad, flags);
+  patchify_kernel<<<grid_for(total), 256, 0, stream>>>(images, patches, B, S, p, kpad, win, flags);
   return (int)cudaGetLastError();
 }
-int pool_tokens(const float* x, __half* y, int B, int grid, int dim, int factor, cudaStream_t stream) {
+int pool_tokens(const float* x, __half* y, int B, int grid, int dim, int factor, int win, cudaStream_t stream) {
   const long long total = (long long)B * (grid / factor) * (grid / factor) * dim;
-  pool_kernel<<<grid_for(total), 256, 0, stream>>>(x, y, B, grid, dim, factor);
+  pool_kernel<<<grid_for(total), 256, 0, stream>>>(x, y, B, grid, dim, factor, win);
   return (int)cudaGetLastError();
 }
 int finite_check(const float* x, long long n, int* flags, int bit, cudaStream_t stream) {

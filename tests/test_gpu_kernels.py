@@ -143,3 +143,35 @@ def test_attention_windowed(lib, hd, grid, win, heads):
     ow = ref_attention(x[:, :, 0], x[:, :, 1], x[:, :, 2])  # [B, nw, H, w2, hd]
     ow = ow.reshape(B, n, n, heads, win, win, hd).permute(0, 1, 4, 2, 5, 3, 6).reshape(B, T, E)
     assert float((o.float() - ow).abs().max()) < 1e-2
+
+
+@pytest.mark.parametrize("items,L", [(2, 576), (1, 5184), (9, 576)])
+def test_attention_tcgen05_packed_qkv(lib, items, L):
+    """tcgen05/TMEM flash attention (hd 80) on the backbone's packed QKV layout vs fp32 torch."""
+    H, hd = 16, 80
+    E = H * hd
+    g = torch.Generator(device="cuda").manual_seed(L + items)
+    qkv = (torch.randn(items, L, 3, H, hd, device="cuda", generator=g) * 2).half()
+    o = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, stream()))
+    torch.cuda.synchronize()
+    x = qkv.permute(2, 0, 3, 1, 4)  # [3, items, H, L, hd]
+    ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
+    assert float((o.float() - ref).abs().max()) < 1e-2
+
+
+def test_attention_tcgen05_large_logits(lib):
+    """Peaked softmax (lazy-rescale path): scores growing along the key axis."""
+    items, L, H, hd = 1, 576, 16, 80
+    E = H * hd
+    g = torch.Generator(device="cuda").manual_seed(7)
+    qkv = torch.randn(items, L, 3, H, hd, device="cuda", generator=g)
+    qkv[:, :, 0] *= 4
+    qkv[:, :, 1] *= torch.linspace(0.1, 6, L, device="cuda")[None, :, None, None]
+    qkv = qkv.half()
+    o = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, stream()))
+    torch.cuda.synchronize()
+    x = qkv.permute(2, 0, 3, 1, 4)
+    ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
+    assert float((o.float() - ref).abs().max()) < 2e-2
