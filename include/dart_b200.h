@@ -108,8 +108,10 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 
 /* tcgen05/TMEM flash attention on a packed QKV buffer [items * L, 3 * heads * hd] fp16 (q | k | v
  * column blocks, head-major inside each), o [items * L, heads * hd] fp16.  hd = 80, L % 192 == 0
- * (the backbone's windowed and global attention, model.py:390-409). */
-int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd, void* stream);
+ * (the backbone's windowed and global attention, model.py:390-409).  debug_host: NULL, or host-mapped
+ * int32[8] that receives a protocol-hang report (tests only). */
+int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
+                       int32_t* debug_host, void* stream);
 
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */

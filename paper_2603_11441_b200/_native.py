@@ -97,7 +97,7 @@ def load() -> ctypes.CDLL:
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int64, I32, I32, P]
     lib.dart_attention.restype = ctypes.c_int
-    lib.dart_attention_qkv.argtypes = [P, P, I32, I32, I32, I32, P]
+    lib.dart_attention_qkv.argtypes = [P, P, I32, I32, I32, I32, P, P]
     lib.dart_attention_qkv.restype = ctypes.c_int
     lib.dart_launch_count.argtypes = [P]
     lib.dart_launch_count.restype = ctypes.c_int64

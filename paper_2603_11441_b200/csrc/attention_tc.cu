@@ -119,14 +119,14 @@ __global__ void __launch_bounds__(256, 1)
         const int h = (item / q_tiles) % a.heads;
         const int z = item / (q_tiles * a.heads);
         const int row0 = z * a.L;
-        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_wait_dbg(q_empty, (it & 1) ^ 1, 1000000 + it, a.dbg);
         mbar_arrive_expect_tx(q_full, L::Q_BYTES);
         for (int b = 0; b < L::NB; ++b)
           tma_load_2d(smem + b * L::Q_BLOCK, &tmQ, q_full, a.q_col + h * HD + b * 16, row0 + qt * BQ);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
-          mbar_wait(&kv_empty[st], ph ^ 1);
+          mbar_wait_dbg(&kv_empty[st], ph ^ 1, 2000000 + g, a.dbg);
           uint8_t* sk = smem + L::OFF_K + st * L::K_BYTES;
           uint8_t* sv = smem + L::OFF_V + st * L::V_BYTES;
           mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t sq = smem_u32(smem);
       auto issue_s = [&](int gg) {
         const int st = gg & 1;
-        mbar_wait(&k_full[st], (gg >> 1) & 1);
+        mbar_wait_dbg(&k_full[st], (gg >> 1) & 1, 3000000 + gg, a.dbg);
         tc_fence_after();
         const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
 #pragma unroll
@@ -156,15 +156,15 @@ __global__ void __launch_bounds__(256, 1)
       };
       int it = 0, g = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        mbar_wait(q_full, it & 1);
+        mbar_wait_dbg(q_full, it & 1, 4000000 + it, a.dbg);
         tc_fence_after();
         issue_s(g);
         if (nkv > 1) issue_s(g + 1);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
-          mbar_wait(&p_full[st], ph);
-          mbar_wait(&v_full[st], ph);
+          mbar_wait_dbg(&p_full[st], ph, 5000000 + g, a.dbg);
+          mbar_wait_dbg(&v_full[st], ph, 6000000 + g, a.dbg);
           tc_fence_after();
           const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
 #pragma unroll
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < nkv; ++j, ++g) {
         const int st = g & 1;
         const uint32_t ph = (g >> 1) & 1;
-        mbar_wait(&s_full[st], ph);
+        mbar_wait_dbg(&s_full[st], ph, 7000000 + g, a.dbg);
         tc_fence_after();
         const uint32_t sbase = lane_base + st * BKV;
         float mx = -INFINITY;
@@ -204,12 +204,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) mx = fmax3f(mx, v[i], v[i + 1]);
         }
-        if ((mx - m_ref) * c > RESCALE_LOG2) {  // also true for the first tile (m_ref = -inf)
+        // warp-uniform decision: tcgen05.ld/st below are warp-collective (.sync.aligned)
+        if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
+          const float m_new = fmaxf(m_ref, mx);
           if (j > 0) {
             const int gp = g - 1;  // previous P.V must be complete before O is rescaled
-            mbar_wait(&o_done[gp & 1], (gp >> 1) & 1);
+            mbar_wait_dbg(&o_done[gp & 1], (gp >> 1) & 1, 8000000 + gp, a.dbg);
             tc_fence_after();
-            const float f = fast_exp2((m_ref - mx) * c);
+            const float f = fast_exp2((m_ref - m_new) * c);
 #pragma unroll 1
             for (int ch = 0; ch < L::ON / 16; ++ch) {
               float v[16];
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(256, 1)
               tmem_st16(lane_base + L::OCOL + ch * 16, u);
             }
           }
-          m_ref = mx;
+          m_ref = m_new;
         }
         const float nb = -m_ref * c;
 #pragma unroll 1
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       // epilogue: O / rowsum -> fp16 rows of the output
       const int gl = g - 1;
-      mbar_wait(&o_done[gl & 1], (gl >> 1) & 1);
+      mbar_wait_dbg(&o_done[gl & 1], (gl >> 1) & 1, 9000000 + gl, a.dbg);
       tc_fence_after();
       float lsum[16];
       tmem_ld16(lane_base + L::OCOL + HD, lsum);

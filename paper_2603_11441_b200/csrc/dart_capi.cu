@@ -87,7 +87,7 @@ bool tc_attention_enabled() {
 // Backbone self-attention on a packed QKV buffer [items * L, 3E] (q | k | v column blocks,
 // head-major), tcgen05 kernel.
 int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, int hd, int E, int num_sms,
-                   cudaStream_t s) {
+                   cudaStream_t s, int* dbg = nullptr) {
   CUtensorMap tq, tkv;
   const uint64_t rows = (uint64_t)items * L;
   if (!make_tmap_ex(&tq, qkv, 3 * E, rows, 3 * E, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
@@ -103,6 +103,7 @@ int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, in
   a.o = o;
   a.o_ld = E;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+  a.dbg = dbg;
   int rc = attention_tc(tq, tkv, a, num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
@@ -865,11 +866,12 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 }  // extern "C"
 
 extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
-                                  void* stream) {
+                                  int32_t* debug_host, void* stream) {
   if (!qkv || !o || items <= 0 || heads <= 0 || L <= 0) return fail(DART_ERR_INVALID, "dart_attention_qkv: bad args");
   if (!attention_tc_supported(hd, L)) return fail(DART_ERR_INVALID, "dart_attention_qkv: unsupported hd / L");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return attn_tc_packed((const __half*)qkv, (__half*)o, items, heads, L, hd, heads * hd, sms, (cudaStream_t)stream);
+  return attn_tc_packed((const __half*)qkv, (__half*)o, items, heads, L, hd, heads * hd, sms, (cudaStream_t)stream,
+                        debug_host);
 }

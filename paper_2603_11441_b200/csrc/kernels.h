@@ -81,6 +81,7 @@ struct AttnTcArgs {
   __half* o;                   // [items * L, o_ld]
   int o_ld;
   float scale_log2;
+  int* dbg = nullptr;          // host-mapped hang report (tests only), see mbar_wait_dbg
 };
 bool attention_tc_supported(int head_dim, int L);
 // tmQ: 2-D map over QKV [rows, cols] fp16, box {16, 128}, 32B swizzle; tmKV: same, box {16, 192}.

@@ -153,7 +153,7 @@ def test_attention_tcgen05_packed_qkv(lib, items, L):
     g = torch.Generator(device="cuda").manual_seed(L + items)
     qkv = (torch.randn(items, L, 3, H, hd, device="cuda", generator=g) * 2).half()
     o = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
-    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, stream()))
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, stream()))
     torch.cuda.synchronize()
     x = qkv.permute(2, 0, 3, 1, 4)  # [3, items, H, L, hd]
     ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
@@ -170,7 +170,7 @@ def test_attention_tcgen05_large_logits(lib):
     qkv[:, :, 1] *= torch.linspace(0.1, 6, L, device="cuda")[None, :, None, None]
     qkv = qkv.half()
     o = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
-    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, stream()))
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, stream()))
     torch.cuda.synchronize()
     x = qkv.permute(2, 0, 3, 1, 4)
     ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
