@@ -43,6 +43,17 @@ for (M, N, K, epi, name) in [(5184, 3840, 1280, 0, "qkv"), (5184, 1280, 1280, 3,
     fl = 2 * M * N * K
     print(f"{name:16s} {M}x{N}x{K} e{epi}: {t*1e3:8.1f} us {fl/t/1e9:7.1f} | {tc*1e3:8.1f} us {fl/tc/1e9:7.1f}")
 
+print("ATTN tcgen05 (packed QKV)  items L: us  TF/s  Gexp/s")
+for (items, L, name) in [(1, 5184, "bb global"), (9, 576, "bb windowed")]:
+    H, hd = 16, 80
+    E = H * hd
+    qkv = torch.randn(items * L, 3 * E, device="cuda").half()
+    o = torch.empty(items * L, E, device="cuda", dtype=torch.float16)
+    f = lambda: _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, st.cuda_stream))
+    t = bench(f, reps=20)
+    fl = 4 * items * H * L * L * hd
+    print(f"{name:16s} {items} {L}: {t*1e3:9.1f} us {fl/t/1e9:7.1f} TF/s {items*H*L*L/t/1e6:8.1f} Gexp/s")
+
 print("ATTN  batch heads Lq Lk hd: us  TF/s  Gexp/s")
 for (B, H, Lq, Lk, hd, name) in [(1, 16, 5184, 5184, 80, "bb global"), (9, 16, 576, 576, 80, "bb windowed"),
                                   (4, 16, 5184, 5184, 16, "enc self N=4"), (4, 16, 5184, 32, 16, "enc text N=4"),
