@@ -23,7 +23,8 @@ struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 4 epilogue staging buffers of 4 KB
+  static constexpr int BAR_OFF = EPI_OFF + 4 * 4096;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 };
@@ -42,7 +43,7 @@ __device__ __forceinline__ void store_f16x32(act_t* dst, const float* v) {
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const GemmEpi& e) {
+__device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const GemmEpi& e, int rope_tok) {
   if (e.bias != nullptr) {
     const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
 #pragma unroll
@@ -60,40 +61,115 @@ __device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const
   }
   if (EPI == EPI_QKV_ROPE) {
     if (col < e.rope_cols) {
+      // rope_tok: this row's true token (computed once per tile row by the caller)
       const int half_hd = e.rope_hd >> 1;
-      int tok = row % e.rope_T;
-      if (e.wm_grid > 0) tok = wm_to_token(tok, e.wm_grid, e.wm_win);
-      const float* ct = e.rope_cos + (size_t)tok * half_hd;
-      const float* st = e.rope_sin + (size_t)tok * half_hd;
+      const float* ct = e.rope_cos + (size_t)rope_tok * half_hd;
+      const float* st = e.rope_sin + (size_t)rope_tok * half_hd;
+      int p = (col % e.rope_hd) >> 1;  // pair index within the head, wraps at half_hd
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        int p = ((col + j) % e.rope_hd) >> 1;
-        float c = __ldg(ct + p), s = __ldg(st + p);
-        float ev = v[j], od = v[j + 1];
+        const float c = __ldg(ct + p), s = __ldg(st + p);
+        const float ev = v[j], od = v[j + 1];
         v[j] = ev * c - od * s;
         v[j + 1] = ev * s + od * c;
+        p = (p + 1 == half_hd) ? 0 : p + 1;
       }
     }
   }
-  if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) {
-    store_f16x32(reinterpret_cast<act_t*>(e.out) + (size_t)row * e.ldo + col, v);
-  } else if (EPI == EPI_F32 || EPI == EPI_F32_F16) {
-    if (e.wm_scatter) {
-      const int T = e.wm_grid * e.wm_grid;
-      row = (row / T) * T + wm_to_token(row % T, e.wm_grid, e.wm_win);
+}
+
+// ---- coalesced chunk I/O through a per-warp staging buffer -----------------------------
+// A warp owns a 32-row x 32-column chunk (thread = row after tcgen05.ld).  The chunk goes
+// through 4 KB of shared memory whose 16-byte slots are XOR-swizzled by row, so both the
+// row-per-thread accesses and the line-per-8-lanes global accesses run at 4 wavefronts per
+// 128-bit instruction, and every global load/store moves full 128-byte lines.
+__device__ __forceinline__ float4* slot32(float* buf, int r, int k) {  // fp32 row r, 16B slot k (0..7)
+  return reinterpret_cast<float4*>(buf) + r * 8 + (k ^ (r & 7));
+}
+__device__ __forceinline__ uint4* slot16(float* buf, int r, int k) {  // fp16 row r, 16B slot k (0..3)
+  return reinterpret_cast<uint4*>(buf) + r * 4 + (k ^ (r & 3));
+}
+
+// dst_row(r): global row for chunk row r (identity, or the FPN's window-major -> token scatter)
+__device__ __forceinline__ int chunk_dst_row(int row, const GemmEpi& e) {
+  if (e.wm_scatter) {
+    const int T = e.wm_grid * e.wm_grid;
+    return (row / T) * T + wm_to_token(row % T, e.wm_grid, e.wm_win);
+  }
+  return row;
+}
+
+// Write the warp's chunk of fp32 values (v = this lane's row) to out (+= residual if RESID).
+template <bool RESID>
+__device__ __forceinline__ void chunk_store_f32(float* buf, const float* v, float* out, int ldo, int row0, int col,
+                                                int M, const GemmEpi& e) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3, k = lane & 7;  // coalesced phase: 4 rows x 8 slots per instruction
+  if (RESID) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = i * 4 + sub;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row0 + r < M) x = *reinterpret_cast<const float4*>(out + (size_t)(row0 + r) * ldo + col + 4 * k);
+      *slot32(buf, r, k) = x;
     }
-    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
+    __syncwarp();
+  }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    if (EPI == EPI_F32_F16) store_f16x32(reinterpret_cast<act_t*>(e.out2) + (size_t)row * e.ldo2 + col, v);
+  for (int q = 0; q < 8; ++q) {
+    float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    if (RESID) {
+      const float4 x = *slot32(buf, lane, q);
+      o.x += x.x;
+      o.y += x.y;
+      o.z += x.z;
+      o.w += x.w;
+    }
+    *slot32(buf, lane, q) = o;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = i * 4 + sub;
+    if (row0 + r < M)
+      *reinterpret_cast<float4*>(out + (size_t)chunk_dst_row(row0 + r, e) * ldo + col + 4 * k) = *slot32(buf, r, k);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void chunk_store_f16(float* buf, const float* v, act_t* out, int ldo, int row0, int col,
+                                                int M, const GemmEpi& e) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
+    u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
+    u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
+    u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
+    *slot16(buf, lane, q) = u;
+  }
+  __syncwarp();
+  const int sub = lane >> 2, k = lane & 3;  // 8 rows x 4 slots (64 B rows) per instruction
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = i * 8 + sub;
+    if (row0 + r < M)
+      *reinterpret_cast<uint4*>(out + (size_t)chunk_dst_row(row0 + r, e) * ldo + col + 8 * k) = *slot16(buf, r, k);
+  }
+  __syncwarp();
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_store(float* buf, const float* v, int row0, int col, int M,
+                                               const GemmEpi& e) {
+  if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) {
+    chunk_store_f16(buf, v, reinterpret_cast<act_t*>(e.out), e.ldo, row0, col, M, e);
+  } else if (EPI == EPI_F32 || EPI == EPI_F32_F16) {
+    chunk_store_f32<false>(buf, v, reinterpret_cast<float*>(e.out), e.ldo, row0, col, M, e);
+    if (EPI == EPI_F32_F16) chunk_store_f16(buf, v, reinterpret_cast<act_t*>(e.out2), e.ldo2, row0, col, M, e);
   } else if (EPI == EPI_F32_RESID) {
-    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
-    float4 r[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) r[q] = o[q];
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      o[q] = make_float4(r[q].x + v[4 * q], r[q].y + v[4 * q + 1], r[q].z + v[4 * q + 2], r[q].w + v[4 * q + 3]);
+    chunk_store_f32<true>(buf, v, reinterpret_cast<float*>(e.out), e.ldo, row0, col, M, e);
   }
 }
 
@@ -192,6 +268,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int quarter = warp & 3;
+    float* stage_buf = reinterpret_cast<float*>(smem + L::EPI_OFF) + quarter * 1024;  // 4 KB per warp
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -202,6 +279,11 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = m0 + quarter * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      int rope_tok = 0;
+      if (EPI == EPI_QKV_ROPE) {
+        rope_tok = row % epi.rope_T;
+        if (epi.wm_grid > 0) rope_tok = wm_to_token(rope_tok, epi.wm_grid, epi.wm_win);
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -213,7 +295,8 @@ __global__ void __launch_bounds__(256, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (row < M) epilogue_chunk<EPI>(v, row, n0 + c, epi);
+        epilogue_chunk<EPI>(v, row, n0 + c, epi, rope_tok);
+        epilogue_store<EPI>(stage_buf, v, m0 + quarter * 32, n0 + c, M, epi);
       }
     }
   }
