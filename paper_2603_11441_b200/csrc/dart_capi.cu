@@ -73,6 +73,18 @@ bool make_tmap_ex(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows
 bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld, uint32_t box_rows) {
   return make_tmap_ex(m, ptr, inner, rows, ld, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
+// fp32 [rows, inner] map with 32 x 32 boxes (128 B rows, 128B swizzle): the GEMM residual tiles.
+bool make_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 // Attention implementation switch for A/B tests: DART_ATTN_IMPL=mma forces the mma.sync kernel.
 bool tc_attention_enabled() {
@@ -322,8 +334,15 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
   if (!make_tmap(&ta, A, W.K, M, lda, 128)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (A)");
   if (e.bias == nullptr) e.bias = W.b;
   m->launches++;
-  const int bn = gemm_pick_bn(M, W.N, m->num_sms);
-  int rc = gemm_tc(ta, W.tmap[bn_slot(bn)], M, W.N, W.K, bn, epi, e, m->num_sms, s);
+  CUtensorMap tc;
+  int bn;
+  if (epi == EPI_F32_RESID) {
+    bn = gemm_resid_bn(W.N);
+    if (!make_tmap_f32(&tc, e.out, W.N, M, e.ldo)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (C)");
+  } else {
+    bn = gemm_pick_bn(M, W.N, m->num_sms);
+  }
+  int rc = gemm_tc(ta, W.tmap[bn_slot(bn)], &tc, M, W.N, W.K, bn, epi, e, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
 }
@@ -810,9 +829,10 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int bn = gemm_pick_bn(M, N, sms);
-  CUtensorMap ta, tb;
-  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, bn))
+  const int bn = epi == EPI_F32_RESID ? gemm_resid_bn(N) : gemm_pick_bn(M, N, sms);
+  CUtensorMap ta, tb, tc;
+  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, bn) ||
+      (epi == EPI_F32_RESID && !make_tmap_f32(&tc, out, N, M, N)))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   GemmEpi e;
   e.bias = bias;
@@ -825,7 +845,7 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.rope_T = rope_T > 0 ? rope_T : 1;
   e.rope_hd = rope_hd > 0 ? rope_hd : 2;
   e.rope_cols = rope_cols;
-  int rc = gemm_tc(ta, tb, M, N, K, bn, epi, e, sms, (cudaStream_t)stream);
+  int rc = gemm_tc(ta, tb, &tc, M, N, K, bn, epi, e, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }

@@ -18,13 +18,14 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 fp16 = 128 B = one swizzle atom row
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool RESID = false>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 4 epilogue staging buffers of 4 KB
-  static constexpr int BAR_OFF = EPI_OFF + 4 * 4096;
+  static constexpr int RES_OFF = EPI_OFF + 4 * 4096;    // residual tile (RESID epilogue only)
+  static constexpr int BAR_OFF = RES_OFF + (RESID ? BM * BN * 4 : 0);
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 };
@@ -173,18 +174,47 @@ __device__ __forceinline__ void epilogue_store(float* buf, const float* v, int r
   }
 }
 
+// Residual epilogue (EPI_F32_RESID, BN <= 128): warp 3 TMA-loads the tile's fp32 residual
+// [128 x BN] into smem (32x32 boxes, 128B swizzle == slot32 layout) while the MMAs run; each
+// epilogue warp adds its accumulator chunk in place and TMA-stores the chunk back.
+template <int EPI>
+__device__ __forceinline__ void resid_chunk(float* buf, const float* v, const CUtensorMap* tmC, int row0, int col) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4* s = slot32(buf, lane, q);
+    float4 x = *s;
+    x.x += v[4 * q];
+    x.y += v[4 * q + 1];
+    x.z += v[4 * q + 2];
+    x.w += v[4 * q + 3];
+    *s = x;
+  }
+  fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy) store
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmC, buf, col, row0);
+    tma_store_commit();
+  }
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(256, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, GemmEpi epi) {
-  using L = GemmSmem<BN, STAGES>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi epi) {
+  using L = GemmSmem<BN, STAGES, EPI == EPI_F32_RESID>;
+  constexpr bool RESID = EPI == EPI_F32_RESID;
+  constexpr int CPW = BN / 32;  // 32-column chunks per epilogue warp and tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 1);
+  float* resid = reinterpret_cast<float*>(smem + L::RES_OFF);  // [4 warps][CPW chunks][32 x 32]
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -204,6 +234,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    mbar_init(rfull, 1);
+    mbar_init(rempty, 4);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
@@ -266,6 +298,19 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&tfull[acc]);
       }
     }
+  } else if (warp == 3) {
+    if (RESID && lane == 0) {  // residual prefetch, one tile ahead of the epilogue
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int m0 = (tile / num_n) * BM;
+        const int n0 = (tile % num_n) * BN;
+        mbar_wait(rempty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(rfull, BM * BN * 4);
+        for (int q = 0; q < 4; ++q)
+          for (int c = 0; c < CPW; ++c)
+            tma_load_2d(resid + (q * CPW + c) * 1024, &tmC, rfull, n0 + 32 * c, m0 + 32 * q);
+      }
+    }
   } else if (warp >= 4) {
     const int quarter = warp & 3;
     float* stage_buf = reinterpret_cast<float*>(smem + L::EPI_OFF) + quarter * 1024;  // 4 KB per warp
@@ -296,8 +341,22 @@ __global__ void __launch_bounds__(256, 1)
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         epilogue_chunk<EPI>(v, row, n0 + c, epi, rope_tok);
-        epilogue_store<EPI>(stage_buf, v, m0 + quarter * 32, n0 + c, M, epi);
+        if constexpr (RESID) {
+          if (c == 0) mbar_wait(rfull, it & 1);
+          resid_chunk<EPI>(resid + (quarter * CPW + c / 32) * 1024, v, &tmC, m0 + quarter * 32, n0 + c);
+        } else {
+          epilogue_store<EPI>(stage_buf, v, m0 + quarter * 32, n0 + c, M, epi);
+        }
       }
+      if constexpr (RESID) {  // residual buffer reusable once the TMA stores have read it
+        if (lane == 0) {
+          tma_store_wait_read0();
+          mbar_arrive(rempty);
+        }
+      }
+    }
+    if constexpr (RESID) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes landed
     }
   }
   tc_fence_before();
@@ -309,9 +368,9 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int BN, int STAGES, int EPI>
-int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, const GemmEpi& epi, int num_sms,
-                cudaStream_t stream) {
-  using L = GemmSmem<BN, STAGES>;
+int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, int M, int N, int K,
+                const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES, EPI == EPI_F32_RESID>;
   auto kern = gemm_tc_kernel<BN, STAGES, EPI>;
   static bool configured = false;
   if (!configured) {
@@ -321,20 +380,19 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int 
   }
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, 256, L::TOTAL, stream>>>(tA, tB, M, N, K, epi);
+  kern<<<grid, 256, L::TOTAL, stream>>>(tA, tB, tC, M, N, K, epi);
   return (int)cudaGetLastError();
 }
 
 template <int BN, int STAGES>
-int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, const GemmEpi& epi,
-                 int num_sms, cudaStream_t stream) {
+int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, int M, int N,
+                 int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   switch (epi_mode) {
-    case EPI_F16: return launch_gemm<BN, STAGES, EPI_F16>(tA, tB, M, N, K, epi, num_sms, stream);
-    case EPI_F16_RELU: return launch_gemm<BN, STAGES, EPI_F16_RELU>(tA, tB, M, N, K, epi, num_sms, stream);
-    case EPI_F32: return launch_gemm<BN, STAGES, EPI_F32>(tA, tB, M, N, K, epi, num_sms, stream);
-    case EPI_F32_RESID: return launch_gemm<BN, STAGES, EPI_F32_RESID>(tA, tB, M, N, K, epi, num_sms, stream);
-    case EPI_QKV_ROPE: return launch_gemm<BN, STAGES, EPI_QKV_ROPE>(tA, tB, M, N, K, epi, num_sms, stream);
-    case EPI_F32_F16: return launch_gemm<BN, STAGES, EPI_F32_F16>(tA, tB, M, N, K, epi, num_sms, stream);
+    case EPI_F16: return launch_gemm<BN, STAGES, EPI_F16>(tA, tB, tC, M, N, K, epi, num_sms, stream);
+    case EPI_F16_RELU: return launch_gemm<BN, STAGES, EPI_F16_RELU>(tA, tB, tC, M, N, K, epi, num_sms, stream);
+    case EPI_F32: return launch_gemm<BN, STAGES, EPI_F32>(tA, tB, tC, M, N, K, epi, num_sms, stream);
+    case EPI_QKV_ROPE: return launch_gemm<BN, STAGES, EPI_QKV_ROPE>(tA, tB, tC, M, N, K, epi, num_sms, stream);
+    case EPI_F32_F16: return launch_gemm<BN, STAGES, EPI_F32_F16>(tA, tB, tC, M, N, K, epi, num_sms, stream);
   }
   return (int)cudaErrorInvalidValue;
 }
@@ -367,16 +425,24 @@ int gemm_pick_bn(int M, int N, int num_sms) {
   return best;
 }
 
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int BN, int epi_mode,
-            const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, int M, int N, int K, int BN,
+            int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
+  if (epi_mode == EPI_F32_RESID) {  // TMA residual epilogue: BN <= 128, fewer mainloop stages
+    if (!tC) return (int)cudaErrorInvalidValue;
+    if (BN == 128) return launch_gemm<128, 4, EPI_F32_RESID>(tA, tB, *tC, M, N, K, epi, num_sms, stream);
+    if (BN == 64) return launch_gemm<64, 6, EPI_F32_RESID>(tA, tB, *tC, M, N, K, epi, num_sms, stream);
+    return (int)cudaErrorInvalidValue;
+  }
   switch (BN) {
-    case 256: return dispatch_epi<256, 4>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
-    case 128: return dispatch_epi<128, 6>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
-    case 64: return dispatch_epi<64, 8>(epi_mode, tA, tB, M, N, K, epi, num_sms, stream);
+    case 256: return dispatch_epi<256, 4>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
+    case 128: return dispatch_epi<128, 6>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
+    case 64: return dispatch_epi<64, 8>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
   }
   return (int)cudaErrorInvalidValue;
 }
+
+int gemm_resid_bn(int N) { return N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : 0); }
 
 }  // namespace dart

@@ -48,9 +48,12 @@ __host__ __device__ inline int token_to_wm(int t, int grid, int win) {
 
 int gemm_bn_for(int N);
 int gemm_pick_bn(int M, int N, int num_sms);
-// tB must be a tensor map over W [N, K] with box {64, BN}.
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, int M, int N, int K, int BN, int epi_mode,
-            const GemmEpi& epi, int num_sms, cudaStream_t stream);
+// tB must be a tensor map over W [N, K] with box {64, BN}.  EPI_F32_RESID additionally needs
+// tC: fp32 map over the residual/output [M, N] (row stride ldo) with box {32, 32}, 128B swizzle,
+// and BN = gemm_resid_bn(N).
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, int M, int N, int K, int BN,
+            int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream);
+int gemm_resid_bn(int N);
 
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {
