@@ -143,12 +143,22 @@ __global__ void __launch_bounds__(WARPS * 32, HD == 16 ? 6 : 1) flash_attn_kerne
     m_r[1] = mx1;
     const float nb0 = -mx0 * c, nb1 = -mx1 * c;
     uint32_t p[4][4];
+    // hd 16 is exp-bound: the last POLY n-tiles (POLY/8 of the exps) use the FMA-pipe exp2
+    constexpr int POLY = HD == 16 ? 2 : 0;
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-      const float p0 = fast_exp2(fmaf(s[n][0], c, nb0));
-      const float p1 = fast_exp2(fmaf(s[n][1], c, nb0));
-      const float p2 = fast_exp2(fmaf(s[n][2], c, nb1));
-      const float p3 = fast_exp2(fmaf(s[n][3], c, nb1));
+      float p0, p1, p2, p3;
+      if (n >= 8 - POLY) {
+        p0 = exp2_poly(fmaf(s[n][0], c, nb0));
+        p1 = exp2_poly(fmaf(s[n][1], c, nb0));
+        p2 = exp2_poly(fmaf(s[n][2], c, nb1));
+        p3 = exp2_poly(fmaf(s[n][3], c, nb1));
+      } else {
+        p0 = fast_exp2(fmaf(s[n][0], c, nb0));
+        p1 = fast_exp2(fmaf(s[n][1], c, nb0));
+        p2 = fast_exp2(fmaf(s[n][2], c, nb1));
+        p3 = fast_exp2(fmaf(s[n][3], c, nb1));
+      }
       p[n >> 1][(n & 1) * 2 + 0] = pack_half2(p0, p1);
       p[n >> 1][(n & 1) * 2 + 1] = pack_half2(p2, p3);
     }

@@ -245,6 +245,18 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for x <= 0 on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f with the
+// 1.5*2^23 magic constant, degree-3 polynomial for 2^f on [-0.5, 0.5] (max rel. err 7.5e-5,
+// below the fp16 half-ulp the result is rounded to), exponent add by integer arithmetic.
+// Offloading part of a softmax's exps here balances the MUFU (16/clk/SM) and FMA pipes.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.0551716648f, f, 0.2426111251f), f, 0.6932609677f), f, 0.9999280572f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
