@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(WARPS * 32, HD == 16 ? 6 : 1) flash_attn_kerne
     const float nb0 = -mx0 * c, nb1 = -mx1 * c;
     uint32_t p[4][4];
     // hd 16 is exp-bound: the last POLY n-tiles (POLY/8 of the exps) use the FMA-pipe exp2
-    constexpr int POLY = HD == 16 ? 2 : 0;
+    constexpr int POLY = 0;  // measured: the hd-16 kernel is issue-bound, not MUFU-bound (poly made it slower)
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       float p0, p1, p2, p3;
