@@ -57,7 +57,35 @@ __global__ void __launch_bounds__(WARPS * 32, HD == 16 ? 6 : 1) flash_attn_kerne
     const __half* src = qb + (ok ? tok_offset(z, qi, a.q_batch_stride, a.q_tok_stride, a.img_stride_q, a.win, a.grid, a.nwin) : 0) + c * 8;
     cp_async16(smem_u32(&sQ[r * PITCH + c * 8]), src, ok);
   }
+  // K/V tile loads.  Dense items (win == 0, every enc-dec call) use per-thread source
+  // pointers computed once; only the tile offset is added per tile.
+  constexpr int NT = WARPS * 32;
+  constexpr int NL = (BKV * CH + NT - 1) / NT;  // 16-byte chunks per thread per tile
+  const __half* kp[NL];
+  const __half* vp[NL];
+  int krow[NL];
+  uint32_t soff[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) {
+    const int idx = tid + i * NT;
+    const int r = idx / CH, cc = idx % CH;  // compile-time divisors
+    krow[i] = idx < BKV * CH ? r : 1 << 30;
+    soff[i] = (uint32_t)(r * PITCH + cc * 8);
+    kp[i] = kb + (long long)zkv * a.k_batch_stride + (long long)r * a.k_tok_stride + cc * 8;
+    vp[i] = vb + (long long)zkv * a.v_batch_stride + (long long)r * a.v_tok_stride + cc * 8;
+  }
+  const long long k_step = (long long)BKV * a.k_tok_stride, v_step = (long long)BKV * a.v_tok_stride;
   auto load_kv = [&](int buf, int kt) {
+    if (a.win == 0) {
+#pragma unroll
+      for (int i = 0; i < NL; ++i) {
+        if (krow[i] >= BKV) continue;
+        const bool ok = kt * BKV + krow[i] < a.Lk;
+        cp_async16(smem_u32(&sK[buf][soff[i]]), ok ? kp[i] + kt * k_step : kb, ok);
+        cp_async16(smem_u32(&sV[buf][soff[i]]), ok ? vp[i] + kt * v_step : vb, ok);
+      }
+      return;
+    }
     for (int idx = tid; idx < BKV * CH; idx += WARPS * 32) {
       const int r = idx / CH, c = idx % CH;
       const int ki = kt * BKV + r;
