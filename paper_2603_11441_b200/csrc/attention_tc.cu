@@ -23,8 +23,12 @@ namespace dart {
 namespace {
 
 constexpr int BQ = 128;
-constexpr int BKV = 192;
 constexpr float RESCALE_LOG2 = 8.0f;
+
+// Key-tile width per head dim: hd 80 uses 192-key tiles (TMEM 512 columns, 1 CTA/SM);
+// hd 16 (enc-dec, exp-bound) uses 96-key tiles so TMEM fits 256 columns and 2 CTAs share an SM.
+template <int HD>
+constexpr int kv_tile() { return HD == 80 ? 192 : 96; }
 
 __device__ __forceinline__ uint64_t desc_sw32(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
@@ -45,8 +49,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 
-template <int HD>
+template <int HD, int BKV>
 struct FaSmem {
+  static constexpr int TMEM = (2 * BKV + HD + 16) <= 256 ? 256 : 512;  // S0 | S1 | O (+ row-sum block)
   static constexpr int NB = HD / 16;                 // 16-dim column blocks
   static constexpr int Q_BLOCK = BQ * 32;            // bytes per Q column block
   static constexpr int KV_BLOCK = BKV * 32;          // bytes per K/V column block
@@ -61,10 +66,10 @@ struct FaSmem {
   static constexpr int ON = HD + 16;                 // O columns (values + row-sum block)
 };
 
-template <int HD>
+template <int HD, int BKV>
 __global__ void __launch_bounds__(256, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
-  using L = FaSmem<HD>;
+  using L = FaSmem<HD, BKV>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
@@ -79,9 +84,9 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = warp_id(), lane = lane_id();
-  const int q_tiles = (a.L + BQ - 1) / BQ;
+  const int q_tiles = (a.Lq + BQ - 1) / BQ;
   const int n_items = q_tiles * a.heads * a.items;
-  const int nkv = a.L / BKV;
+  const int nkv = a.Lkv / BKV;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(256, 1)
         make_uint2(0x3C003C00u, 0x3C003C00u);
   }
   fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 2) tmem_alloc<L::TMEM>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -118,11 +123,11 @@ __global__ void __launch_bounds__(256, 1)
         const int qt = item % q_tiles;
         const int h = (item / q_tiles) % a.heads;
         const int z = item / (q_tiles * a.heads);
-        const int row0 = z * a.L;
+        const int row0 = z * a.Lkv;
         mbar_wait_dbg(q_empty, (it & 1) ^ 1, 1000000 + it, a.dbg);
         mbar_arrive_expect_tx(q_full, L::Q_BYTES);
         for (int b = 0; b < L::NB; ++b)
-          tma_load_2d(smem + b * L::Q_BLOCK, &tmQ, q_full, a.q_col + h * HD + b * 16, row0 + qt * BQ);
+          tma_load_2d(smem + b * L::Q_BLOCK, &tmQ, q_full, a.q_col + h * HD + b * 16, z * a.Lq + qt * BQ);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
@@ -251,13 +256,13 @@ __global__ void __launch_bounds__(256, 1)
       tmem_ld_wait();
       const float inv = 1.f / lsum[0];
       const int qrow = qt * BQ + r;
-      __half* dst = a.o + ((long long)z * a.L + qrow) * a.o_ld + h * HD;
+      __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
 #pragma unroll 1
       for (int ch = 0; ch < HD / 16; ++ch) {
         float v[16];
         tmem_ld16(lane_base + L::OCOL + ch * 16, v);
         tmem_ld_wait();
-        if (qrow < a.L) {
+        if (qrow < a.Lq) {
           uint4 w0, w1;
           w0.x = pack_half2(v[0] * inv, v[1] * inv);
           w0.y = pack_half2(v[2] * inv, v[3] * inv);
@@ -277,27 +282,43 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<L::TMEM>(tmem);
   }
+}
+
+template <int HD>
+int launch_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms,
+              cudaStream_t stream) {
+  constexpr int BKV = kv_tile<HD>();
+  using Lay = FaSmem<HD, BKV>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(fa_tc_kernel<HD, BKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  const int ctas_per_sm = Lay::TMEM == 256 ? 2 : 1;
+  const int items = ((a.Lq + BQ - 1) / BQ) * a.heads * a.items;
+  const int grid = items < num_sms * ctas_per_sm ? items : num_sms * ctas_per_sm;
+  fa_tc_kernel<HD, BKV><<<grid, 256, Lay::TOTAL, stream>>>(tmQ, tmKV, a);
+  return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-bool attention_tc_supported(int head_dim, int L) { return head_dim == 80 && L % BKV == 0 && L >= BKV; }
+int attention_tc_kv_tile(int head_dim) { return head_dim == 80 ? kv_tile<80>() : head_dim == 16 ? kv_tile<16>() : 0; }
 
-int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms,
+bool attention_tc_supported(int head_dim, int Lkv) {
+  const int t = attention_tc_kv_tile(head_dim);
+  return t > 0 && Lkv % t == 0 && Lkv >= t;
+}
+
+int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream) {
-  using Lay = FaSmem<80>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fa_tc_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
-  const int items = ((a.L + BQ - 1) / BQ) * a.heads * a.items;
-  const int grid = items < num_sms ? items : num_sms;
-  fa_tc_kernel<80><<<grid, 256, Lay::TOTAL, stream>>>(tmQ, tmKV, a);
-  return (int)cudaGetLastError();
+  if (head_dim == 80) return launch_tc<80>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 16) return launch_tc<16>(tmQ, tmKV, a, num_sms, stream);
+  return (int)cudaErrorInvalidValue;
 }
 
 }  // namespace dart

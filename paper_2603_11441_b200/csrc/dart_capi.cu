@@ -98,27 +98,37 @@ bool tc_attention_enabled() {
 
 // Backbone self-attention on a packed QKV buffer [items * L, 3E] (q | k | v column blocks,
 // head-major), tcgen05 kernel.
-int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, int hd, int E, int num_sms,
-                   cudaStream_t s, int* dbg = nullptr) {
-  CUtensorMap tq, tkv;
-  const uint64_t rows = (uint64_t)items * L;
-  if (!make_tmap_ex(&tq, qkv, 3 * E, rows, 3 * E, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
-      !make_tmap_ex(&tkv, qkv, 3 * E, rows, 3 * E, 16, 192, CU_TENSOR_MAP_SWIZZLE_32B))
+// tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
+// [items*Lkv, kv_ld] (k at k_col, v at v_col), output [items*Lq, o_ld] at column h*hd.
+int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv_ld, int k_col, int v_col, __half* o,
+            int o_ld, int items, int heads, int Lq, int Lkv, int hd, int num_sms, cudaStream_t s, int* dbg = nullptr) {
+  CUtensorMap tq, tkv;  // maps cover exactly the used column ranges
+  const int q_inner = q_col + heads * hd, kv_inner = (k_col > v_col ? k_col : v_col) + heads * hd;
+  if (!make_tmap_ex(&tq, qbuf, q_inner, (uint64_t)items * Lq, q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !make_tmap_ex(&tkv, kvbuf, kv_inner, (uint64_t)items * Lkv, kv_ld, 16, attention_tc_kv_tile(hd),
+                    CU_TENSOR_MAP_SWIZZLE_32B))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (attention)");
   AttnTcArgs a;
-  a.L = L;
+  a.Lq = Lq;
+  a.Lkv = Lkv;
   a.heads = heads;
   a.items = items;
-  a.q_col = 0;
-  a.k_col = E;
-  a.v_col = 2 * E;
+  a.q_col = q_col;
+  a.k_col = k_col;
+  a.v_col = v_col;
   a.o = o;
-  a.o_ld = E;
+  a.o_ld = o_ld;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.dbg = dbg;
-  int rc = attention_tc(tq, tkv, a, num_sms, s);
+  int rc = attention_tc(tq, tkv, a, hd, num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
+}
+
+// Backbone self-attention on a packed QKV buffer [items * L, 3E].
+int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, int hd, int E, int num_sms,
+                   cudaStream_t s, int* dbg = nullptr) {
+  return attn_tc(qkv, 3 * E, 0, qkv, 3 * E, E, 2 * E, o, E, items, heads, L, L, hd, num_sms, s, dbg);
 }
 
 struct GemmW {
@@ -462,6 +472,20 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
   const int rows = sp.items * sp.Lq;
   LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
   RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
+  const int Lk = sp.kv16 == nullptr ? sp.Lq : sp.Lk;
+  if (tc_attention_enabled() && sp.kv_mod == 0 && attention_tc_supported(hd, Lk) &&
+      (sp.kv16 == nullptr || sp.kv_batch_stride == (long long)Lk * sp.kv_tok_stride)) {
+    // tcgen05 path: encoder self-attention (T x T) and decoder cross-attention (201 x T)
+    if (sp.kv16 == nullptr) {
+      RUN(gemm(m, h, rows, D, w.kv, EPI_F16, epi_out(kv, 2 * D), s));
+      m->launches++;
+      RUN(attn_tc(q, D, 0, kv, 2 * D, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
+    } else {
+      m->launches++;
+      RUN(attn_tc(q, D, 0, sp.kv16, sp.kv_tok_stride, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
+    }
+    return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+  }
   AttnArgs a = attn_base(H, hd);
   a.q = q;
   a.q_tok_stride = D;

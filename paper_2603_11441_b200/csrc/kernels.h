@@ -78,7 +78,7 @@ int attention(const AttnArgs& a, int head_dim, cudaStream_t stream);
 
 // tcgen05 flash attention over contiguous row blocks of a token-major QKV buffer.
 struct AttnTcArgs {
-  int L;                       // rows per item (window or image); multiple of 192
+  int Lq, Lkv;                 // query / key rows per item; Lkv a multiple of attention_tc_kv_tile(hd)
   int heads, items;
   int q_col, k_col, v_col;     // column offsets of q / k / v in the QKV buffer
   __half* o;                   // [items * L, o_ld]
@@ -86,9 +86,11 @@ struct AttnTcArgs {
   float scale_log2;
   int* dbg = nullptr;          // host-mapped hang report (tests only), see mbar_wait_dbg
 };
-bool attention_tc_supported(int head_dim, int L);
-// tmQ: 2-D map over QKV [rows, cols] fp16, box {16, 128}, 32B swizzle; tmKV: same, box {16, 192}.
-int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms,
+int attention_tc_kv_tile(int head_dim);  // 192 (hd 80), 96 (hd 16), 0 = unsupported
+bool attention_tc_supported(int head_dim, int Lkv);
+// tmQ: 2-D map over the Q buffer [items*Lq, cols] fp16, box {16, 128}, 32B swizzle;
+// tmKV: map over the K/V buffer [items*Lkv, cols], box {16, kv_tile}.
+int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream);
 
 // Row kernels.

@@ -145,10 +145,10 @@ def test_attention_windowed(lib, hd, grid, win, heads):
     assert float((o.float() - ow).abs().max()) < 1e-2
 
 
-@pytest.mark.parametrize("items,L", [(2, 576), (1, 5184), (9, 576)])
-def test_attention_tcgen05_packed_qkv(lib, items, L):
-    """tcgen05/TMEM flash attention (hd 80) on the backbone's packed QKV layout vs fp32 torch."""
-    H, hd = 16, 80
+@pytest.mark.parametrize("items,L,hd", [(2, 576, 80), (1, 5184, 80), (9, 576, 80), (2, 5184, 16), (3, 576, 16)])
+def test_attention_tcgen05_packed_qkv(lib, items, L, hd):
+    """tcgen05/TMEM flash attention (hd 80 backbone, hd 16 enc-dec) on a packed QKV layout vs fp32 torch."""
+    H = 16
     E = H * hd
     g = torch.Generator(device="cuda").manual_seed(L + items)
     qkv = (torch.randn(items, L, 3, H, hd, device="cuda", generator=g) * 2).half()
