@@ -94,13 +94,20 @@ int dart_postprocess(dart_model* m, const double* boxes, const double* score_log
 /* Kernel-level entry points (used by the per-kernel parity tests and microbenchmarks).
  * dart_gemm: out = epilogue(A[M,K] . W[N,K]^T + bias), A/W fp16 K-major, K % 64 == 0,
  *   N % 64 == 0; epi 0 fp16 out, 1 fp16 relu, 2 fp32 out, 3 fp32 out += , 4 fp16 with RoPE on
- *   columns < rope_cols (tables [rope_T, rope_hd/2]), 5 fp32 out + fp16 out2.
+ *   columns < rope_cols (the model's 2-D RoPE tables [rope_T, rope_hd/2] = row | column angles,
+ *   rope_T a square grid <= 72^2, rope_hd / 4 <= 20), 5 fp32 out + fp16 out2.
+ * dart_gemm_plan: the tile plan dart_gemm / the model forwards use for (M, N, epi) on this GPU
+ *   (bn = tile width, cg = 1: 128-row tiles per SM, 2: 256-row tiles per CTA pair).
+ * dart_gemm_force_plan: force (bn, cg) for every later GEMM whose N allows it (tests and A/B
+ *   measurement); bn = 0 restores the automatic plan.
  * dart_attention: o = softmax(q k^T / sqrt(hd)) v, fp16 in/out, tokens `*_tok_stride`
  *   elements apart, heads hd apart, batch items `*_batch_stride` apart; win > 0 selects the
  *   windowed token map over a grid x grid token image (batch = images * (grid/win)^2). */
 int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* out2, int32_t M, int32_t N,
               int32_t K, int32_t epi, const float* rope_cos, const float* rope_sin, int32_t rope_T, int32_t rope_hd,
               int32_t rope_cols, void* stream);
+void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
+void dart_gemm_force_plan(int32_t bn, int32_t cg);
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
                    int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,
                    int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,

@@ -28,6 +28,8 @@ EXPORTS = (
     "dart_encdec",
     "dart_postprocess",
     "dart_gemm",
+    "dart_gemm_plan",
+    "dart_gemm_force_plan",
     "dart_attention",
     "dart_attention_qkv",
     "dart_launch_count",
@@ -94,6 +96,10 @@ def load() -> ctypes.CDLL:
     lib.dart_postprocess.restype = ctypes.c_int
     lib.dart_gemm.argtypes = [P, P, P, P, P, I32, I32, I32, I32, P, P, I32, I32, I32, P]
     lib.dart_gemm.restype = ctypes.c_int
+    lib.dart_gemm_plan.argtypes = [I32, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
+    lib.dart_gemm_plan.restype = None
+    lib.dart_gemm_force_plan.argtypes = [I32, I32]
+    lib.dart_gemm_force_plan.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int64, I32, I32, P]
     lib.dart_attention.restype = ctypes.c_int

@@ -10,6 +10,7 @@
 //   backbone  residual stream x [B*T, E] fp32; LN outputs / qkv / attention out / MLP hidden fp16.
 //   enc-dec   class-shared prefix e1 [B*T, d] fp32; per-class residual e [B*N*T, d] fp32;
 //             decoder memory K/V for all layers [B*N*T, 6*2d] fp16; decoder stream [B*N*201, d] fp32.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -135,9 +136,9 @@ struct GemmW {
   __half* w = nullptr;  // [N, K] fp16
   float* b = nullptr;   // [N]
   int N = 0, K = 0;
-  CUtensorMap tmap[3];  // box rows 256 / 128 / 64 (index = bn_slot(BN)), built where N allows
+  CUtensorMap tmap[4];  // box rows 256 / 128 / 64 / 32 (index = box_slot(rows)), built where N allows
 };
-inline int bn_slot(int bn) { return bn == 256 ? 0 : bn == 128 ? 1 : 2; }
+inline int box_slot(int rows) { return rows == 256 ? 0 : rows == 128 ? 1 : rows == 64 ? 2 : 3; }
 struct LNW {
   float* g = nullptr;
   float* b = nullptr;
@@ -257,9 +258,9 @@ bool upload_wT(dart_model* m, const float* h, int in, int out, __half* dst, int 
 
 bool finish_gemmw(GemmW& g) {
   bool any = false;
-  for (int bn = 256; bn >= 64; bn >>= 1) {
-    if (g.N % bn) continue;
-    if (!make_tmap(&g.tmap[bn_slot(bn)], g.w, g.K, g.N, g.K, bn)) return false;
+  for (int rows = 256; rows >= 32; rows >>= 1) {  // W box rows = plan.bn / plan.cg
+    if (g.N % rows) continue;
+    if (!make_tmap(&g.tmap[box_slot(rows)], g.w, g.K, g.N, g.K, rows)) return false;
     any = true;
   }
   return any;
@@ -338,21 +339,25 @@ int check_desc(const dart_model_desc* d) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+// Output tensor maps of a GEMM epilogue (see gemm_tc): fp32 box 32x32 SW128, fp16 box 32x32 SW64.
+bool make_out_maps(int epi, const GemmEpi& e, int M, int N, CUtensorMap* tc, CUtensorMap* td) {
+  if (epi == EPI_F32_RESID || (epi == EPI_F32 && !e.wm_scatter))
+    return make_tmap_f32(tc, e.out, N, M, e.ldo);
+  if (epi == EPI_F16 || epi == EPI_F16_RELU || epi == EPI_QKV_ROPE)
+    return make_tmap_ex(td, e.out, N, M, e.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  return true;
+}
+
 int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi, GemmEpi e, cudaStream_t s) {
   if (M <= 0) return 0;
   CUtensorMap ta;
   if (!make_tmap(&ta, A, W.K, M, lda, 128)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (A)");
   if (e.bias == nullptr) e.bias = W.b;
   m->launches++;
-  CUtensorMap tc;
-  int bn;
-  if (epi == EPI_F32_RESID) {
-    bn = gemm_resid_bn(W.N);
-    if (!make_tmap_f32(&tc, e.out, W.N, M, e.ldo)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (C)");
-  } else {
-    bn = gemm_pick_bn(M, W.N, m->num_sms);
-  }
-  int rc = gemm_tc(ta, W.tmap[bn_slot(bn)], &tc, M, W.N, W.K, bn, epi, e, m->num_sms, s);
+  CUtensorMap tc, td;
+  if (!make_out_maps(epi, e, M, W.N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
+  const GemmPlan plan = gemm_plan(M, W.N, epi, m->num_sms);
+  int rc = gemm_tc(ta, W.tmap[box_slot(plan.bn / plan.cg)], &tc, &td, M, W.N, W.K, plan, epi, e, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
 }
@@ -677,6 +682,7 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
       e.rope_cos = m->rope_cos;
       e.rope_sin = m->rope_sin;
       e.rope_T = T;
+      e.rope_grid = G;
       e.rope_hd = hd;
       e.rope_cols = 2 * E;  // q and k
       e.wm_grid = G;
@@ -853,10 +859,9 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int bn = epi == EPI_F32_RESID ? gemm_resid_bn(N) : gemm_pick_bn(M, N, sms);
+  const GemmPlan plan = gemm_plan(M, N, epi, sms);
   CUtensorMap ta, tb, tc;
-  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, bn) ||
-      (epi == EPI_F32_RESID && !make_tmap_f32(&tc, out, N, M, N)))
+  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, plan.bn / plan.cg))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   GemmEpi e;
   e.bias = bias;
@@ -867,12 +872,27 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.rope_cos = rope_cos;
   e.rope_sin = rope_sin;
   e.rope_T = rope_T > 0 ? rope_T : 1;
+  e.rope_grid = (int)lround(sqrt((double)e.rope_T));
   e.rope_hd = rope_hd > 0 ? rope_hd : 2;
   e.rope_cols = rope_cols;
-  int rc = gemm_tc(ta, tb, &tc, M, N, K, bn, epi, e, sms, (cudaStream_t)stream);
+  e.dbg_noload = getenv("DART_GEMM_NOLOAD") != nullptr;
+  CUtensorMap td;
+  if (!make_out_maps(epi, e, M, N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
+  int rc = gemm_tc(ta, tb, &tc, &td, M, N, K, plan, epi, e, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }
+
+void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const GemmPlan p = gemm_plan(M, N, epi, sms);
+  if (bn) *bn = p.bn;
+  if (cg) *cg = p.cg;
+}
+
+void dart_gemm_force_plan(int32_t bn, int32_t cg) { gemm_force_plan(bn, cg); }
 
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
                    int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,

@@ -2,12 +2,21 @@
 //
 // Replaces every `_linear` on the DART hot path (reference model.py:356-358:
 // y = x @ W + b with W stored [in, out]; here W is stored transposed [out, in] so
-// both operands are K-major).  Warp roles (256 threads, 1 CTA per SM):
-//   warp 0  TMA producer  (A 128x64 and W BNx64 fp16 tiles, 128B swizzle, STAGES-deep ring)
-//   warp 1  MMA issuer    (one thread, tcgen05.mma.cta_group::1.kind::f16, fp32 accumulators in TMEM)
+// both operands are K-major).  Warp roles (384 threads, 1 CTA per SM):
+//   warp 0  TMA producer  (A 128x64 and W (BN/CG)x64 fp16 tiles, 128B swizzle, STAGES-deep ring)
+//   warp 1  MMA issuer    (one thread, tcgen05.mma.cta_group::CG.kind::f16, fp32 accumulators in TMEM)
 //   warp 2  TMEM allocator
-//   warps 4-7 epilogue    (tcgen05.ld -> bias / ReLU / residual / RoPE -> global)
+//   warps 4-11 epilogue   (two per TMEM lane quarter, alternating 32-column chunks: tcgen05.ld ->
+//                          bias / ReLU / RoPE / residual -> swizzled smem chunk -> TMA bulk store;
+//                          the residual chunk is TMA-prefetched one chunk ahead)
 // Two TMEM accumulator buffers let the epilogue of tile i overlap the MMAs of tile i+1.
+//
+// CG = 2 is the CTA-pair ("2-SM") form: a cluster of 2 CTAs on one TPC computes a 256 x BN
+// tile with M=256 tcgen05.mma.cta_group::2 issued by the leader CTA.  Each CTA loads its own
+// 128 rows of A and HALF of the BN rows of W, so the smem / L2 operand traffic per FLOP is
+// 25-33% lower than the 1-SM form; both CTAs' TMA loads complete on the leader's full barrier,
+// MMA completion is multicast to both CTAs' empty / accumulator-full barriers, and both CTAs'
+// epilogue warps release the accumulator on the leader's barrier.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -17,34 +26,114 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 fp16 = 128 B = one swizzle atom row
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the leader CTA's copy
+constexpr int ROPE_PAD = 21;                 // float2 row stride of the small RoPE tables (bank spread)
+constexpr int ROPE_MAX_GRID = 72;
+constexpr int ROPE_MAX_Q = 20;               // hd / 4
 
-template <int BN, int STAGES, bool RESID = false>
+template <int BN, int STAGES, int EPI, int CG>
 struct GemmSmem {
+  static constexpr int B_ROWS = BN / CG;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 4 epilogue staging buffers of 4 KB
-  static constexpr int RES_OFF = EPI_OFF + 4 * 4096;    // residual tile (RESID epilogue only)
-  static constexpr int BAR_OFF = RES_OFF + (RESID ? BM * BN * 4 : 0);
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x 2 staging buffers of 4 KB (32x32 fp32)
+  static constexpr int ROPE_OFF = EPI_OFF + 16 * 4096;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
+  static constexpr int ROPE_BYTES = EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0;
+  static constexpr int BAR_OFF = ROPE_OFF + ROPE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
+  static constexpr bool RESID = EPI == EPI_F32_RESID;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static_assert(TOTAL <= 227 * 1024, "shared memory budget");
 };
 
-__device__ __forceinline__ void store_f16x32(act_t* dst, const float* v) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion is signalled on the LEADER CTA's barrier (CTA-pair form).
+__device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void umma_f16_cg(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  if constexpr (CG == 1) {
+    umma_f16(tmem_d, a_desc, b_desc, idesc, accumulate);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+  }
+}
+// MMA completion -> barrier at the same smem offset in every CTA of the pair (or the own CTA).
+template <int CG>
+__device__ __forceinline__ void umma_commit_cg(uint64_t* bar) {
+  if constexpr (CG == 1) {
+    umma_commit(bar);
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+}
+// Arrive on the leader CTA's copy of `bar` (rank 0 of the pair).
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+template <int NCOLS, int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* smem_dst) {
+  if constexpr (CG == 1) {
+    tmem_alloc<NCOLS>(smem_dst);
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+                 "n"(NCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+}
+template <int NCOLS, int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t base) {
+  if constexpr (CG == 1) {
+    tmem_dealloc<NCOLS>(base);
+  } else {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(NCOLS) : "memory");
+  }
+}
+
+// 2-D RoPE (reference tensors.py:235-252, model.py:203-213) on a 32-column chunk of this
+// lane's row: pair p of head-local columns (2p, 2p+1) rotates by the row-coordinate angle for
+// p < hd/4 and by the column-coordinate angle otherwise.  `rt` / `ct` point at this token's
+// row of the small per-coordinate tables [coord][ROPE_PAD] of (cos, sin).
+__device__ __forceinline__ void rope_chunk(float* v, int col, int hd, const float2* rt, const float2* ct) {
+  const int q = hd >> 2, half = hd >> 1;
+  int p = (col % hd) >> 1;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 u;
-    u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
-    u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
-    u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
-    u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
-    d[q] = u;
+  for (int j = 0; j < 32; j += 2) {
+    const float2 cs = p < q ? rt[p] : ct[p - q];
+    const float ev = v[j], od = v[j + 1];
+    v[j] = ev * cs.x - od * cs.y;
+    v[j + 1] = ev * cs.y + od * cs.x;
+    p = (p + 1 == half) ? 0 : p + 1;
   }
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const GemmEpi& e, int rope_tok) {
+__device__ __forceinline__ void epilogue_bias_act(float* v, int col, const GemmEpi& e) {
   if (e.bias != nullptr) {
     const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
 #pragma unroll
@@ -59,23 +148,6 @@ __device__ __forceinline__ void epilogue_chunk(float* v, int row, int col, const
   if (EPI == EPI_F16_RELU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
-  }
-  if (EPI == EPI_QKV_ROPE) {
-    if (col < e.rope_cols) {
-      // rope_tok: this row's true token (computed once per tile row by the caller)
-      const int half_hd = e.rope_hd >> 1;
-      const float* ct = e.rope_cos + (size_t)rope_tok * half_hd;
-      const float* st = e.rope_sin + (size_t)rope_tok * half_hd;
-      int p = (col % e.rope_hd) >> 1;  // pair index within the head, wraps at half_hd
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float c = __ldg(ct + p), s = __ldg(st + p);
-        const float ev = v[j], od = v[j + 1];
-        v[j] = ev * c - od * s;
-        v[j + 1] = ev * s + od * c;
-        p = (p + 1 == half_hd) ? 0 : p + 1;
-      }
-    }
   }
 }
 
@@ -100,34 +172,13 @@ __device__ __forceinline__ int chunk_dst_row(int row, const GemmEpi& e) {
   return row;
 }
 
-// Write the warp's chunk of fp32 values (v = this lane's row) to out (+= residual if RESID).
-template <bool RESID>
+// Write the warp's chunk of fp32 values (v = this lane's row) to out.
 __device__ __forceinline__ void chunk_store_f32(float* buf, const float* v, float* out, int ldo, int row0, int col,
                                                 int M, const GemmEpi& e) {
   const int lane = threadIdx.x & 31;
   const int sub = lane >> 3, k = lane & 7;  // coalesced phase: 4 rows x 8 slots per instruction
-  if (RESID) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = i * 4 + sub;
-      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row0 + r < M) x = *reinterpret_cast<const float4*>(out + (size_t)(row0 + r) * ldo + col + 4 * k);
-      *slot32(buf, r, k) = x;
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    if (RESID) {
-      const float4 x = *slot32(buf, lane, q);
-      o.x += x.x;
-      o.y += x.y;
-      o.z += x.z;
-      o.w += x.w;
-    }
-    *slot32(buf, lane, q) = o;
-  }
+  for (int q = 0; q < 8; ++q) *slot32(buf, lane, q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -161,64 +212,41 @@ __device__ __forceinline__ void chunk_store_f16(float* buf, const float* v, act_
   __syncwarp();
 }
 
-template <int EPI>
-__device__ __forceinline__ void epilogue_store(float* buf, const float* v, int row0, int col, int M,
-                                               const GemmEpi& e) {
-  if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) {
-    chunk_store_f16(buf, v, reinterpret_cast<act_t*>(e.out), e.ldo, row0, col, M, e);
-  } else if (EPI == EPI_F32 || EPI == EPI_F32_F16) {
-    chunk_store_f32<false>(buf, v, reinterpret_cast<float*>(e.out), e.ldo, row0, col, M, e);
-    if (EPI == EPI_F32_F16) chunk_store_f16(buf, v, reinterpret_cast<act_t*>(e.out2), e.ldo2, row0, col, M, e);
-  } else if (EPI == EPI_F32_RESID) {
-    chunk_store_f32<true>(buf, v, reinterpret_cast<float*>(e.out), e.ldo, row0, col, M, e);
-  }
+// fp16 32x32 chunk slot under the TMA 64-byte swizzle (64 B rows, 16 B slot k of row r at
+// k ^ ((r >> 1) & 3)): conflict-free for the row-per-lane writes.
+__device__ __forceinline__ uint4* slot16_sw64(float* buf, int r, int k) {
+  return reinterpret_cast<uint4*>(buf) + r * 4 + (k ^ ((r >> 1) & 3));
 }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Residual epilogue (EPI_F32_RESID, BN <= 128): warp 3 TMA-loads the tile's fp32 residual
-// [128 x BN] into smem (32x32 boxes, 128B swizzle == slot32 layout) while the MMAs run; each
-// epilogue warp adds its accumulator chunk in place and TMA-stores the chunk back.
-template <int EPI>
-__device__ __forceinline__ void resid_chunk(float* buf, const float* v, const CUtensorMap* tmC, int row0, int col) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float4* s = slot32(buf, lane, q);
-    float4 x = *s;
-    x.x += v[4 * q];
-    x.y += v[4 * q + 1];
-    x.z += v[4 * q + 2];
-    x.w += v[4 * q + 3];
-    *s = x;
-  }
-  fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy) store
-  __syncwarp();
-  if (lane == 0) {
-    tma_store_2d(tmC, buf, col, row0);
-    tma_store_commit();
-  }
-}
+constexpr int GEMM_THREADS = 384;
 
-template <int BN, int STAGES, int EPI>
-__global__ void __launch_bounds__(256, 1)
+template <int BN, int STAGES, int EPI, int CG>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi epi) {
-  using L = GemmSmem<BN, STAGES, EPI == EPI_F32_RESID>;
-  constexpr bool RESID = EPI == EPI_F32_RESID;
-  constexpr int CPW = BN / 32;  // 32-column chunks per epilogue warp and tile
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int M, int N,
+                   int K, GemmEpi epi) {
+  // tmC: fp32 [M, N] output / residual map (box 32x32, 128B swizzle); tmD: fp16 [M, N] output map
+  // (box 32x32, 64B swizzle).  Outputs leave through per-warp smem chunks and TMA bulk stores.
+  using L = GemmSmem<BN, STAGES, EPI, CG>;
+  constexpr bool RESID = L::RESID;
+  constexpr int CPW = BN / 64;  // 32-column chunks per epilogue warp and tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rfull = tempty + 2;
-  uint64_t* rempty = rfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 1);
-  float* resid = reinterpret_cast<float*>(smem + L::RES_OFF);  // [4 warps][CPW chunks][32 x 32]
+  uint64_t* rfull = tempty + 2;  // [8 warps][2 buffers]: residual chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 16);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int num_m = (M + BM - 1) / BM;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int cl = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
   const int nk = K / BK;
@@ -226,21 +254,34 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (RESID || EPI == EPI_F32) tma_prefetch_desc(&tmC);
+    if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8 * CG);
     }
-    mbar_init(rfull, 1);
-    mbar_init(rempty, 4);
+    for (int i = 0; i < 16; ++i) mbar_init(&rfull[i], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (EPI == EPI_QKV_ROPE && warp >= 4) {
+    // small per-coordinate RoPE tables from the [T, hd/2] tables: row angles of token (c, 0)
+    // (pairs < hd/4) and column angles of token (0, c) (pairs >= hd/4)
+    float2* rs = reinterpret_cast<float2*>(smem + L::ROPE_OFF);
+    const int g = epi.rope_grid, q = epi.rope_hd >> 2, half = epi.rope_hd >> 1;
+    for (int i = threadIdx.x - 128; i < 2 * g * q; i += GEMM_THREADS - 128) {
+      const int which = i / (g * q), c = (i / q) % g, f = i % q;
+      const size_t src = which == 0 ? (size_t)c * g * half + f : (size_t)c * half + q + f;
+      rs[(which * ROPE_MAX_GRID + c) * ROPE_PAD + f] = make_float2(epi.rope_cos[src], epi.rope_sin[src]);
+    }
+  }
+  if (warp == 2) tmem_alloc_cg<L::TMEM_COLS, CG>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -248,16 +289,24 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * BM;
-        const int n0 = (tile % num_n) * BN;
+      for (int tile = cl; tile < num_tiles; tile += ncl) {
+        const int m0 = (tile / num_n) * BM * CG + rank * BM;
+        const int n0 = (tile % num_n) * BN + rank * L::B_ROWS;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-          tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
+          if (epi.dbg_noload && (tile != cl || kb >= STAGES)) {
+            if (rank == 0) mbar_arrive(&full[stage]);
+          } else if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+            tma_load_2d_cg2(sa, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2d_cg2(sb, &tmB, &full[stage], kb * BK, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -266,12 +315,12 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(BM, BN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = cl; tile < num_tiles; tile += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -287,115 +336,200 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // advance 16 fp16 = 32 B along K inside the swizzle atom (encoded >> 4)
-            umma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            umma_f16_cg<CG>(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          umma_commit_cg<CG>(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
-      }
-    }
-  } else if (warp == 3) {
-    if (RESID && lane == 0) {  // residual prefetch, one tile ahead of the epilogue
-      int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        const int m0 = (tile / num_n) * BM;
-        const int n0 = (tile % num_n) * BN;
-        mbar_wait(rempty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(rfull, BM * BN * 4);
-        for (int q = 0; q < 4; ++q)
-          for (int c = 0; c < CPW; ++c)
-            tma_load_2d(resid + (q * CPW + c) * 1024, &tmC, rfull, n0 + 32 * c, m0 + 32 * q);
+        umma_commit_cg<CG>(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
-    const int quarter = warp & 3;
-    float* stage_buf = reinterpret_cast<float*>(smem + L::EPI_OFF) + quarter * 1024;  // 4 KB per warp
-    int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * 2048;  // 2 x 4 KB per warp
+    uint64_t* rbar = rfull + (warp - 4) * 2;
+    const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
+    // residual chunk g of this warp -> smem buffer g & 1 (lane 0 issues; one chunk ahead)
+    auto resid_load = [&](int g) {
+      const int t = cl + (g / CPW) * ncl;
+      if (t >= num_tiles) return;
+      const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
+      const int cc = (t % num_n) * BN + ((g % CPW) * 2 + half) * 32;
+      mbar_arrive_expect_tx(&rbar[g & 1], 32 * 32 * 4);
+      tma_load_2d(bufs + (g & 1) * 1024, &tmC, &rbar[g & 1], cc, rr);
+    };
+    if (RESID && lane == 0) resid_load(0);
+    int it = 0, g = 0;
+    for (int tile = cl; tile < num_tiles; tile += ncl, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile / num_n) * BM;
+      const int m0 = (tile / num_n) * BM * CG + rank * BM;
       const int n0 = (tile % num_n) * BN;
+      const int row0 = m0 + quarter * 32;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + quarter * 32 + lane;
+      const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      int rope_tok = 0;
+      const float2 *rt = nullptr, *ct = nullptr;
       if (EPI == EPI_QKV_ROPE) {
-        rope_tok = row % epi.rope_T;
-        if (epi.wm_grid > 0) rope_tok = wm_to_token(rope_tok, epi.wm_grid, epi.wm_win);
+        int tok = row % epi.rope_T;
+        if (epi.wm_grid > 0) tok = wm_to_token(tok, epi.wm_grid, epi.wm_win);
+        const int tr = tok / epi.rope_grid, tc = tok - tr * epi.rope_grid;
+        rt = rope_s + tr * ROPE_PAD;
+        ct = rope_s + (ROPE_MAX_GRID + tc) * ROPE_PAD;
       }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * 32; c < BN; c += 64, ++g) {
+        float* buf = bufs + (g & 1) * 1024;
+        if (lane == 0) {
+          if (RESID) {
+            bulk_wait_read0();  // store g-1 has read buffer (g+1)&1
+            resid_load(g + 1);
+          } else {
+            bulk_wait_read1();  // store g-2 has read this buffer
+          }
+        }
+        __syncwarp();
         float v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
-        if (c + 32 >= BN) {
-          // all accumulator columns of this buffer are in registers: hand TMEM back early
+        if (c + 64 >= BN) {
+          // all of this warp's accumulator columns are in registers: hand TMEM back early
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (CG == 1) {
+              mbar_arrive(&tempty[acc]);
+            } else {
+              mbar_arrive_leader(&tempty[acc]);
+            }
+          }
         }
-        epilogue_chunk<EPI>(v, row, n0 + c, epi, rope_tok);
+        epilogue_bias_act<EPI>(v, n0 + c, epi);
+        if (EPI == EPI_QKV_ROPE && n0 + c < epi.rope_cols) rope_chunk(v, n0 + c, epi.rope_hd, rt, ct);
+        if ((EPI == EPI_F32 && epi.wm_scatter) || EPI == EPI_F32_F16) {  // row scatter / 2 outputs: plain stores
+          chunk_store_f32(buf, v, reinterpret_cast<float*>(epi.out), epi.ldo, row0, n0 + c, M, epi);
+          if (EPI == EPI_F32_F16)
+            chunk_store_f16(buf, v, reinterpret_cast<act_t*>(epi.out2), epi.ldo2, row0, n0 + c, M, epi);
+          continue;
+        }
         if constexpr (RESID) {
-          if (c == 0) mbar_wait(rfull, it & 1);
-          resid_chunk<EPI>(resid + (quarter * CPW + c / 32) * 1024, v, &tmC, m0 + quarter * 32, n0 + c);
+          mbar_wait(&rbar[g & 1], (g >> 1) & 1);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4* sp = slot32(buf, lane, q);
+            float4 x = *sp;
+            x.x += v[4 * q];
+            x.y += v[4 * q + 1];
+            x.z += v[4 * q + 2];
+            x.w += v[4 * q + 3];
+            *sp = x;
+          }
+        } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_F16) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *slot32(buf, lane, q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
-          epilogue_store<EPI>(stage_buf, v, m0 + quarter * 32, n0 + c, M, epi);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
+            u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
+            u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
+            u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
+            *slot16_sw64(buf, lane, q) = u;
+          }
         }
-      }
-      if constexpr (RESID) {  // residual buffer reusable once the TMA stores have read it
+        fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy) store
+        __syncwarp();
         if (lane == 0) {
-          tma_store_wait_read0();
-          mbar_arrive(rempty);
+          if (RESID || EPI == EPI_F32 || EPI == EPI_F32_F16)
+            tma_store_2d(&tmC, buf, n0 + c, row0);
+          else
+            tma_store_2d(&tmD, buf, n0 + c, row0);
+          tma_store_commit();
         }
       }
     }
-    if constexpr (RESID) {
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes landed
-    }
+    if (lane == 0) bulk_wait_all();  // output writes landed before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // the peer's MMAs / arrivals are done
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<L::TMEM_COLS>(tmem_base);
+    tmem_dealloc_cg<L::TMEM_COLS, CG>(tmem_base);
   }
 }
 
-template <int BN, int STAGES, int EPI>
-int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, int M, int N, int K,
-                const GemmEpi& epi, int num_sms, cudaStream_t stream) {
-  using L = GemmSmem<BN, STAGES, EPI == EPI_F32_RESID>;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI>;
+template <int BN, int STAGES, int EPI, int CG>
+int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, const CUtensorMap& tD, int M,
+                int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES, EPI, CG>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, 256, L::TOTAL, stream>>>(tA, tB, tC, M, N, K, epi);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN);
+  const int units = num_sms / CG;
+  const int grid = (tiles < units ? tiles : units) * CG;
+  if constexpr (CG == 1) {
+    kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(tA, tB, tC, tD, M, N, K, epi);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, M, N, K, epi);
+    if (e != cudaSuccess) return (int)e;
+  }
   return (int)cudaGetLastError();
 }
 
-template <int BN, int STAGES>
-int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, int M, int N,
-                 int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+// Deepest operand ring that fits 227 KB next to the epilogue staging (and RoPE tables).
+template <int BN, int EPI, int CG>
+constexpr int stages_for() {
+  constexpr int stage = BM * BK * 2 + (BN / CG) * BK * 2;
+  constexpr int fixed = 16 * 4096 + (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) + 256 + 1024;
+  constexpr int n = (227 * 1024 - fixed) / stage;
+  return n > 8 ? 8 : n;
+}
+
+template <int BN, int EPI, int CG>
+int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, const CUtensorMap& tD, int M,
+                   int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+}
+
+template <int BN, int CG>
+int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
+                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   switch (epi_mode) {
-    case EPI_F16: return launch_gemm<BN, STAGES, EPI_F16>(tA, tB, tC, M, N, K, epi, num_sms, stream);
-    case EPI_F16_RELU: return launch_gemm<BN, STAGES, EPI_F16_RELU>(tA, tB, tC, M, N, K, epi, num_sms, stream);
-    case EPI_F32: return launch_gemm<BN, STAGES, EPI_F32>(tA, tB, tC, M, N, K, epi, num_sms, stream);
-    case EPI_QKV_ROPE: return launch_gemm<BN, STAGES, EPI_QKV_ROPE>(tA, tB, tC, M, N, K, epi, num_sms, stream);
-    case EPI_F32_F16: return launch_gemm<BN, STAGES, EPI_F32_F16>(tA, tB, tC, M, N, K, epi, num_sms, stream);
+    case EPI_F16: return launch_planned<BN, EPI_F16, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F16_RELU: return launch_planned<BN, EPI_F16_RELU, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32: return launch_planned<BN, EPI_F32, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_RESID: return launch_planned<BN, EPI_F32_RESID, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_QKV_ROPE: return launch_planned<BN, EPI_QKV_ROPE, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_F16: return launch_planned<BN, EPI_F32_F16, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
   }
   return (int)cudaErrorInvalidValue;
 }
+
+GemmPlan g_forced{0, 0};  // dart_gemm_force_plan (tests / A-B measurement); bn 0 = automatic
 
 }  // namespace
 
@@ -406,43 +540,63 @@ int gemm_bn_for(int N) {
   return 0;
 }
 
-// Tile width minimising wave-quantised work: cost = waves(tiles / SMs) * (BN + 32), where the
-// +32 charges per-tile fixed cost (epilogue drain, A re-reads).  E.g. M=5184, N=1280 picks 128
-// (410 tiles = 2.8 waves) over 256 (205 tiles = 1.4 waves).
-int gemm_pick_bn(int M, int N, int num_sms) {
-  int best = 0;
-  long long best_cost = 0;
-  for (int bn = 256; bn >= 64; bn >>= 1) {
-    if (N % bn) continue;
-    const long long tiles = (long long)((M + BM - 1) / BM) * (N / bn);
-    const long long waves = (tiles + num_sms - 1) / num_sms;
-    const long long cost = waves * (bn + 32);
-    if (best == 0 || cost < best_cost) {
-      best = bn;
-      best_cost = cost;
+// Tile plan minimising wave-quantised work.  Candidates: 1-SM 128 x BN tiles on every SM and
+// 2-SM 256 x BN tiles on SM pairs.  cost = waves * BN / eff(BN): narrow tiles pay for operand
+// re-reads (measured MMA efficiency relative to BN = 256 on B200: 0.66 at 128, 0.45 at 64);
+// the CTA-pair form wins ties (lower operand traffic per FLOP).
+GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
+  (void)epi_mode;
+  GemmPlan best{0, 1};
+  double best_cost = 0;
+  for (int cg = 2; cg >= 1; --cg) {
+    for (int bn = 256; bn >= 64; bn >>= 1) {
+      if (N % bn) continue;
+      const long long tiles = (long long)((M + BM * cg - 1) / (BM * cg)) * (N / bn);
+      const long long units = num_sms / cg;
+      const long long waves = (tiles + units - 1) / units;
+      const double eff = bn == 256 ? 1.0 : bn == 128 ? 0.66 : 0.45;
+      const double cost = (double)waves * bn / eff * (cg == 2 ? 0.97 : 1.0);
+      if (best.bn == 0 || cost < best_cost) {
+        best = GemmPlan{bn, cg};
+        best_cost = cost;
+      }
     }
   }
+  const GemmPlan o = g_forced;
+  if (o.bn > 0 && N % o.bn == 0) best = o;
   return best;
 }
 
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, int M, int N, int K, int BN,
-            int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+void gemm_force_plan(int bn, int cg) { g_forced = GemmPlan{bn, cg == 2 ? 2 : 1}; }
+
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, const CUtensorMap* tD, int M, int N,
+            int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (M <= 0) return 0;
+  const int BN = plan.bn;
   if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
-  if (epi_mode == EPI_F32_RESID) {  // TMA residual epilogue: BN <= 128, fewer mainloop stages
-    if (!tC) return (int)cudaErrorInvalidValue;
-    if (BN == 128) return launch_gemm<128, 4, EPI_F32_RESID>(tA, tB, *tC, M, N, K, epi, num_sms, stream);
-    if (BN == 64) return launch_gemm<64, 6, EPI_F32_RESID>(tA, tB, *tC, M, N, K, epi, num_sms, stream);
+  if (epi_mode == EPI_QKV_ROPE && (epi.rope_grid <= 0 || epi.rope_grid > ROPE_MAX_GRID ||
+                                   epi.rope_grid * epi.rope_grid != epi.rope_T || epi.rope_hd % 4 != 0 ||
+                                   epi.rope_hd / 4 > ROPE_MAX_Q))
     return (int)cudaErrorInvalidValue;
-  }
-  switch (BN) {
-    case 256: return dispatch_epi<256, 4>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
-    case 128: return dispatch_epi<128, 6>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
-    case 64: return dispatch_epi<64, 8>(epi_mode, tA, tB, tA, M, N, K, epi, num_sms, stream);
+  const bool f32_out = epi_mode == EPI_F32_RESID || (epi_mode == EPI_F32 && !epi.wm_scatter);
+  const bool f16_out = epi_mode == EPI_F16 || epi_mode == EPI_F16_RELU || epi_mode == EPI_QKV_ROPE;
+  if ((f32_out && !tC) || (f16_out && !tD)) return (int)cudaErrorInvalidValue;
+  const CUtensorMap& c = tC ? *tC : tA;
+  const CUtensorMap& d = tD ? *tD : tA;
+  if (plan.cg == 2) {
+    switch (BN) {
+      case 256: return dispatch_epi<256, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 128: return dispatch_epi<128, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 64: return dispatch_epi<64, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+    }
+  } else {
+    switch (BN) {
+      case 256: return dispatch_epi<256, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 128: return dispatch_epi<128, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 64: return dispatch_epi<64, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+    }
   }
   return (int)cudaErrorInvalidValue;
 }
-
-int gemm_resid_bn(int N) { return N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : 0); }
 
 }  // namespace dart

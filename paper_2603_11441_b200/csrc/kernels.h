@@ -24,7 +24,8 @@ struct GemmEpi {
   int ldo2 = 0;
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
-  int rope_T = 1;
+  int rope_T = 1;     // tokens per image (rows repeat with period rope_T)
+  int rope_grid = 0;  // sqrt(rope_T): the tables are the reference's 2-D RoPE (row | column angles)
   int rope_hd = 2;
   int rope_cols = 0;
   // Window-major row order (grid x grid tokens, win x win windows): rows are stored window by
@@ -33,6 +34,7 @@ struct GemmEpi {
   int wm_grid = 0;
   int wm_win = 0;
   int wm_scatter = 0;
+  int dbg_noload = 0;  // microbenchmarks only: after the first ring fill, stages are re-used without TMA
 };
 
 // window-major row index <-> token index within one image
@@ -47,13 +49,18 @@ __host__ __device__ inline int token_to_wm(int t, int grid, int win) {
 }
 
 int gemm_bn_for(int N);
-int gemm_pick_bn(int M, int N, int num_sms);
-// tB must be a tensor map over W [N, K] with box {64, BN}.  EPI_F32_RESID additionally needs
-// tC: fp32 map over the residual/output [M, N] (row stride ldo) with box {32, 32}, 128B swizzle,
-// and BN = gemm_resid_bn(N).
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, int M, int N, int K, int BN,
-            int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream);
-int gemm_resid_bn(int N);
+// Tile plan: 128 x bn tiles per SM (cg 1) or 256 x bn tiles per CTA pair (cg 2).
+struct GemmPlan {
+  int bn, cg;
+};
+GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms);
+void gemm_force_plan(int bn, int cg);  // bn 0: automatic
+// tA: map over A [M, K] with box {64, 128}; tB: map over W [N, K] with box {64, plan.bn / plan.cg}.
+// Output maps over out [M, N] (row stride ldo), box {32, 32}: tC fp32 with 128B swizzle
+// (EPI_F32 / EPI_F32_F16 without wm_scatter, and the EPI_F32_RESID residual), tD fp16 with 64B
+// swizzle (EPI_F16, EPI_F16_RELU, EPI_QKV_ROPE); the unused one may be null.
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, const CUtensorMap* tD, int M, int N,
+            int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream);
 
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {

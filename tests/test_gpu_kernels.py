@@ -79,26 +79,90 @@ def test_gemm_epilogues(lib, epi):
         assert rel_err(out, ref) < 1e-5 and rel_err(out2, ref) < 2e-3
 
 
-def test_gemm_rope_epilogue(lib):
+PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (128, 2), (64, 2)]
+
+
+@pytest.mark.parametrize("bn,cg", PLANS)
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 5])
+def test_gemm_forced_plans(lib, bn, cg, epi):
+    """Every tile plan (1-SM 128 x bn and CTA-pair 256 x bn tiles) and epilogue, with M and N tails
+    that leave partial 256-row tiles and several waves."""
+    if epi == 3 and bn > 128:
+        pytest.skip("the residual epilogue stages 128 x bn fp32 in smem: bn <= 128")
+    T, E = 576, 1280
+    M, N, K = (1700, 3840, 1280) if epi == 4 else (1333, 1536, 320)
+    g = torch.Generator(device="cuda").manual_seed(bn * 10 + cg + epi)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(N, device="cuda", generator=g)
+    ref = A.float() @ W.float().T + bias
+    lib.dart_gemm_force_plan(bn, cg)
+    try:
+        if epi in (0, 1):
+            out = torch.empty(M, N, device="cuda", dtype=torch.float16)
+            run_gemm(lib, A, W, bias, epi, out)
+            assert rel_err(out, ref.clamp_min(0) if epi == 1 else ref) < 2e-3
+        elif epi == 2:
+            out = torch.empty(M, N, device="cuda")
+            run_gemm(lib, A, W, bias, 2, out)
+            assert rel_err(out, ref) < 1e-5
+        elif epi == 3:
+            resid = torch.randn(M, N, device="cuda", generator=g)
+            out = resid.clone()
+            run_gemm(lib, A, W, bias, 3, out)
+            assert rel_err(out, ref + resid) < 1e-5
+        elif epi == 4:
+            hd, H = 80, 16
+            cos, sin = rope_tables(24, hd)
+            out = torch.empty(M, N, device="cuda", dtype=torch.float16)
+            run_gemm(lib, A, W, bias, 4, out, rope=(cos, sin, T, hd, 2 * E))
+            y = ref.reshape(M, 3, H, hd)
+            tok = torch.arange(M, device="cuda") % T
+            c, s = cos[tok][:, None, None, :], sin[tok][:, None, None, :]
+            rot = y.clone()
+            rot[:, :2, :, 0::2] = (y[..., 0::2] * c - y[..., 1::2] * s)[:, :2]
+            rot[:, :2, :, 1::2] = (y[..., 0::2] * s + y[..., 1::2] * c)[:, :2]
+            assert rel_err(out, rot.reshape(M, N)) < 2e-3
+        else:
+            out = torch.empty(M, N, device="cuda")
+            out2 = torch.empty(M, N, device="cuda", dtype=torch.float16)
+            run_gemm(lib, A, W, bias, 5, out, out2)
+            assert rel_err(out, ref) < 1e-5 and rel_err(out2, ref) < 2e-3
+    finally:
+        lib.dart_gemm_force_plan(0, 0)
+
+
+def rope_tables(grid, hd):
+    """The reference's 2-D RoPE tables (model.py:203-213): [T, hd/2] = [row angles | col angles]."""
+    q = hd // 4
+    inv = 100.0 ** (-torch.arange(q, dtype=torch.float64) / q)
+    r = torch.arange(grid, dtype=torch.float64).repeat_interleave(grid)
+    c = torch.arange(grid, dtype=torch.float64).repeat(grid)
+    ang = torch.cat([r[:, None] * inv, c[:, None] * inv], 1)
+    return torch.cos(ang).float().cuda().contiguous(), torch.sin(ang).float().cuda().contiguous()
+
+
+@pytest.mark.parametrize("T,M", [(576, 576), (5184, 5184), (576, 1152)])
+def test_gemm_rope_epilogue(lib, T, M):
     """QKV projection with RoPE on q and k (reference model.py:392-397, tensors.py:235-252)."""
-    T, E, H = 576, 1280, 16
+    E, H = 1280, 16
     hd = E // H
     g = torch.Generator(device="cuda").manual_seed(3)
-    A = torch.randn(T, E, device="cuda", generator=g).half()
+    A = torch.randn(M, E, device="cuda", generator=g).half()
     W = (torch.randn(3 * E, E, device="cuda", generator=g) / math.sqrt(E)).half()
     bias = torch.randn(3 * E, device="cuda", generator=g)
-    ang = torch.rand(T, hd // 2, device="cuda", generator=g) * 10
-    cos, sin = torch.cos(ang).contiguous(), torch.sin(ang).contiguous()
-    out = torch.empty(T, 3 * E, device="cuda", dtype=torch.float16)
+    cos, sin = rope_tables(int(round(T ** 0.5)), hd)
+    out = torch.empty(M, 3 * E, device="cuda", dtype=torch.float16)
     run_gemm(lib, A, W, bias, 4, out, rope=(cos, sin, T, hd, 2 * E))
-    y = (A.float() @ W.float().T + bias).reshape(T, 3, H, hd)
+    y = (A.float() @ W.float().T + bias).reshape(M, 3, H, hd)
     ev, od = y[..., 0::2], y[..., 1::2]
-    c, s = cos[:, None, None, :], sin[:, None, None, :]
+    tok = torch.arange(M, device="cuda") % T
+    c, s = cos[tok][:, None, None, :], sin[tok][:, None, None, :]
     rot = torch.empty_like(y)
     rot[..., 0::2] = ev * c - od * s
     rot[..., 1::2] = ev * s + od * c
     rot[:, 2] = y[:, 2]
-    assert rel_err(out, rot.reshape(T, 3 * E)) < 2e-3
+    assert rel_err(out, rot.reshape(M, 3 * E)) < 2e-3
 
 
 def ref_attention(q, k, v):
