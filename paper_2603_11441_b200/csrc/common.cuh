@@ -60,6 +60,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Pure spin on mbarrier.test_wait (no suspend): lowest wake-up latency for short waits.
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra SPIN_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 // Bounded wait for debugging protocol hangs: after ~2 s records (1, block, thread, tag, parity)
 // into host-mapped memory `dbg` and traps.  With dbg == nullptr it is a plain wait.
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
@@ -75,7 +87,11 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, volatile int* dbg) {
   if (dbg == nullptr) {
+#ifdef DART_SPIN_WAITS
+    mbar_spin(bar, parity);
+#else
     mbar_wait(bar, parity);
+#endif
     return;
   }
   const long long t0 = clock64();

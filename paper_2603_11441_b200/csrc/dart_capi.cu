@@ -121,6 +121,7 @@ int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv
   a.o_ld = o_ld;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.dbg = dbg;
+  a.softmax_only = getenv("DART_FA_SOFTMAX_ONLY") != nullptr;
   int rc = attention_tc(tq, tkv, a, hd, num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;

@@ -92,6 +92,7 @@ struct AttnTcArgs {
   int o_ld;
   float scale_log2;
   int* dbg = nullptr;          // host-mapped hang report (tests only), see mbar_wait_dbg
+  int softmax_only = 0;        // microbenchmark: softmax warps run on stale S without MMA / TMA
 };
 int attention_tc_kv_tile(int head_dim);  // 192 (hd 80), 96 (hd 16), 0 = unsupported
 bool attention_tc_supported(int head_dim, int Lkv);

@@ -40,15 +40,23 @@ __device__ __forceinline__ bool before(double sa, int qa, double sb, int qb) {
   return sa > sb || (sa == sb && qa < qb);
 }
 
+// One CTA per class.  Dynamic smem: scores [P] f64 | query ids [P] | candidate boxes [Q][4] f64 |
+// suppression masks [Q][W] u64 (W = ceil(Q/64)) | kept list [Q].
 __global__ void __launch_bounds__(PP_THREADS) pp_class_kernel(const double* __restrict__ boxes,
                                                               const double* __restrict__ score_logits,
                                                               const double* __restrict__ presence_logits, int Q,
                                                               double pthr, double sthr, double nthr, int* kept_count,
                                                               int* kept_query, double* kept_score,
                                                               double* presence_prob) {
-  __shared__ double ss[PP_MAXQ];
-  __shared__ int sq[PP_MAXQ];
-  __shared__ int kept[PP_MAXQ];
+  extern __shared__ __align__(16) uint8_t pp_smem[];
+  int P = 2;
+  while (P < Q) P <<= 1;
+  const int W = (Q + 63) >> 6;
+  double* ss = reinterpret_cast<double*>(pp_smem);
+  double* cb = ss + P;                                      // [Q][4]
+  uint64_t* mask = reinterpret_cast<uint64_t*>(cb + 4 * Q);  // [Q][W]
+  int* sq = reinterpret_cast<int*>(mask + (size_t)Q * W);    // [P]
+  int* kept = sq + P;                                       // [Q]
   __shared__ int nkept, ncand;
   __shared__ bool skip;
   const int c = blockIdx.x, tid = threadIdx.x;
@@ -64,8 +72,6 @@ __global__ void __launch_bounds__(PP_THREADS) pp_class_kernel(const double* __re
     if (tid == 0) kept_count[c] = 0;
     return;
   }
-  int P = 2;
-  while (P < Q) P <<= 1;
   for (int i = tid; i < P; i += PP_THREADS) {
     if (i < Q) {
       const double s = sigmoid_d(score_logits[(long long)c * Q + i]);
@@ -100,31 +106,42 @@ __global__ void __launch_bounds__(PP_THREADS) pp_class_kernel(const double* __re
       __syncthreads();
     }
   }
-  // greedy NMS over the ncand leading candidates
+  // candidate boxes in priority order, then the suppression matrix in parallel:
+  // bit k of row e (k < e) = !(IoU(e, k) < thr), the reference's test (pipeline.py:261)
   const int n = ncand;
   const double* bc = boxes + (long long)c * Q * 4;
-  for (int e = 0; e < n; ++e) {
-    double be[4];
-    const int qe = sq[e];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) be[j] = bc[qe * 4 + j];
-    bool sup = false;
-    for (int k = tid; k < nkept; k += PP_THREADS) {
-      double bk[4];
-      const int qk = sq[kept[k]];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bk[j] = bc[qk * 4 + j];
-      sup |= !(iou_d(be, bk) < nthr);
-    }
-    const bool any = __syncthreads_or(sup);
-    if (!any && tid == 0) kept[nkept++] = e;
-    __syncthreads();
+  for (int i = tid; i < n * 4; i += PP_THREADS) cb[i] = bc[sq[i >> 2] * 4 + (i & 3)];
+  __syncthreads();
+  for (int it = tid; it < n * W; it += PP_THREADS) {
+    const int e = it / W, w = it - e * W;
+    uint64_t m = 0;
+    const int k1 = min(e, 64 * w + 64);
+    for (int k = 64 * w; k < k1; ++k)
+      if (!(iou_d(cb + 4 * e, cb + 4 * k) < nthr)) m |= 1ull << (k - 64 * w);
+    mask[it] = m;
   }
-  for (int k = tid; k < nkept; k += PP_THREADS) {
+  __syncthreads();
+  // greedy pass in priority order (one warp): e survives iff no kept k suppresses it
+  if (tid < 32) {
+    uint64_t km = 0;  // lane w: kept bits of word w
+    int nk = 0;
+    for (int e = 0; e < n; ++e) {
+      const uint64_t m = tid < W ? mask[e * W + tid] : 0;
+      if (!__any_sync(0xffffffffu, (m & km) != 0)) {
+        if (tid == (e >> 6)) km |= 1ull << (e & 63);
+        if (tid == 0) kept[nk] = e;
+        ++nk;
+      }
+    }
+    if (tid == 0) nkept = nk;
+  }
+  __syncthreads();
+  const int nk = nkept;
+  for (int k = tid; k < nk; k += PP_THREADS) {
     kept_query[(long long)c * Q + k] = sq[kept[k]];
     kept_score[(long long)c * Q + k] = ss[kept[k]];
   }
-  if (tid == 0) kept_count[c] = nkept;
+  if (tid == 0) kept_count[c] = nk;
 }
 
 // Cross-class NMS over the per-class survivors (pipeline.py:289-293): order by
@@ -207,7 +224,14 @@ int postprocess_classes(const double* boxes, const double* score_logits, const d
                         double* kept_score, double* presence_prob, cudaStream_t stream) {
   if (N <= 0) return 0;
   if (Q > PP_MAXQ) return (int)cudaErrorInvalidValue;
-  pp_class_kernel<<<N, PP_THREADS, 0, stream>>>(boxes, score_logits, presence_logits, Q, presence_thr, score_thr,
+  int P = 2;
+  while (P < Q) P <<= 1;
+  const size_t smem = (size_t)P * 8 + (size_t)Q * 32 + (size_t)Q * ((Q + 63) / 64) * 8 + (size_t)P * 4 + (size_t)Q * 4;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pp_class_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  pp_class_kernel<<<N, PP_THREADS, smem, stream>>>(boxes, score_logits, presence_logits, Q, presence_thr, score_thr,
                                                 nms_thr, kept_count, kept_query, kept_score, presence_prob);
   return (int)cudaGetLastError();
 }

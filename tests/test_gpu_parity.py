@@ -142,7 +142,7 @@ def test_nms_survivors_random():
     cfg = D.PipelineConfig(score_threshold=0.0)
     for seed in range(40):
         rng = np.random.default_rng(seed)
-        n = int(rng.integers(1, 64))
+        n = int(rng.integers(1, 64)) if seed < 20 else int(rng.integers(64, 300))  # 1..5 mask words
         boxes = np.column_stack([rng.uniform(0.2, 0.8, n), rng.uniform(0.2, 0.8, n), rng.uniform(0.05, 0.4, n),
                                  rng.uniform(0.05, 0.4, n)])[None]
         scores = rng.uniform(-3, 3, (1, n))
