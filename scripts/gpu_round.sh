@@ -1,0 +1,10 @@
+#!/bin/bash
+# One GPU pass: gpu tests, N=4 / N=80 bench lines, N=4 launch list.
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench_n4.json 2> gpurun_out/bench_n4.err
+timeout 600 python bench.py --classes 80 --steps 10 --no-cpu-baseline > gpurun_out/bench_n80.json 2> gpurun_out/bench_n80.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n4.csv python scripts/profile_step.py --classes 4 > gpurun_out/prof_n4.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_n80.csv python scripts/profile_step.py --classes 80 > gpurun_out/prof_n80.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench_n4.json gpurun_out/bench_n80.json
