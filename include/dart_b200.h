@@ -119,6 +119,9 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
  * int32[8] that receives a protocol-hang report (tests only). */
 int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
                        int32_t* debug_host, void* stream);
+/* Tests: on != 0 makes every later tcgen05 attention launch re-run all of its items through the
+ * max-tracking softmax pass (the path items take when the fixed-reference pass overflows). */
+void dart_attention_force_safe(int32_t on);
 
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */

@@ -60,12 +60,30 @@ struct FaCfg {
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
   static constexpr int OFF_BAR = OFF_V + STAGES * V_BYTES;
   static constexpr int NBARS = 4 + 4 * STAGES + 3 * NS;
-  static constexpr int OFF_RED = OFF_BAR + NBARS * 8 + 16;  // [2][SPLIT][128] partial row maxima
+  static constexpr int OFF_OVF = OFF_BAR + NBARS * 8 + 16;         // overflow bitmask of local items
+  static constexpr int OVF_WORDS = ATTN_TC_MAX_LOCAL_ITEMS / 32;
+  static constexpr int OFF_RED = OFF_OVF + OVF_WORDS * 4;          // [2][SPLIT][128] partial row maxima
   static constexpr int TOTAL = OFF_RED + (SPLIT > 1 ? 2 * SPLIT * BQ * 4 : 0) + 1024;
   static_assert(TOTAL * CTAS <= 227 * 1024, "shared memory budget");
+  static_assert(COLS % 16 == 0, "a 16-key P.V step stays inside one softmax slice");
 };
 
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY>
+// Softmax numerics.  Pass 0 (every item): the reference max m of each row is taken over the
+// FIRST key tile only and kept for the whole row, so later tiles need no max, no vote and no O
+// rescale: P = 2^((s - m) c) may exceed 1.  fp16 P overflows (to inf) only if a later score
+// exceeds m by more than 16 / c; the fp32 row sum (ones column of O) is then not finite and
+// the item is marked in a per-CTA bitmask.  Pass 1 re-runs the marked items with the classic
+// per-tile running max and lazy rescale (P <= 2^8), overwriting their output rows.
+// SPIN bit 0: the MMA issuer spins on its barriers; bit 1: the softmax warps spin on S-ready.
+template <bool SPIN>
+__device__ __forceinline__ void wait_sel(uint64_t* bar, uint32_t parity, int tag, int* dbg) {
+  if (SPIN && dbg == nullptr)
+    mbar_spin(bar, parity);
+  else
+    mbar_wait_dbg(bar, parity, tag, dbg);
+}
+
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN>
 __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREADS, CTAS)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
   using L = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
@@ -82,6 +100,10 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   uint64_t* p_full = s_full + NS;          // NS
   uint64_t* o_done = p_full + NS;          // NS
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NS);
+  uint32_t* ovf = reinterpret_cast<uint32_t*>(smem + L::OFF_OVF);
+  // TMEM column (within an S buffer) of the fp16 P pair holding key k: slice k / COLS keeps its
+  // P in the first half of its own S columns
+  auto p_col = [](int k) { return (k / L::COLS) * L::COLS + (k % L::COLS) / 2; };
 
   const int warp = warp_id(), lane = lane_id();
   const int q_tiles = (a.Lq + BQ - 1) / BQ;
@@ -108,6 +130,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
     }
     fence_barrier_init();
   }
+  for (int i = threadIdx.x; i < L::OVF_WORDS; i += blockDim.x) ovf[i] = 0u;
   // ones block of every V stage (column block NB): the row-sum column of O
   for (int i = threadIdx.x; i < STAGES * BKV * 4; i += blockDim.x) {
     const int s = i / (BKV * 4), r = i % (BKV * 4);
@@ -121,181 +144,237 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0, g = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int qt = item % q_tiles;
-        const int h = (item / q_tiles) % a.heads;
-        const int z = item / (q_tiles * a.heads);
-        const int row0 = z * a.Lkv;
-        const int qb = it & 1;
-        mbar_wait_dbg(&q_empty[qb], ((it >> 1) & 1) ^ 1, 1000000 + it, a.dbg);
-        mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
-        for (int b = 0; b < L::NB; ++b)
-          tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
-                      z * a.Lq + qt * BQ);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          const int st = g % STAGES;
-          const uint32_t ph = ((g / STAGES) & 1) ^ 1;
-          uint8_t* sk = smem + L::OFF_K + st * L::K_BYTES;
-          uint8_t* sv = smem + L::OFF_V + st * L::V_BYTES;
-          mbar_wait_dbg(&k_empty[st], ph, 2000000 + g, a.dbg);
-          mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
+  // pipeline state, continued across the two passes
+  int p_it = 0, p_g = 0;  // producer
+  int m_it = 0, m_g = 0;  // MMA issuer
+  int s_g = 0;            // softmax
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      tc_fence_before();
+      __syncthreads();  // every softmax warp has recorded its overflow bits
+      tc_fence_after();
+      if (a.softmax_only) break;
+      uint32_t any = a.force_safe;
+      for (int i = 0; i < L::OVF_WORDS; ++i) any |= ovf[i];
+      if (!any) break;
+    }
+    auto todo = [&](int local) {
+      return pass == 0 || a.force_safe || ((ovf[local >> 5] >> (local & 31)) & 1u);
+    };
+    if (warp == 0) {
+      if (lane == 0 && a.softmax_only != 1) {
+        int local = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+          if (!todo(local)) continue;
+          const int qt = item % q_tiles;
+          const int h = (item / q_tiles) % a.heads;
+          const int z = item / (q_tiles * a.heads) + a.z_base;
+          const int row0 = z * a.Lkv;
+          const int qb = p_it & 1;
+          mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, a.dbg);
+          mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
           for (int b = 0; b < L::NB; ++b)
-            tma_load_2d(sk + b * L::KV_BLOCK, &tmKV, &k_full[st], a.k_col + h * HD + b * 16, row0 + j * BKV);
-          mbar_wait_dbg(&v_empty[st], ph, 2500000 + g, a.dbg);
-          mbar_arrive_expect_tx(&v_full[st], L::K_BYTES);
-          for (int b = 0; b < L::NB; ++b)
-            tma_load_2d(sv + b * L::KV_BLOCK, &tmKV, &v_full[st], a.v_col + h * HD + b * 16, row0 + j * BKV);
+            tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
+                        z * a.Lq + qt * BQ);
+          ++p_it;
+          for (int j = 0; j < nkv; ++j, ++p_g) {
+            const int st = p_g % STAGES;
+            const uint32_t ph = ((p_g / STAGES) & 1) ^ 1;
+            uint8_t* sk = smem + L::OFF_K + st * L::K_BYTES;
+            uint8_t* sv = smem + L::OFF_V + st * L::V_BYTES;
+            mbar_wait_dbg(&k_empty[st], ph, 2000000 + p_g, a.dbg);
+            mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
+            for (int b = 0; b < L::NB; ++b)
+              tma_load_2d(sk + b * L::KV_BLOCK, &tmKV, &k_full[st], a.k_col + h * HD + b * 16, row0 + j * BKV);
+            mbar_wait_dbg(&v_empty[st], ph, 2500000 + p_g, a.dbg);
+            mbar_arrive_expect_tx(&v_full[st], L::K_BYTES);
+            for (int b = 0; b < L::NB; ++b)
+              tma_load_2d(sv + b * L::KV_BLOCK, &tmKV, &v_full[st], a.v_col + h * HD + b * 16, row0 + j * BKV);
+          }
         }
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
-      constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, L::ON) | (1u << 16);  // B (V) MN-major
-      int it = 0, g = 0;
-      auto issue_s = [&](int gg, uint32_t sq) {
-        const int st = gg % STAGES;
-        mbar_wait_dbg(&k_full[st], (gg / STAGES) & 1, 3000000 + gg, a.dbg);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
-#pragma unroll
-        for (int b = 0; b < L::NB; ++b)
-          umma_f16(tmem + (gg % NS) * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
-                   desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[gg % NS]);
-      };
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int qb = it & 1;
-        const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
-        mbar_wait_dbg(&q_full[qb], (it >> 1) & 1, 4000000 + it, a.dbg);
-        tc_fence_after();
-        for (int j = 0; j < NS && j < nkv; ++j) issue_s(g + j, sq);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          const int sb = g % NS, st = g % STAGES;
-          mbar_wait_dbg(&p_full[sb], (g / NS) & 1, 5000000 + g, a.dbg);
-          mbar_wait_dbg(&v_full[st], (g / STAGES) & 1, 6000000 + g, a.dbg);
+      __syncwarp();
+    } else if (warp == 1) {
+      if (lane == 0 && a.softmax_only != 1) {
+        constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
+        constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, L::ON) | (1u << 16);  // B (V) MN-major
+        auto issue_s = [&](int gg, uint32_t sq) {
+          const int st = gg % STAGES;
+          wait_sel<SPIN & 1>(&k_full[st], (gg / STAGES) & 1, 3000000 + gg, a.dbg);
           tc_fence_after();
-          const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
+          const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
 #pragma unroll
-          for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA: P columns 8*kc, V rows 16*kc
-            umma_f16_ts(tmem + L::OCOL, tmem + sb * BKV + kc * 8, desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
-                        idesc_pv, (j | kc) != 0);
-          umma_commit(&v_empty[st]);
-          umma_commit(&o_done[sb]);
-          if (j + NS < nkv) issue_s(g + NS, sq);
-          if (j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
+          for (int b = 0; b < L::NB; ++b)
+            umma_f16(tmem + (gg % NS) * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
+                     desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
+          umma_commit(&k_empty[st]);
+          umma_commit(&s_full[gg % NS]);
+        };
+        int local = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+          if (!todo(local)) continue;
+          const int qb = m_it & 1;
+          const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
+          mbar_wait_dbg(&q_full[qb], (m_it >> 1) & 1, 4000000 + m_it, a.dbg);
+          tc_fence_after();
+          for (int j = 0; j < NS && j < nkv; ++j) issue_s(m_g + j, sq);
+          for (int j = 0; j < nkv; ++j, ++m_g) {
+            const int sb = m_g % NS, st = m_g % STAGES;
+            wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
+            wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
+            tc_fence_after();
+            const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
+#pragma unroll
+            for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
+              umma_f16_ts(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16), desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
+                          idesc_pv, (j | kc) != 0);
+            umma_commit(&v_empty[st]);
+            umma_commit(&o_done[sb]);
+            if (j + NS < nkv) issue_s(m_g + NS, sq);
+            if (j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
+          }
+          ++m_it;
         }
       }
-    }
-  } else {
-    // softmax warp: TMEM lane quarter (warp & 3), column slice `part` of every S tile
-    const int quarter = warp & 3, part = (warp - 2) >> 2;
-    const int r = quarter * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
-    const float c = a.scale_log2;
-    int g = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int qt = item % q_tiles;
-      const int h = (item / q_tiles) % a.heads;
-      const int z = item / (q_tiles * a.heads);
-      float m_ref = -INFINITY;
-      for (int j = 0; j < nkv; ++j, ++g) {
-        const int sb = g % NS;
-        mbar_wait_dbg(&s_full[sb], (g / NS) & 1, 7000000 + g, a.dbg);
-        tc_fence_after();
-        const uint32_t sbase = lane_base + sb * BKV + part * L::COLS;
-        float v[L::COLS];
-        tmem_ld_cols<L::COLS>(sbase, v);
-        tmem_ld_wait();
+      __syncwarp();
+    } else {
+      // softmax warp: TMEM lane quarter (warp & 3), column slice `part` of every S tile
+      const int quarter = warp & 3, part = (warp - 2) >> 2;
+      const int r = quarter * 32 + lane;
+      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+      float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
+      const float c = a.scale_log2;
+      // row max of the loaded S slice, combined over the SPLIT slices of this row
+      auto row_max = [&](const float* v, int gg) {
         float pm[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) pm[k] = v[k];
 #pragma unroll
         for (int i = 8; i < L::COLS; i += 16)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) pm[k] = i + 8 + k < L::COLS ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
+          for (int k = 0; k < 8; ++k)
+            pm[k] = i + 8 + k < L::COLS ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
         float mx = fmaxf(fmax3f(pm[0], pm[1], pm[2]), fmax3f(fmax3f(pm[3], pm[4], pm[5]), pm[6], pm[7]));
-        if constexpr (SPLIT > 1) {  // combine the row maxima of the SPLIT column slices
-          float* rb = red + (g & 1) * SPLIT * BQ;
+        if constexpr (SPLIT > 1) {
+          float* rb = red + (gg & 1) * SPLIT * BQ;
           rb[part * BQ + r] = mx;
           named_bar_sync(1 + quarter, 32 * SPLIT);
 #pragma unroll
           for (int q = 0; q < SPLIT; ++q) mx = fmaxf(mx, rb[q * BQ + r]);
         }
-        // warp-uniform decision (identical in every slice of this row quarter): tcgen05.ld/st
-        // are warp-collective (.sync.aligned)
-        if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
-          const float m_new = fmaxf(m_ref, mx);
-          if (j > 0 && part == 0) {
-            const int gp = g - 1;  // previous P.V must be complete before O is rescaled
-            mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, a.dbg);
-            tc_fence_after();
-            const float f = fast_exp2((m_ref - m_new) * c);
-#pragma unroll 1
-            for (int ch = 0; ch < L::ON / 16; ++ch) {
-              float o[16];
-              tmem_ld16(lane_base + L::OCOL + ch * 16, o);
-              tmem_ld_wait();
-              uint32_t u[16];
+        return mx;
+      };
+      int local = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        if (!todo(local)) continue;
+        const int qt = item % q_tiles;
+        const int h = (item / q_tiles) % a.heads;
+        const int z = item / (q_tiles * a.heads) + a.z_base;
+        float m_ref = -INFINITY;
+        float nb = 0.f, cr = 0.f, br = 0.f;
+        for (int j = 0; j < nkv; ++j, ++s_g) {
+          const int sb = s_g % NS;
+          if (a.softmax_only != 1) wait_sel<(SPIN >> 1) & 1>(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, a.dbg);
+          if (a.softmax_only == 2) {  // microbenchmark: MMA/TMA pipeline alone
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[sb]);
+            continue;
+          }
+          tc_fence_after();
+          const uint32_t sbase = lane_base + sb * BKV + part * L::COLS;
+          float v[L::COLS];
+          tmem_ld_cols<L::COLS>(sbase, v);
+          tmem_ld_wait();
+          uint32_t p[L::COLS / 2];
+          if (pass == 0) {
+            if (j == 0) {
+              m_ref = row_max(v, s_g);
+              nb = -m_ref * c;
+              cr = c * (1.0f / EXP_R);
+              br = (nb - EXP_XMIN) * (1.0f / EXP_R);
+            }
+            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * f);
-              tmem_st16(lane_base + L::OCOL + ch * 16, u);
+            for (int i = 0; i < L::COLS / 2; ++i) {
+              float x0, x1;
+              if ((i & 7) < NPOLY / 2) {  // NPOLY of every 16 exponentials on the FMA pipe
+                exp2_poly2_sat(v[2 * i], v[2 * i + 1], cr, br, x0, x1);
+              } else {
+                f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
+                x0 = fast_exp2(x0);
+                x1 = fast_exp2(x1);
+              }
+              p[i] = pack_half2(x0, x1);
+            }
+          } else {
+            const float mx = row_max(v, s_g);
+            // warp-uniform decision (identical in every slice of this row quarter): tcgen05.ld/st
+            // are warp-collective (.sync.aligned)
+            if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
+              const float m_new = fmaxf(m_ref, mx);
+              if (j > 0 && part == 0) {
+                const int gp = s_g - 1;  // previous P.V must be complete before O is rescaled
+                mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, a.dbg);
+                tc_fence_after();
+                const float f = fast_exp2((m_ref - m_new) * c);
+#pragma unroll 1
+                for (int ch = 0; ch < L::ON / 16; ++ch) {
+                  float o[16];
+                  tmem_ld16(lane_base + L::OCOL + ch * 16, o);
+                  tmem_ld_wait();
+                  uint32_t u[16];
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * f);
+                  tmem_st16(lane_base + L::OCOL + ch * 16, u);
+                }
+              }
+              m_ref = m_new;
+            }
+            nb = -m_ref * c;
+            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
+#pragma unroll
+            for (int i = 0; i < L::COLS / 2; ++i) {
+              float x0, x1;
+              f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
+              p[i] = pack_half2(fast_exp2(x0), fast_exp2(x1));
             }
           }
-          m_ref = m_new;
+          // P (fp16 pairs) over this slice's own, already loaded S columns (no cross-slice hazard)
+          tmem_st_cols<L::COLS / 2>(lane_base + sb * BKV + part * L::COLS, p);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && a.softmax_only != 1) mbar_arrive(&p_full[sb]);
         }
-        const float nb = -m_ref * c;
-        const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
-        uint32_t p[L::COLS / 2];
-#pragma unroll
-        for (int i = 0; i < L::COLS / 2; ++i) {
-          float x0, x1;
-          f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
-          // NPOLY of every 16 exponentials (NPOLY / 2 of every 8 pairs) on the FMA pipe
-          if ((i & 7) < NPOLY / 2) {
-            exp2_poly2(x0, x1);
-          } else {
-            x0 = fast_exp2(x0);
-            x1 = fast_exp2(x1);
-          }
-          p[i] = pack_half2(x0, x1);
-        }
-        // P (fp16 pairs) over the already-consumed S columns of this buffer: slice `part` writes
-        // columns part*COLS/2 ..; every slice has loaded its S before the max exchange above
-        tmem_st_cols<L::COLS / 2>(lane_base + sb * BKV + part * (L::COLS / 2), p);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[sb]);
-      }
-      // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
-      // part, part + SPLIT, ...
-      const int gl = g - 1;
-      mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, a.dbg);
-      tc_fence_after();
-      float lsum[8];
-      tmem_ld8(lane_base + L::OCOL + HD, lsum);
-      tmem_ld_wait();
-      const float inv = 1.f / lsum[0];
-      const int qrow = qt * BQ + r;
-      __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
-#pragma unroll 1
-      for (int ch = part; ch < HD / 8; ch += SPLIT) {
-        float o[8];
-        tmem_ld8(lane_base + L::OCOL + ch * 8, o);
+        // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
+        // part, part + SPLIT, ...
+        const int gl = s_g - 1;
+        if (a.softmax_only != 1) mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, a.dbg);
+        tc_fence_after();
+        float lsum[8];
+        tmem_ld8(lane_base + L::OCOL + HD, lsum);
         tmem_ld_wait();
-        if (qrow < a.Lq) {
-          uint4 w;
-          w.x = pack_half2(o[0] * inv, o[1] * inv);
-          w.y = pack_half2(o[2] * inv, o[3] * inv);
-          w.z = pack_half2(o[4] * inv, o[5] * inv);
-          w.w = pack_half2(o[6] * inv, o[7] * inv);
-          reinterpret_cast<uint4*>(dst + ch * 8)[0] = w;
+        const int qrow = qt * BQ + r;
+        if (pass == 0) {
+          const bool bad = qrow < a.Lq && !(fabsf(lsum[0]) < INFINITY);
+          if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&ovf[local >> 5], 1u << (local & 31));
+        }
+        const float inv = 1.f / lsum[0];
+        __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
+#pragma unroll 1
+        for (int ch = part; ch < HD / 8; ch += SPLIT) {
+          float o[8];
+          tmem_ld8(lane_base + L::OCOL + ch * 8, o);
+          tmem_ld_wait();
+          if (qrow < a.Lq) {
+            uint4 w;
+            w.x = pack_half2(o[0] * inv, o[1] * inv);
+            w.y = pack_half2(o[2] * inv, o[3] * inv);
+            w.z = pack_half2(o[4] * inv, o[5] * inv);
+            w.w = pack_half2(o[6] * inv, o[7] * inv);
+            reinterpret_cast<uint4*>(dst + ch * 8)[0] = w;
+          }
         }
       }
     }
@@ -309,24 +388,33 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
 }
 
 // Kernel variants per head dim; variant 0 is the production choice, the others exist for A/B
-// measurement (DART_FA_VARIANT, scripts/bench_attn.py).  Measured on B200 (enc self-attention
-// N=80, 80x16 heads x 5184^2): variant 0 (96-key tiles, 2 CTAs/SM, 6/16 poly exps) 9.49 ms;
-// 4/16 poly 9.96 ms; 8/16 poly 10.65 ms; column-split softmax (2 warps per lane quarter)
-// 10.6 ms; 48-key tiles with 4 CTAs/SM 11.3 ms; 3-4 S buffers (1 CTA/SM) 12-16 ms.
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY>
+// measurement (DART_FA_VARIANT, scripts/bench_attn.py).
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN>
 int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
   using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
-  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY>;
+  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int items = ((a.Lq + BQ - 1) / BQ) * a.heads * a.items;
-  const int grid = items < num_sms * CTAS ? items : num_sms * CTAS;
-  kern<<<grid, Lay::THREADS, Lay::TOTAL, stream>>>(tmQ, tmKV, a);
-  return (int)cudaGetLastError();
+  // items of one launch: each CTA may own at most ATTN_TC_MAX_LOCAL_ITEMS (overflow bitmask)
+  const long long per_z = (long long)((a.Lq + BQ - 1) / BQ) * a.heads;
+  const long long max_grid = (long long)num_sms * CTAS;
+  int zchunk = a.items;
+  while (zchunk > 1 && (per_z * zchunk + max_grid - 1) / max_grid > ATTN_TC_MAX_LOCAL_ITEMS) zchunk = (zchunk + 1) / 2;
+  for (int z0 = 0; z0 < a.items; z0 += zchunk) {
+    AttnTcArgs b = a;
+    b.items = a.items - z0 < zchunk ? a.items - z0 : zchunk;
+    b.z_base = a.z_base + z0;
+    const long long items = per_z * b.items;
+    const int grid = (int)(items < max_grid ? items : max_grid);
+    kern<<<grid, Lay::THREADS, Lay::TOTAL, stream>>>(tmQ, tmKV, b);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
 }
 
 int fa_variant() {
@@ -338,8 +426,26 @@ int fa_variant() {
   return v;
 }
 
-// (HD, variant) -> key tile; must match the launch below.
-int kv_tile_of(int hd, int /*var*/) {
+// Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16).
+#define DART_FA80_VARIANTS(X)   \
+  X(0, 80, 64, 3, 2, 2, 1, 0, 0) \
+  X(1, 80, 64, 3, 1, 4, 2, 0, 0) \
+  X(2, 80, 64, 4, 1, 5, 2, 0, 0) \
+  X(3, 80, 64, 3, 1, 4, 2, 4, 0)
+#define DART_FA16_VARIANTS(X)   \
+  X(0, 16, 96, 4, 2, 2, 1, 6, 0) \
+  X(1, 16, 96, 4, 1, 3, 2, 6, 0) \
+  X(2, 16, 96, 4, 1, 4, 2, 6, 0) \
+  X(3, 16, 96, 6, 1, 4, 2, 8, 0) \
+  X(4, 16, 96, 4, 2, 2, 1, 8, 0) \
+  X(5, 16, 96, 4, 2, 2, 1, 4, 0)
+
+int kv_tile_of(int hd, int var) {
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN) \
+  if (hd == HD && var == V) return BKV;
+  DART_FA80_VARIANTS(X)
+  DART_FA16_VARIANTS(X)
+#undef X
   if (hd == 80) return 64;
   if (hd == 16) return 96;
   return 0;
@@ -357,20 +463,13 @@ bool attention_tc_supported(int head_dim, int Lkv) {
 int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream) {
   const int var = fa_variant();
-  if (head_dim == 80) {
-    switch (var) {
-      case 1: return launch_v<80, 64, 3, 2, 2, 2, 0>(tmQ, tmKV, a, num_sms, stream);
-      case 2: return launch_v<80, 64, 3, 2, 2, 1, 2>(tmQ, tmKV, a, num_sms, stream);
-      default: return launch_v<80, 64, 3, 2, 2, 1, 0>(tmQ, tmKV, a, num_sms, stream);
-    }
-  }
-  if (head_dim == 16) {
-    switch (var) {
-      case 1: return launch_v<16, 96, 4, 2, 2, 1, 4>(tmQ, tmKV, a, num_sms, stream);
-      case 2: return launch_v<16, 96, 4, 2, 2, 2, 6>(tmQ, tmKV, a, num_sms, stream);
-      default: return launch_v<16, 96, 4, 2, 2, 1, 6>(tmQ, tmKV, a, num_sms, stream);
-    }
-  }
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN) \
+  if (head_dim == HD && var == V) return launch_v<HD, BKV, ST, CT, NS, SP, NP, SN>(tmQ, tmKV, a, num_sms, stream);
+  DART_FA80_VARIANTS(X)
+  DART_FA16_VARIANTS(X)
+#undef X
+  if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0>(tmQ, tmKV, a, num_sms, stream);
   return (int)cudaErrorInvalidValue;
 }
 

@@ -360,6 +360,34 @@ __device__ __forceinline__ void exp2_poly2(float& x0, float& x1) {
   x1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
+// Fixed-reference softmax exponentials (attention_tc.cu fast path): x = s*c + nb may be positive
+// (the reference max comes from the first key tile only).  The FMA-pipe variant clamps x to
+// [EXP_XMIN, EXP_XMAX] with one saturating FFMA per element, y = sat((x - XMIN) / R), and maps it
+// back with one packed FFMA: results stay exact to ~R*2^-24 in x, below 2^-126 flush to ~0 and
+// above 2^16 still overflow the fp16 P to inf (the overflow signal the kernel checks).
+constexpr float EXP_XMIN = -126.0f, EXP_XMAX = 17.0f, EXP_R = EXP_XMAX - EXP_XMIN;
+__device__ __forceinline__ float ffma_sat(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^(s*c+nb) for a pair on the FMA pipe; cr = c/R, br = (nb - XMIN)/R.
+__device__ __forceinline__ void exp2_poly2_sat(float s0, float s1, float cr, float br, float& x0, float& x1) {
+  const uint64_t y = f2_pack(ffma_sat(s0, cr, br), ffma_sat(s1, cr, br));
+  const uint64_t x = ffma2(y, f2_pack(EXP_R, EXP_R), f2_pack(EXP_XMIN, EXP_XMIN));
+  const uint64_t t = fadd2(x, f2_pack(12582912.0f, 12582912.0f));
+  const uint64_t j = fadd2(t, f2_pack(-12582912.0f, -12582912.0f));
+  const uint64_t f = ffma2(j, f2_pack(-1.0f, -1.0f), x);
+  uint64_t p = ffma2(f2_pack(0.0551716648f, 0.0551716648f), f, f2_pack(0.2426111251f, 0.2426111251f));
+  p = ffma2(p, f, f2_pack(0.6932609677f, 0.6932609677f));
+  p = ffma2(p, f, f2_pack(0.9999280572f, 0.9999280572f));
+  float t0, t1, p0, p1;
+  f2_unpack(t, t0, t1);
+  f2_unpack(p, p0, p1);
+  x0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  x1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));

@@ -97,8 +97,9 @@ bool tc_attention_enabled() {
   return v == 1;
 }
 
-// Backbone self-attention on a packed QKV buffer [items * L, 3E] (q | k | v column blocks,
-// head-major), tcgen05 kernel.
+// Tests: route every tcgen05 attention item through the max-tracking (overflow-safe) pass too.
+int g_attn_force_safe = 0;
+
 // tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
 // [items*Lkv, kv_ld] (k at k_col, v at v_col), output [items*Lq, o_ld] at column h*hd.
 int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv_ld, int k_col, int v_col, __half* o,
@@ -121,7 +122,11 @@ int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv
   a.o_ld = o_ld;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.dbg = dbg;
-  a.softmax_only = getenv("DART_FA_SOFTMAX_ONLY") != nullptr;
+  a.force_safe = g_attn_force_safe;
+  {
+    const char* e = getenv("DART_FA_SOFTMAX_ONLY");  // microbenchmarks: 1 softmax alone, 2 MMA alone
+    a.softmax_only = e ? atoi(e) : 0;
+  }
   int rc = attention_tc(tq, tkv, a, hd, num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
@@ -929,6 +934,8 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 }
 
 }  // extern "C"
+
+extern "C" void dart_attention_force_safe(int32_t on) { g_attn_force_safe = on ? 1 : 0; }
 
 extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
                                   int32_t* debug_host, void* stream) {

@@ -92,8 +92,11 @@ struct AttnTcArgs {
   int o_ld;
   float scale_log2;
   int* dbg = nullptr;          // host-mapped hang report (tests only), see mbar_wait_dbg
+  int force_safe = 0;          // tests: re-run every item through the max-tracking softmax pass
+  int z_base = 0;              // first item of this launch (items are chunked on the host)
   int softmax_only = 0;        // microbenchmark: softmax warps run on stale S without MMA / TMA
 };
+constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
 int attention_tc_kv_tile(int head_dim);  // 192 (hd 80), 96 (hd 16), 0 = unsupported
 bool attention_tc_supported(int head_dim, int Lkv);
 // tmQ: 2-D map over the Q buffer [items*Lq, cols] fp16, box {16, 128}, 32B swizzle;

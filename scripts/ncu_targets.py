@@ -11,7 +11,7 @@ from paper_2603_11441_b200 import _native
 
 lib = _native.load()
 st = torch.cuda.current_stream().cuda_stream
-which = sys.argv[1:] or ["fc1", "out", "encfc1", "att16", "att80"]
+which = sys.argv[1:] or ["fc1", "out", "encfc1", "att16", "att80", "att80w"]
 calls = []
 for name, (M, N, K, epi) in {"fc1": (5184, 5120, 1280, 1), "out": (5184, 1280, 1280, 3),
                              "encfc1": (20736, 1024, 256, 1)}.items():
@@ -24,17 +24,15 @@ for name, (M, N, K, epi) in {"fc1": (5184, 5120, 1280, 1), "out": (5184, 1280, 1
     calls.append((name, lambda A=A, W=W, bias=bias, out=out, M=M, N=N, K=K, epi=epi: _native.check(
         lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N, K, epi, None, None,
                       0, 0, 0, st))))
-for name, (B, H, L, hd) in {"att16": (4, 16, 5184, 16), "att80": (1, 16, 5184, 80)}.items():
+for name, (B, H, L, hd) in {"att16": (4, 16, 5184, 16), "att80": (1, 16, 5184, 80),
+                            "att80w": (9, 16, 576, 80)}.items():
     if name not in which:
         continue
-    q = torch.randn(B, L, H, hd, device="cuda").half()
-    k = torch.randn(B, L, H, hd, device="cuda").half()
-    v = torch.randn(B, L, H, hd, device="cuda").half()
-    o = torch.empty_like(q)
     E = H * hd
-    calls.append((name, lambda q=q, k=k, v=v, o=o, B=B, H=H, L=L, hd=hd, E=E: _native.check(
-        lib.dart_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, H, L, L, hd, E, E, E, L * E,
-                           L * E, L * E, 0, 0, st))))
+    qkv = torch.randn(B * L, 3 * E, device="cuda").half()
+    o = torch.empty(B * L, E, device="cuda", dtype=torch.float16)
+    calls.append((name, lambda qkv=qkv, o=o, B=B, H=H, L=L, hd=hd: _native.check(
+        lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), B, H, L, hd, None, st))))
 for _, f in calls:
     f()
 torch.cuda.synchronize()

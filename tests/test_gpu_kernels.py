@@ -224,14 +224,22 @@ def test_attention_tcgen05_packed_qkv(lib, items, L, hd):
     assert float((o.float() - ref).abs().max()) < 1e-2
 
 
-def test_attention_tcgen05_large_logits(lib):
-    """Peaked softmax (lazy-rescale path): scores growing along the key axis."""
-    items, L, H, hd = 1, 576, 16, 80
+@pytest.mark.parametrize("hd,L", [(80, 576), (16, 576), (80, 5184)])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_attention_tcgen05_large_logits(lib, hd, L, mixed):
+    """Peaked softmax: scores growing along the key axis overflow the fixed-reference pass (first
+    key tile's max), so those items are recomputed by the max-tracking pass.  mixed: only half of
+    the heads overflow (per-item selection of the second pass)."""
+    items, H = 1, 16
     E = H * hd
     g = torch.Generator(device="cuda").manual_seed(7)
     qkv = torch.randn(items, L, 3, H, hd, device="cuda", generator=g)
     qkv[:, :, 0] *= 4
-    qkv[:, :, 1] *= torch.linspace(0.1, 6, L, device="cuda")[None, :, None, None]
+    grow = torch.linspace(0.1, 6 if hd == 80 else 14, L, device="cuda")[None, :, None, None]
+    if mixed:
+        qkv[:, :, 1, : H // 2] *= grow
+    else:
+        qkv[:, :, 1] *= grow
     qkv = qkv.half()
     o = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
     _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, stream()))
@@ -239,3 +247,25 @@ def test_attention_tcgen05_large_logits(lib):
     x = qkv.permute(2, 0, 3, 1, 4)
     ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
     assert float((o.float() - ref).abs().max()) < 2e-2
+
+
+@pytest.mark.parametrize("items,L,hd", [(2, 576, 80), (2, 5184, 16)])
+def test_attention_tcgen05_forced_safe_pass(lib, items, L, hd):
+    """Every item re-run through the max-tracking pass gives the same result as the fast pass."""
+    H = 16
+    E = H * hd
+    g = torch.Generator(device="cuda").manual_seed(L + items)
+    qkv = (torch.randn(items, L, 3, H, hd, device="cuda", generator=g) * 2).half()
+    o1 = torch.empty(items, L, E, device="cuda", dtype=torch.float16)
+    o2 = torch.empty_like(o1)
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o1.data_ptr(), items, H, L, hd, None, stream()))
+    lib.dart_attention_force_safe(1)
+    try:
+        _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o2.data_ptr(), items, H, L, hd, None, stream()))
+    finally:
+        lib.dart_attention_force_safe(0)
+    torch.cuda.synchronize()
+    x = qkv.permute(2, 0, 3, 1, 4)
+    ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
+    assert float((o1.float() - ref).abs().max()) < 1e-2
+    assert float((o2.float() - ref).abs().max()) < 1e-2
