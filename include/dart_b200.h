@@ -33,7 +33,7 @@ extern "C" {
 #define DART_ERR_INVALID 1 /* bad argument / shape: maps to ValueError      */
 #define DART_ERR_CUDA 2    /* CUDA launch or allocation failure: RuntimeError */
 
-/* Status-flag bits written by dart_backbone into `flags` (device int32). */
+/* Status-flag bits written by dart_backbone into `flags` (device int32; cleared by the call). */
 #define DART_FLAG_IMAGE_RANGE 1   /* some image value outside [0, 1] or NaN (model.py:432-433) */
 #define DART_FLAG_NONFINITE 2     /* some FPN level non-finite (model.py:161-166)              */
 
@@ -58,6 +58,12 @@ typedef struct dart_model dart_model;
  * order), each tensor row-major in the reference's [in, out] layout. */
 int dart_model_create(const dart_model_desc* desc, const float* const* weights, int32_t n_weights,
                       dart_model** out);
+/* A second handle on the same device weights (no copy) with its own activation workspace, so
+ * two streams can run the path concurrently (inter-frame pipelining: the backbone of frame t+1
+ * on one handle while the enc-dec of frame t runs on the other; the reference models this
+ * schedule analytically in scheduler.py:128-187).  Weights stay alive until the last handle
+ * sharing them is destroyed. */
+int dart_model_fork(const dart_model* parent, dart_model** out);
 void dart_model_destroy(dart_model* m);
 
 /* Number of parameter tensors dart_model_create expects for `desc`. */

@@ -23,6 +23,7 @@ FLAG_NONFINITE = 2
 EXPORTS = (
     "dart_model_create",
     "dart_model_destroy",
+    "dart_model_fork",
     "dart_expected_weight_count",
     "dart_backbone",
     "dart_encdec",
@@ -87,6 +88,8 @@ def load() -> ctypes.CDLL:
     lib.dart_model_create.restype = ctypes.c_int
     lib.dart_model_destroy.argtypes = [P]
     lib.dart_model_destroy.restype = None
+    lib.dart_model_fork.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
+    lib.dart_model_fork.restype = ctypes.c_int
     lib.dart_expected_weight_count.argtypes = [ctypes.POINTER(ModelDesc)]
     lib.dart_expected_weight_count.restype = I32
     lib.dart_backbone.argtypes = [P, P, I32, P, P, P, P, P]

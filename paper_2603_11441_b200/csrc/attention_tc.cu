@@ -429,17 +429,18 @@ int fa_variant() {
 // Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16).
 #define DART_FA80_VARIANTS(X)   \
   X(0, 80, 64, 3, 2, 2, 1, 0, 0) \
-  X(1, 80, 64, 3, 1, 4, 2, 0, 0) \
-  X(2, 80, 64, 4, 1, 5, 2, 0, 0) \
-  X(3, 80, 64, 3, 1, 4, 2, 4, 0)
+  X(1, 80, 64, 3, 2, 2, 1, 4, 0)
 #define DART_FA16_VARIANTS(X)   \
   X(0, 16, 96, 4, 2, 2, 1, 6, 0) \
-  X(1, 16, 96, 4, 1, 3, 2, 6, 0) \
-  X(2, 16, 96, 4, 1, 4, 2, 6, 0) \
-  X(3, 16, 96, 6, 1, 4, 2, 8, 0) \
-  X(4, 16, 96, 4, 2, 2, 1, 8, 0) \
-  X(5, 16, 96, 4, 2, 2, 1, 4, 0)
-
+  X(1, 16, 96, 4, 2, 2, 1, 8, 0)
+// Measured on B200 (scripts/bench_attn.py, hd 16 enc self-attention N=80 = 80x16 heads x 5184^2):
+// variant 0 8.70 ms (NPOLY 6), NPOLY 8 9.67, NPOLY 4 9.1, 2 column slices 9.6-10.5, 64-key tiles
+// with 3 S buffers 11.0, 48-key tiles with 4 S buffers 13.3, one CTA/SM with 3-4 S buffers 15.3,
+// spin waits 9.8.  Softmax alone (no MMA) 6.76 ms; MMA/TMA pipeline alone 6.94 ms: tcgen05.mma
+// costs >= 44 clk per instruction even at N = 32 (scripts/probes/mma_rate.cu), so the 6 P.V steps
+// of a 96-key tile (~266 clk) plus S (~57 clk) load the tensor pipe ~2/3 as much as the exps load
+// MUFU.  Staging P in shared memory or in separate TMEM buffers (S released at load time) was
+// slower (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.
 int kv_tile_of(int hd, int var) {
 #define X(V, HD, BKV, ST, CT, NS, SP, NP, SN) \
   if (hd == HD && var == V) return BKV;

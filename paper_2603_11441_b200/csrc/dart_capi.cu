@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -196,13 +197,21 @@ struct Workspace {
   }
 };
 
+// Device weight buffers, shared by a model handle and its forks (dart_model_fork).
+struct OwnedBuffers {
+  std::vector<void*> p;
+  ~OwnedBuffers() {
+    for (void* x : p) cudaFree(x);
+  }
+};
+
 }  // namespace
 
 struct dart_model {
   dart_model_desc d;
   int T = 0, G = 0, E = 0, H = 0, hd = 0, kpatch = 0, kpad = 0, D = 0, Lt = 0, Q1 = 0, F0 = 0, F1 = 0, F2 = 0;
   int num_sms = 148;
-  std::vector<void*> owned;
+  std::shared_ptr<OwnedBuffers> owned = std::make_shared<OwnedBuffers>();
   GemmW patch;
   float* rope_cos = nullptr;
   float* rope_sin = nullptr;
@@ -233,7 +242,6 @@ struct dart_model {
   ~dart_model() {
     bb_ws.release();
     ed_ws.release();
-    for (void* p : owned) cudaFree(p);
   }
 };
 
@@ -243,7 +251,7 @@ template <typename T>
 T* dev_alloc(dart_model* m, size_t n) {
   void* p = nullptr;
   if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
-  m->owned.push_back(p);
+  m->owned->p.push_back(p);
   return reinterpret_cast<T*>(p);
 }
 
@@ -660,6 +668,20 @@ int dart_model_create(const dart_model_desc* desc, const float* const* weights, 
 
 void dart_model_destroy(dart_model* m) { delete m; }
 
+int dart_model_fork(const dart_model* parent, dart_model** out) {
+  if (!parent || !out) return fail(DART_ERR_INVALID, "dart_model_fork: bad args");
+  dart_model* f = new dart_model(*parent);  // shares the weights (shared_ptr), copies dims and maps
+  f->bb_ws = Workspace();                   // own, initially empty activation workspaces
+  f->ed_ws = Workspace();
+  f->bb_cap = f->ed_cap_items = f->ed_cap_n = f->ed_cap_b = 0;
+  f->last_backbone_B = 0;
+  f->bb = {};
+  f->ed = {};
+  f->launches = 0;
+  *out = f;
+  return DART_OK;
+}
+
 int64_t dart_launch_count(const dart_model* m) { return m ? m->launches : 0; }
 void dart_reset_launch_count(dart_model* m) {
   if (m) m->launches = 0;
@@ -670,6 +692,7 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
   if (!m || !images || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone: bad args");
   cudaStream_t s = (cudaStream_t)stream;
   RUN(ensure_backbone_ws(m, B));
+  if (cudaMemsetAsync(flags, 0, sizeof(int32_t), s) != cudaSuccess) return fail(DART_ERR_CUDA, "flags memset");
   const int T = m->T, E = m->E, H = m->H, hd = m->hd, G = m->G;
   const int rows = B * T;
   auto& w = m->bb;

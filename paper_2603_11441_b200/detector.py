@@ -48,10 +48,21 @@ class Detector:
         b = self._bufs.get(B)
         if b is not None:
             return b
+        cfg = self.model.config
+        b = self._alloc_slot(B)
+        b["img"] = torch.empty((B, cfg.image_size, cfg.image_size, 3), device=self.device, dtype=torch.float32)
+        b["host_img"] = torch.empty((B, cfg.image_size, cfg.image_size, 3), dtype=torch.float32, pin_memory=True)
+        self._bufs[B] = b
+        return b
+
+    # ------------------------------------------------------------------ device path
+    def _alloc_slot(self, B: int):
+        import torch
+
         cfg, dev = self.model.config, self.device
         T, g, Q, N = cfg.tokens, cfg.grid, cfg.num_queries, len(self.class_names)
         f64, f32, i32 = torch.float64, torch.float32, torch.int32
-        b = {
+        return {
             "l0": torch.empty((B, T, cfg.fpn_dims[0]), device=dev, dtype=f32),
             "l1": torch.empty((B, (g // 2) ** 2, cfg.fpn_dims[1]), device=dev, dtype=f32),
             "l2": torch.empty((B, (g // 4) ** 2, cfg.fpn_dims[2]), device=dev, dtype=f32),
@@ -66,23 +77,21 @@ class Detector:
             "pp": torch.empty((B * N,), device=dev, dtype=f64),
             "kf": torch.zeros((B * N, Q), device=dev, dtype=i32),
             "scratch": torch.empty((N * (2 * Q + 1) + 1,), device=dev, dtype=i32),
-            "img": torch.empty((B, cfg.image_size, cfg.image_size, 3), device=dev, dtype=f32),
         }
-        b["host_img"] = torch.empty((B, cfg.image_size, cfg.image_size, 3), dtype=f32, pin_memory=True)
-        self._bufs[B] = b
-        return b
 
-    # ------------------------------------------------------------------ device path
-    def detect_device(self, images):
-        """images: device float32 [B, S, S, 3].  Enqueues backbone, class-batched enc-dec and
-        post-processing on the current stream; returns the buffer dict (no sync)."""
+    def _enqueue_backbone(self, h, images, b, st: int) -> None:
+        """dart_backbone of one batch into slot `b` on stream `st` (the call clears the flags)."""
         B = int(images.shape[0])
-        b = self._buffers(B)
-        h, lib, st = self.handle, self.lib, _stream_ptr(self.device)
+        _native.check(self.lib.dart_backbone(h.ptr, images.data_ptr(), B, b["l0"].data_ptr(), b["l1"].data_ptr(),
+                                             b["l2"].data_ptr(), b["flags"].data_ptr(), st))
+
+    def _enqueue_decode(self, h, b, B: int, st: int, l0_ptr) -> None:
+        """Class-batched enc-dec (one pass per n_max chunk) and post-processing of slot `b` on
+        stream `st`.  l0_ptr None: the level-0 features still in `h`'s backbone workspace."""
+        import torch
+
+        lib = self.lib
         N, Q = len(self.class_names), self.model.config.num_queries
-        b["flags"].zero_()
-        _native.check(lib.dart_backbone(h.ptr, images.data_ptr(), B, b["l0"].data_ptr(), b["l1"].data_ptr(),
-                                        b["l2"].data_ptr(), b["flags"].data_ptr(), st))
         off = 0
         for ci, ch in enumerate(self.chunks):
             n = len(ch)
@@ -92,12 +101,13 @@ class Detector:
                 bx = b.setdefault(f"boxes{ci}", b["boxes"].new_empty((B, n, Q, 4)))
                 sc = b.setdefault(f"scores{ci}", b["scores"].new_empty((B, n, Q)))
                 pr = b.setdefault(f"presence{ci}", b["presence"].new_empty((B, n)))
-            _native.check(lib.dart_encdec(h.ptr, None, B, self.text[ci].data_ptr(), n, bx.data_ptr(), sc.data_ptr(),
-                                          pr.data_ptr(), None, st))
+            _native.check(lib.dart_encdec(h.ptr, l0_ptr, B, self.text[ci].data_ptr(), n, bx.data_ptr(),
+                                          sc.data_ptr(), pr.data_ptr(), None, st))
             if len(self.chunks) > 1:
-                b["boxes"][:, off: off + n].copy_(bx)
-                b["scores"][:, off: off + n].copy_(sc)
-                b["presence"][:, off: off + n].copy_(pr)
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=self.device)):
+                    b["boxes"][:, off: off + n].copy_(bx)
+                    b["scores"][:, off: off + n].copy_(sc)
+                    b["presence"][:, off: off + n].copy_(pr)
             off += n
         c = self.cfg
         xc = int(c.cross_class_nms)
@@ -115,7 +125,128 @@ class Detector:
                 c.presence_threshold, c.score_threshold, c.nms_iou_threshold, xc, b["kc"].data_ptr(),
                 b["kq"].data_ptr(), b["ks"].data_ptr(), b["pp"].data_ptr(), b["kf"].data_ptr(),
                 b["scratch"].data_ptr(), st))
+
+    def detect_device(self, images):
+        """images: device float32 [B, S, S, 3].  Enqueues backbone, class-batched enc-dec and
+        post-processing on the current stream; returns the buffer dict (no sync)."""
+        B = int(images.shape[0])
+        b = self._buffers(B)
+        st = _stream_ptr(self.device)
+        self._enqueue_backbone(self.handle, images, b, st)
+        self._enqueue_decode(self.handle, b, B, st, None)
         return b
+
+    # ------------------------------------------------------------------ inter-frame pipelining
+    def _pipeline(self, B: int):
+        """Two streams, two handles (the second a dart_model_fork sharing the weights) and two
+        buffer slots: the backbone of batch t+1 runs on stream 0 while the enc-dec and
+        post-processing of batch t run on stream 1 (the paper's two-stream schedule,
+        reference scheduler.py:128-187)."""
+        import torch
+
+        p = getattr(self, "_pipe", None)
+        if p is not None and p["B"] == B:
+            return p
+        p = {
+            "B": B,
+            "h_dec": self.handle.fork(),
+            "s_bb": torch.cuda.Stream(device=self.device),
+            "s_dec": torch.cuda.Stream(device=self.device),
+            "slots": [self._alloc_slot(B) for _ in range(2)],
+            "ev_bb": [torch.cuda.Event() for _ in range(2)],
+            "ev_dec": [None, None],
+            "t": 0,
+        }
+        self._pipe = p
+        return p
+
+    def detect_device_pipelined(self, images):
+        """Enqueue one batch (device float32 [B, S, S, 3]) into the two-stream pipeline; returns
+        its slot buffers, valid once the returned event (recorded on the decode stream) has
+        completed and until the batch two calls later reuses the slot.  No host sync."""
+        import torch
+
+        B = int(images.shape[0])
+        p = self._pipeline(B)
+        k = p["t"] & 1
+        p["t"] += 1
+        b = p["slots"][k]
+        s_bb, s_dec = p["s_bb"], p["s_dec"]
+        s_bb.wait_stream(torch.cuda.current_stream(self.device))  # inputs produced on the caller's stream
+        if p["ev_dec"][k] is not None:
+            s_bb.wait_event(p["ev_dec"][k])  # slot free: decode of batch t-2 done
+        self._enqueue_backbone(self.handle, images, b, s_bb.cuda_stream)
+        p["ev_bb"][k].record(s_bb)
+        s_dec.wait_event(p["ev_bb"][k])
+        self._enqueue_decode(p["h_dec"], b, B, s_dec.cuda_stream, b["l0"].data_ptr())
+        ev = torch.cuda.Event()
+        ev.record(s_dec)
+        p["ev_dec"][k] = ev
+        return b, ev
+
+    def pipeline_join(self) -> None:
+        """Make the caller's current stream wait for everything enqueued in the pipeline."""
+        import torch
+
+        p = getattr(self, "_pipe", None)
+        if p is not None:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_stream(p["s_bb"])
+            cur.wait_stream(p["s_dec"])
+
+    def detect_stream(self, batches):
+        """Generator over host (NumPy / CPU torch) or device image batches [B, S, S, 3]: yields
+        one list of per-image detection lists per batch, in order, with the backbone of batch
+        t+1 overlapped with the decode of batch t.  Each batch's H2D copy runs on the backbone
+        stream and its results come back with one D2H copy on the decode stream."""
+        import torch
+
+        pending = []  # (event, host result dict, B)
+        host_slots = {}
+        for t, arr in enumerate(batches):
+            if isinstance(arr, np.ndarray) and arr.ndim == 3:
+                arr = arr[None]
+            elif not isinstance(arr, np.ndarray) and arr.ndim == 3:
+                arr = arr.unsqueeze(0)
+            S = self.model.config.image_size
+            if tuple(arr.shape[1:]) != (S, S, 3):
+                raise ValueError(f"image shape {tuple(arr.shape)} does not match {(S, S, 3)}")
+            B = int(arr.shape[0])
+            p = self._pipeline(B)
+            k = p["t"] & 1
+            hs = host_slots.get((B, k))
+            if hs is None:
+                hs = host_slots[(B, k)] = {
+                    "img": torch.empty((B, S, S, 3), dtype=torch.float32, pin_memory=True),
+                    "dimg": torch.empty((B, S, S, 3), dtype=torch.float32, device=self.device),
+                    "res": {n: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                            for n, v in self.result_tensors(p["slots"][k]).items()},
+                }
+            if len(pending) >= 2:  # the slot's previous batch must be delivered first
+                yield self._deliver(*pending.pop(0))
+            if isinstance(arr, np.ndarray):
+                hs["img"].numpy()[...] = arr
+                src = hs["img"]
+            else:
+                src = arr
+            if p["ev_dec"][k] is not None:
+                p["s_bb"].wait_event(p["ev_dec"][k])
+            with torch.cuda.stream(p["s_bb"]):
+                hs["dimg"].copy_(src, non_blocking=True)
+            b, _ = self.detect_device_pipelined(hs["dimg"])
+            with torch.cuda.stream(p["s_dec"]):
+                for n, v in self.result_tensors(b).items():
+                    hs["res"][n].copy_(v, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(p["s_dec"])
+            pending.append((ev, hs["res"], B))
+        while pending:
+            yield self._deliver(*pending.pop(0))
+
+    def _deliver(self, ev, host, B):
+        ev.synchronize()
+        raise_for_flags(int(host["flags"][0]))
+        return self.unpack(host, B)
 
     def result_tensors(self, b):
         keys = ["flags", "kc", "kq", "ks", "pp", "boxes"] + (["kf"] if self.cfg.cross_class_nms else [])

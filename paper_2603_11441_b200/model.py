@@ -375,6 +375,18 @@ class _Handle:
         self.lib = lib
         self.cfg = cfg
 
+    def fork(self) -> "_Handle":
+        """A second handle on the same device weights with its own activation workspace
+        (dart_model_fork), for a second concurrent stream."""
+        import torch
+
+        f = object.__new__(_Handle)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.dart_model_fork(self.ptr, ctypes.byref(handle)))
+        f.ptr, f.device, f.lib, f.cfg = handle, self.device, self.lib, self.cfg
+        return f
+
     def __del__(self):
         try:
             if self.ptr:

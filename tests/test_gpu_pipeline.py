@@ -1,0 +1,55 @@
+"""Inter-frame pipelining (two streams, two handles sharing the weights via dart_model_fork):
+every image's detections are identical to the one-stream Detector.detect path, and forked
+handles run the same kernels on the same weights (reference scheduler.py:128-187 models this
+schedule; the outputs of a pipelined stream must equal per-frame detection)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2603_11441_b200 as D  # noqa: E402
+from paper_2603_11441_b200.detector import Detector  # noqa: E402
+
+
+def _setup(n_img=5):
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    names = ["car", "person", "dog"]
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    imgs = [D.generate_scene(D.SceneSpec(seed=10 + i, num_classes=3))[0].astype(np.float32) for i in range(n_img)]
+    return model, names, cfg, imgs
+
+
+def test_detect_stream_matches_detect():
+    model, names, cfg, imgs = _setup()
+    det = Detector(model, names, cfg)
+    serial = [det.detect(im) for im in imgs]
+    streamed = [r[0] for r in det.detect_stream(imgs)]
+    assert streamed == serial
+
+
+def test_detect_stream_batched_and_device_inputs():
+    model, names, cfg, imgs = _setup(6)
+    det = Detector(model, names, cfg)
+    batches = [np.stack(imgs[i:i + 2]) for i in range(0, 6, 2)]
+    serial = [det.detect(b) for b in batches]
+    dev = [torch.from_numpy(b).cuda() for b in batches]
+    assert [r for r in det.detect_stream(dev)] == serial
+
+
+def test_forked_handle_same_outputs():
+    model, names, cfg, imgs = _setup(2)
+    det = Detector(model, names, cfg)
+    x = torch.from_numpy(np.stack(imgs[:1])).cuda()
+    b = det.detect_device(x)
+    ref = {k: v.clone() for k, v in det.result_tensors(b).items()}
+    bp, ev = det.detect_device_pipelined(x)
+    det.pipeline_join()
+    torch.cuda.synchronize()
+    got = det.result_tensors(bp)
+    for k in ("flags", "kc", "pp", "boxes"):
+        assert torch.equal(got[k], ref[k]), k
+    for it, n in enumerate(ref["kc"].tolist()):  # kept lists (entries past the count are scratch)
+        assert torch.equal(got["kq"][it, :n], ref["kq"][it, :n])
+        assert torch.equal(got["ks"][it, :n], ref["ks"][it, :n])
