@@ -128,6 +128,10 @@ int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, i
 /* Tests: on != 0 makes every later tcgen05 attention launch re-run all of its items through the
  * max-tracking softmax pass (the path items take when the fixed-reference pass overflows). */
 void dart_attention_force_safe(int32_t on);
+/* Microbenchmarks: device int64[7 * 256] receiving CTA 0's clock64 stamps of its first 256 key
+ * tiles (S ready, P written, P seen by the MMA issuer, MMAs issued, V ready, P.V issued, next K
+ * ready); NULL disables. */
+void dart_attention_trace(int64_t* device_buf);
 
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */

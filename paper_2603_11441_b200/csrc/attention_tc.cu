@@ -59,7 +59,7 @@ struct FaCfg {
   static constexpr int OFF_K = 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
   static constexpr int OFF_BAR = OFF_V + STAGES * V_BYTES;
-  static constexpr int NBARS = 4 + 4 * STAGES + 3 * NS;
+  static constexpr int NBARS = 4 + 4 * STAGES + 3 * NS + 1;
   static constexpr int OFF_OVF = OFF_BAR + NBARS * 8 + 16;         // overflow bitmask of local items
   static constexpr int OVF_WORDS = ATTN_TC_MAX_LOCAL_ITEMS / 32;
   static constexpr int OFF_RED = OFF_OVF + OVF_WORDS * 4;          // [2][SPLIT][128] partial row maxima
@@ -75,6 +75,12 @@ struct FaCfg {
 // the item is marked in a per-CTA bitmask.  Pass 1 re-runs the marked items with the classic
 // per-tile running max and lazy rescale (P <= 2^8), overwriting their output rows.
 // SPIN bit 0: the MMA issuer spins on its barriers; bit 1: the softmax warps spin on S-ready.
+// LEAN: every tcgen05.commit occupies the tensor pipe like a ~44-clk MMA (scripts/probes/
+// mma_rate.cu), so per key tile only S-ready is committed; K / V / Q stage releases become
+// thread arrivals by softmax warp 2 (S(g) complete => K(g) consumed, and P.V(g-2), issued
+// before S(g), complete => V(g-2) consumed), O-complete is committed once per item (and per
+// tile only in the rare max-tracking pass, for its O rescale), and V loads get their own
+// producer thread (warp 0 lane 1) so they never hold back K loads.
 template <bool SPIN>
 __device__ __forceinline__ void wait_sel(uint64_t* bar, uint32_t parity, int tag, int* dbg) {
   if (SPIN && dbg == nullptr)
@@ -83,7 +89,7 @@ __device__ __forceinline__ void wait_sel(uint64_t* bar, uint32_t parity, int tag
     mbar_wait_dbg(bar, parity, tag, dbg);
 }
 
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN>
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN>
 __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREADS, CTAS)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
   using L = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
@@ -99,7 +105,8 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   uint64_t* s_full = v_empty + STAGES;     // NS
   uint64_t* p_full = s_full + NS;          // NS
   uint64_t* o_done = p_full + NS;          // NS
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NS);
+  uint64_t* item_done = o_done + NS;       // 1 (LEAN): all P.V of an item complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_done + 1);
   uint32_t* ovf = reinterpret_cast<uint32_t*>(smem + L::OFF_OVF);
   // TMEM column (within an S buffer) of the fp16 P pair holding key k: slice k / COLS keeps its
   // P in the first half of its own S columns
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       mbar_init(&p_full[s], 4 * SPLIT);
       mbar_init(&o_done[s], 1);
     }
+    mbar_init(item_done, 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -145,9 +153,9 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   const uint32_t tmem = *tmem_slot;
 
   // pipeline state, continued across the two passes
-  int p_it = 0, p_g = 0;  // producer
-  int m_it = 0, m_g = 0;  // MMA issuer
-  int s_g = 0;            // softmax
+  int p_it = 0, p_g = 0, pv_g = 0;  // producer (Q/K thread, V thread)
+  int m_it = 0, m_g = 0, m_g1 = 0;  // MMA issuer (m_g1: tiles of the max-tracking pass)
+  int s_g = 0, s_it = 0, s_g1 = 0;  // softmax
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
       tc_fence_before();
@@ -162,7 +170,8 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       return pass == 0 || a.force_safe || ((ovf[local >> 5] >> (local & 31)) & 1u);
     };
     if (warp == 0) {
-      if (lane == 0 && a.softmax_only != 1) {
+      if (lane < (LEAN ? 2 : 1) && a.softmax_only != 1) {
+        const bool do_qk = lane == 0, do_v = !LEAN || lane == 1;
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
           if (!todo(local)) continue;
@@ -170,26 +179,34 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           const int h = (item / q_tiles) % a.heads;
           const int z = item / (q_tiles * a.heads) + a.z_base;
           const int row0 = z * a.Lkv;
-          const int qb = p_it & 1;
-          mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, a.dbg);
-          mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
-          for (int b = 0; b < L::NB; ++b)
-            tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
-                        z * a.Lq + qt * BQ);
-          ++p_it;
-          for (int j = 0; j < nkv; ++j, ++p_g) {
-            const int st = p_g % STAGES;
-            const uint32_t ph = ((p_g / STAGES) & 1) ^ 1;
-            uint8_t* sk = smem + L::OFF_K + st * L::K_BYTES;
-            uint8_t* sv = smem + L::OFF_V + st * L::V_BYTES;
-            mbar_wait_dbg(&k_empty[st], ph, 2000000 + p_g, a.dbg);
-            mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
+          if (do_qk) {
+            const int qb = p_it & 1;
+            mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, a.dbg);
+            mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
             for (int b = 0; b < L::NB; ++b)
-              tma_load_2d(sk + b * L::KV_BLOCK, &tmKV, &k_full[st], a.k_col + h * HD + b * 16, row0 + j * BKV);
-            mbar_wait_dbg(&v_empty[st], ph, 2500000 + p_g, a.dbg);
-            mbar_arrive_expect_tx(&v_full[st], L::K_BYTES);
-            for (int b = 0; b < L::NB; ++b)
-              tma_load_2d(sv + b * L::KV_BLOCK, &tmKV, &v_full[st], a.v_col + h * HD + b * 16, row0 + j * BKV);
+              tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
+                          z * a.Lq + qt * BQ);
+            ++p_it;
+          }
+          for (int j = 0; j < nkv; ++j) {
+            if (do_qk) {
+              const int st = p_g % STAGES;
+              mbar_wait_dbg(&k_empty[st], ((p_g / STAGES) & 1) ^ 1, 2000000 + p_g, a.dbg);
+              mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
+              uint8_t* sk = smem + L::OFF_K + st * L::K_BYTES;
+              for (int b = 0; b < L::NB; ++b)
+                tma_load_2d(sk + b * L::KV_BLOCK, &tmKV, &k_full[st], a.k_col + h * HD + b * 16, row0 + j * BKV);
+              ++p_g;
+            }
+            if (do_v) {
+              const int st = pv_g % STAGES;
+              mbar_wait_dbg(&v_empty[st], ((pv_g / STAGES) & 1) ^ 1, 2500000 + pv_g, a.dbg);
+              mbar_arrive_expect_tx(&v_full[st], L::K_BYTES);
+              uint8_t* sv = smem + L::OFF_V + st * L::V_BYTES;
+              for (int b = 0; b < L::NB; ++b)
+                tma_load_2d(sv + b * L::KV_BLOCK, &tmKV, &v_full[st], a.v_col + h * HD + b * 16, row0 + j * BKV);
+              ++pv_g;
+            }
           }
         }
       }
@@ -201,13 +218,14 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         auto issue_s = [&](int gg, uint32_t sq) {
           const int st = gg % STAGES;
           wait_sel<SPIN & 1>(&k_full[st], (gg / STAGES) & 1, 3000000 + gg, a.dbg);
+          if (a.trace && blockIdx.x == 0 && gg >= 2 && gg - 2 < 256) a.trace[1536 + gg - 2] = clock64();
           tc_fence_after();
           const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
 #pragma unroll
           for (int b = 0; b < L::NB; ++b)
             umma_f16(tmem + (gg % NS) * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
                      desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
-          umma_commit(&k_empty[st]);
+          if constexpr (!LEAN) umma_commit(&k_empty[st]);
           umma_commit(&s_full[gg % NS]);
         };
         int local = 0;
@@ -221,17 +239,26 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           for (int j = 0; j < nkv; ++j, ++m_g) {
             const int sb = m_g % NS, st = m_g % STAGES;
             wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
+            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = clock64();
             wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
+            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1024 + m_g] = clock64();
             tc_fence_after();
             const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
 #pragma unroll
             for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
               umma_f16_ts(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16), desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
                           idesc_pv, (j | kc) != 0);
-            umma_commit(&v_empty[st]);
-            umma_commit(&o_done[sb]);
+            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1280 + m_g] = clock64();
+            if constexpr (LEAN) {
+              if (pass == 1) umma_commit(&o_done[m_g1++ % NS]);
+              if (j == nkv - 1) umma_commit(item_done);
+            } else {
+              umma_commit(&v_empty[st]);
+              umma_commit(&o_done[sb]);
+            }
             if (j + NS < nkv) issue_s(m_g + NS, sq);
-            if (j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
+            if (!LEAN && j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
+            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[768 + m_g] = clock64();
           }
           ++m_it;
         }
@@ -275,6 +302,12 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         for (int j = 0; j < nkv; ++j, ++s_g) {
           const int sb = s_g % NS;
           if (a.softmax_only != 1) wait_sel<(SPIN >> 1) & 1>(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, a.dbg);
+          if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[s_g] = clock64();
+          if (LEAN && warp == 2 && lane == 0 && a.softmax_only != 1) {
+            mbar_arrive(&k_empty[s_g % STAGES]);                    // S(g) has consumed K(g)
+            if (s_g >= 2) mbar_arrive(&v_empty[(s_g - 2) % STAGES]);  // P.V(g-2) precedes S(g)
+            if (j == nkv - 1) mbar_arrive(&q_empty[s_it & 1]);      // last S of the item read Q
+          }
           if (a.softmax_only == 2) {  // microbenchmark: MMA/TMA pipeline alone
             tc_fence_before();
             __syncwarp();
@@ -314,7 +347,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
               const float m_new = fmaxf(m_ref, mx);
               if (j > 0 && part == 0) {
-                const int gp = s_g - 1;  // previous P.V must be complete before O is rescaled
+                const int gp = LEAN ? s_g1 - 1 : s_g - 1;  // previous P.V complete before O is rescaled
                 mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, a.dbg);
                 tc_fence_after();
                 const float f = fast_exp2((m_ref - m_new) * c);
@@ -346,11 +379,19 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           tc_fence_before();
           __syncwarp();
           if (lane == 0 && a.softmax_only != 1) mbar_arrive(&p_full[sb]);
+          if (pass == 1) ++s_g1;
+          if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[256 + s_g] = clock64();
         }
         // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
         // part, part + SPLIT, ...
         const int gl = s_g - 1;
-        if (a.softmax_only != 1) mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, a.dbg);
+        if (a.softmax_only != 1) {
+          if constexpr (LEAN)
+            mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, a.dbg);
+          else
+            mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, a.dbg);
+        }
+        ++s_it;
         tc_fence_after();
         float lsum[8];
         tmem_ld8(lane_base + L::OCOL + HD, lsum);
@@ -389,10 +430,10 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
 
 // Kernel variants per head dim; variant 0 is the production choice, the others exist for A/B
 // measurement (DART_FA_VARIANT, scripts/bench_attn.py).
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN>
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN>
 int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
   using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
-  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN>;
+  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
@@ -427,22 +468,27 @@ int fa_variant() {
 }
 
 // Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16).
-#define DART_FA80_VARIANTS(X)   \
-  X(0, 80, 64, 3, 2, 2, 1, 0, 0) \
-  X(1, 80, 64, 3, 2, 2, 1, 4, 0)
-#define DART_FA16_VARIANTS(X)   \
-  X(0, 16, 96, 4, 2, 2, 1, 6, 0) \
-  X(1, 16, 96, 4, 2, 2, 1, 8, 0)
-// Measured on B200 (scripts/bench_attn.py, hd 16 enc self-attention N=80 = 80x16 heads x 5184^2):
-// variant 0 8.70 ms (NPOLY 6), NPOLY 8 9.67, NPOLY 4 9.1, 2 column slices 9.6-10.5, 64-key tiles
-// with 3 S buffers 11.0, 48-key tiles with 4 S buffers 13.3, one CTA/SM with 3-4 S buffers 15.3,
-// spin waits 9.8.  Softmax alone (no MMA) 6.76 ms; MMA/TMA pipeline alone 6.94 ms: tcgen05.mma
-// costs >= 44 clk per instruction even at N = 32 (scripts/probes/mma_rate.cu), so the 6 P.V steps
-// of a 96-key tile (~266 clk) plus S (~57 clk) load the tensor pipe ~2/3 as much as the exps load
-// MUFU.  Staging P in shared memory or in separate TMEM buffers (S released at load time) was
-// slower (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.
+#define DART_FA80_VARIANTS(X)      \
+  X(0, 80, 64, 3, 2, 2, 1, 0, 0, 1) \
+  X(1, 80, 64, 3, 2, 2, 1, 0, 0, 0) \
+  X(2, 80, 64, 3, 2, 2, 1, 4, 0, 1)
+#define DART_FA16_VARIANTS(X)      \
+  X(0, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
+  X(1, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
+  X(2, 16, 96, 4, 2, 2, 1, 8, 0, 1) \
+  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 1)
+// Measured on B200 (scripts/bench_attn.py, hd 16 enc self-attention N=80 = 80x16 heads x 5184^2;
+// box-to-box spread ~8%): variant 0 8.7-9.4 ms; NPOLY 8 9.7, NPOLY 4 9.1; 2 column slices
+// 9.6-10.5; 64-key tiles with 3 S buffers 11.0; 48-key tiles at 4 CTAs/SM 11.1-11.7; one CTA/SM
+// with 3-4 S buffers 15.3; spin waits 9.8.  Softmax alone (no MMA) 6.76 ms, MMA/TMA pipeline
+// alone 6.7-6.9 ms.  tcgen05.mma costs >= 44 clk per instruction and issuer even at N = 32, each
+// commit ~44 clk and each mbarrier wait ~40 clk of the issuer's tensor stream
+// (scripts/probes/mma_rate.cu), so the 6 P.V steps of a 96-key tile plus S, commits and waits
+// make a ~600-clk per-tile MMA chain (scripts/trace_attn.py timelines) that S(g+2) sits behind.
+// Staging P in shared memory or in separate TMEM buffers (S released at load time) was slower
+// (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.
 int kv_tile_of(int hd, int var) {
-#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN) \
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
   if (hd == HD && var == V) return BKV;
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
@@ -464,13 +510,13 @@ bool attention_tc_supported(int head_dim, int Lkv) {
 int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream) {
   const int var = fa_variant();
-#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN) \
-  if (head_dim == HD && var == V) return launch_v<HD, BKV, ST, CT, NS, SP, NP, SN>(tmQ, tmKV, a, num_sms, stream);
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
+  if (head_dim == HD && var == V) return launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN>(tmQ, tmKV, a, num_sms, stream);
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
 #undef X
-  if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0>(tmQ, tmKV, a, num_sms, stream);
-  if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0, 1>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0, 1>(tmQ, tmKV, a, num_sms, stream);
   return (int)cudaErrorInvalidValue;
 }
 

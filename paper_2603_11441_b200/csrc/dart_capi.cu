@@ -100,6 +100,7 @@ bool tc_attention_enabled() {
 
 // Tests: route every tcgen05 attention item through the max-tracking (overflow-safe) pass too.
 int g_attn_force_safe = 0;
+long long* g_attn_trace = nullptr;
 
 // tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
 // [items*Lkv, kv_ld] (k at k_col, v at v_col), output [items*Lq, o_ld] at column h*hd.
@@ -124,6 +125,7 @@ int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   a.dbg = dbg;
   a.force_safe = g_attn_force_safe;
+  a.trace = g_attn_trace;
   {
     const char* e = getenv("DART_FA_SOFTMAX_ONLY");  // microbenchmarks: 1 softmax alone, 2 MMA alone
     a.softmax_only = e ? atoi(e) : 0;
@@ -959,6 +961,7 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 }  // extern "C"
 
 extern "C" void dart_attention_force_safe(int32_t on) { g_attn_force_safe = on ? 1 : 0; }
+extern "C" void dart_attention_trace(int64_t* device_buf) { g_attn_trace = (long long*)device_buf; }
 
 extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
                                   int32_t* debug_host, void* stream) {

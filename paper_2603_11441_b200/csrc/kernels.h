@@ -95,6 +95,7 @@ struct AttnTcArgs {
   int force_safe = 0;          // tests: re-run every item through the max-tracking softmax pass
   int z_base = 0;              // first item of this launch (items are chunked on the host)
   int softmax_only = 0;        // microbenchmark: softmax warps run on stale S without MMA / TMA
+  long long* trace = nullptr;  // microbenchmark: CTA 0 clock64 stamps [7][256] of the first 256 tiles
 };
 constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
 int attention_tc_kv_tile(int head_dim);  // 192 (hd 80), 96 (hd 16), 0 = unsupported
