@@ -458,10 +458,19 @@ def kernel_roofline(det, model, cfg, dev, args):
     t = e0.elapsed_time(e1) / reps / 1000.0
     achieved = 2.0 * M * N * K / t / 1e12
     peak = pk["bf16_tflops"]
+    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
+            tj = json.load(f)["gemm_fc1"]
+        if args.batch == 1:
+            traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+    except Exception:
+        pass
     return {"kernel": "gemm_tc_kernel<256,4,EPI_F16_RELU> (backbone mlp.fc1)", "bound": "tensor",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_kind": f"{pk_kind} burst bf16/fp16 dense", "flop_per_launch": 2.0 * M * N * K,
-            "us_per_launch": t * 1e6, "traffic": None}
+            "us_per_launch": t * 1e6, "traffic": traffic,
+            "traffic_note": "dram read+write bytes per launch, ncu --set full (profiles/r01/roofline_traffic.json)"}
 
 
 def main():

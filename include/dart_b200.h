@@ -132,6 +132,8 @@ void dart_attention_force_safe(int32_t on);
  * tiles (S ready, P written, P seen by the MMA issuer, MMAs issued, V ready, P.V issued, next K
  * ready); NULL disables. */
 void dart_attention_trace(int64_t* device_buf);
+/* Microbenchmarks: select the tcgen05 attention kernel variant (0 = production). */
+void dart_attention_variant(int32_t v);
 
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */

@@ -33,6 +33,7 @@ EXPORTS = (
     "dart_gemm_force_plan",
     "dart_attention_force_safe",
     "dart_attention_trace",
+    "dart_attention_variant",
     "dart_attention",
     "dart_attention_qkv",
     "dart_launch_count",
@@ -114,6 +115,8 @@ def load() -> ctypes.CDLL:
     lib.dart_attention_force_safe.restype = None
     lib.dart_attention_trace.argtypes = [P]
     lib.dart_attention_trace.restype = None
+    lib.dart_attention_variant.argtypes = [I32]
+    lib.dart_attention_variant.restype = None
     lib.dart_launch_count.argtypes = [P]
     lib.dart_launch_count.restype = ctypes.c_int64
     lib.dart_reset_launch_count.argtypes = [P]

@@ -458,13 +458,13 @@ int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& 
   return 0;
 }
 
+int g_fa_variant = -1;  // DART_FA_VARIANT, or attention_tc_set_variant (A/B microbenchmarks)
 int fa_variant() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_fa_variant < 0) {
     const char* e = getenv("DART_FA_VARIANT");
-    v = e ? atoi(e) : 0;
+    g_fa_variant = e ? atoi(e) : 0;
   }
-  return v;
+  return g_fa_variant;
 }
 
 // Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16).
@@ -499,6 +499,8 @@ int kv_tile_of(int hd, int var) {
 }
 
 }  // namespace
+
+void attention_tc_set_variant(int v) { g_fa_variant = v < 0 ? 0 : v; }
 
 int attention_tc_kv_tile(int head_dim) { return kv_tile_of(head_dim, fa_variant()); }
 

@@ -962,6 +962,7 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 
 extern "C" void dart_attention_force_safe(int32_t on) { g_attn_force_safe = on ? 1 : 0; }
 extern "C" void dart_attention_trace(int64_t* device_buf) { g_attn_trace = (long long*)device_buf; }
+extern "C" void dart_attention_variant(int32_t v) { attention_tc_set_variant(v); }
 
 extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, int32_t L, int32_t hd,
                                   int32_t* debug_host, void* stream) {

@@ -98,7 +98,8 @@ struct AttnTcArgs {
   long long* trace = nullptr;  // microbenchmark: CTA 0 clock64 stamps [7][256] of the first 256 tiles
 };
 constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
-int attention_tc_kv_tile(int head_dim);  // 192 (hd 80), 96 (hd 16), 0 = unsupported
+int attention_tc_kv_tile(int head_dim);
+void attention_tc_set_variant(int v);  // microbenchmarks (DART_FA_VARIANT otherwise)  // 192 (hd 80), 96 (hd 16), 0 = unsupported
 bool attention_tc_supported(int head_dim, int Lkv);
 // tmQ: 2-D map over the Q buffer [items*Lq, cols] fp16, box {16, 128}, 32B swizzle;
 // tmKV: map over the K/V buffer [items*Lkv, cols], box {16, kv_tile}.
