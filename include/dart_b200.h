@@ -97,6 +97,15 @@ int dart_postprocess(dart_model* m, const double* boxes, const double* score_log
                      double* kept_score, double* presence_prob, int32_t* keep_flag, int32_t* scratch,
                      void* stream);
 
+/* Mask head (the non-detection-only path, mask_head_forward, model.py:573-579).
+ * dart_model_set_mask_head uploads the four mask tensors (HOST float32, reference [in, out]
+ * layout: mask.query_proj.w [d, d], .b [d], mask.feat_proj.w [F0, d], .b [d]).
+ * dart_mask_head: query_features [B*N, Q, d] fp32 (dart_encdec's optional output), l0 [B, T, F0]
+ * fp32 -> masks [B*N, Q, T] fp32 = (qf Wq + bq) (L0[b] Wf + bf)^T per image b. */
+int dart_model_set_mask_head(dart_model* m, const float* wq, const float* bq, const float* wf, const float* bf);
+int dart_mask_head(dart_model* m, const float* query_features, int32_t B, int32_t N, const float* l0, float* masks,
+                   void* stream);
+
 /* Kernel-level entry points (used by the per-kernel parity tests and microbenchmarks).
  * dart_gemm: out = epilogue(A[M,K] . W[N,K]^T + bias), A/W fp16 K-major, K % 64 == 0,
  *   N % 64 == 0; epi 0 fp16 out, 1 fp16 relu, 2 fp32 out, 3 fp32 out += , 4 fp16 with RoPE on

@@ -399,6 +399,14 @@ def encdec(P, cfg: OracleConfig, level0, texts):
             np.array([o[2] for o in outs], dtype=np.float64), np.stack([o[3] for o in outs]))
 
 
+def mask_head(P, level0, query_features):
+    """Per-query mask logits over the level-0 grid (model.py:573-579):
+    (qf Wq + bq) (L0 Wf + bf)^T -> [N, queries, tokens]."""
+    mq = query_features @ P["mask.query_proj.w"] + P["mask.query_proj.b"]
+    mf = level0 @ P["mask.feat_proj.w"] + P["mask.feat_proj.b"]
+    return mq @ mf.T
+
+
 # ----------------------------------------------------------------------------
 # post-processing (pipeline.py:243-294)
 # ----------------------------------------------------------------------------

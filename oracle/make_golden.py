@@ -8,6 +8,7 @@ here, never on the GPU box.  The fixtures are what pins the oracle restatement
 (`tests/test_gpu_parity.py`).  Configs follow SURVEY.md 8(d):
 
   A  SPEC toy profile (`toy_config(seed=0)`), 64^2, names car/person/dog (+8-class list)
+  M  A with the mask head (mask_head_forward outputs)
   B  small-1008: full-width ViT-H/14 kernels at 4 blocks (globals 1,3), 6+6 enc-dec, 3 classes
   C  full ViT-H/14 DART 1008^2, 4 classes (person, car, dog, bicycle)
 
@@ -134,8 +135,41 @@ def make(name: str, cfg, scene: SceneSpec, names, stride: int, extra_thresholds=
     print(f"{name}: wrote {path}; build {t_build:.1f}s backbone {t_bb:.1f}s encdec {t_ed:.1f}s")
 
 
+def make_mask(name: str, cfg, scene: SceneSpec, names):
+    """Mask-head golden: the reference model WITH its mask head, the
+    reference mask_head_forward (model.py:573-579) on its own backbone/enc-dec outputs."""
+    import hashlib
+
+    model = M.build_model(cfg, with_mask_head=True)
+    image, _ = generate_scene(scene)
+    fpn = M.backbone_forward(model, image, FP32)
+    emb = M.text_encode(model, list(names))
+    raw = M.encdec_forward(model, fpn, emb.stack(list(names)), FP32)
+    masks = M.mask_head_forward(model, fpn, raw)
+    out = {
+        "config_json": np.array(json.dumps(cfg.to_dict())),
+        "weights_checksum": np.array(M.weights_checksum(model)),
+        "mask_param_checksums": np.array([hashlib.blake2b(model.params[n].tobytes(), digest_size=8).hexdigest()
+                                          for n in ("mask.query_proj.w", "mask.query_proj.b", "mask.feat_proj.w",
+                                                    "mask.feat_proj.b")]),
+        "names": np.array(list(names)),
+        "L0": fpn.levels[0],
+        "query_features": raw.query_features,
+        "masks": masks,
+        "score_logits": raw.score_logits,
+    }
+    if cfg.image_size <= 64:
+        out["image"] = image.astype(np.float32)
+    path = os.path.join(OUT, f"golden_{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: wrote {path}; masks {masks.shape}")
+
+
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "A"
+    if which == "M":
+        make_mask("M", M.toy_config(seed=0), SceneSpec(seed=1, num_classes=3), ["car", "person", "dog"])
+        return
     if which == "A":
         make("A", M.toy_config(seed=0), SceneSpec(seed=1, num_classes=3), ["car", "person", "dog"], stride=1,
              extra_thresholds={"mid": dict(presence_threshold=0.3, score_threshold=0.3)},

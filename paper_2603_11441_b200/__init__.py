@@ -20,6 +20,7 @@ from .model import (  # noqa: F401
     encdec_forward,
     load_model,
     mask_head_forward,
+    mask_head_forward_device,
     models_equal,
     save_model,
     set_sub_block,

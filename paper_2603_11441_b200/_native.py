@@ -28,6 +28,8 @@ EXPORTS = (
     "dart_backbone",
     "dart_encdec",
     "dart_postprocess",
+    "dart_model_set_mask_head",
+    "dart_mask_head",
     "dart_gemm",
     "dart_gemm_plan",
     "dart_gemm_force_plan",
@@ -100,6 +102,10 @@ def load() -> ctypes.CDLL:
     lib.dart_encdec.restype = ctypes.c_int
     lib.dart_postprocess.argtypes = [P, P, P, P, I32, I32, F64, F64, F64, I32, P, P, P, P, P, P, P]
     lib.dart_postprocess.restype = ctypes.c_int
+    lib.dart_model_set_mask_head.argtypes = [P, P, P, P, P]
+    lib.dart_model_set_mask_head.restype = ctypes.c_int
+    lib.dart_mask_head.argtypes = [P, P, I32, I32, P, P, P]
+    lib.dart_mask_head.restype = ctypes.c_int
     lib.dart_gemm.argtypes = [P, P, P, P, P, I32, I32, I32, I32, P, P, I32, I32, I32, P]
     lib.dart_gemm.restype = ctypes.c_int
     lib.dart_gemm_plan.argtypes = [I32, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]

@@ -227,8 +227,13 @@ struct dart_model {
   float* queries = nullptr;  // [Q+1, d] fp32 (queries then presence token)
   float *box_w = nullptr, *box_b = nullptr, *score_w = nullptr, *score_b = nullptr, *pres_w = nullptr,
         *pres_b = nullptr;
+  // optional mask head (dart_model_set_mask_head)
+  bool has_mask = false;
+  GemmW mask_q, mask_f;
   // workspaces
-  Workspace bb_ws, ed_ws;
+  Workspace bb_ws, ed_ws, mask_ws;
+  size_t mask_cap_rows = 0, mask_cap_tok = 0;
+  __half *mk_qf = nullptr, *mk_l0 = nullptr, *mk_mq = nullptr, *mk_mf = nullptr;
   int bb_cap = 0, ed_cap_items = 0, ed_cap_n = 0, ed_cap_b = 0;
   int last_backbone_B = 0;
   struct {
@@ -244,6 +249,7 @@ struct dart_model {
   ~dart_model() {
     bb_ws.release();
     ed_ws.release();
+    mask_ws.release();
   }
 };
 
@@ -675,6 +681,9 @@ int dart_model_fork(const dart_model* parent, dart_model** out) {
   dart_model* f = new dart_model(*parent);  // shares the weights (shared_ptr), copies dims and maps
   f->bb_ws = Workspace();                   // own, initially empty activation workspaces
   f->ed_ws = Workspace();
+  f->mask_ws = Workspace();
+  f->mask_cap_rows = f->mask_cap_tok = 0;
+  f->mk_qf = f->mk_l0 = f->mk_mq = f->mk_mf = nullptr;
   f->bb_cap = f->ed_cap_items = f->ed_cap_n = f->ed_cap_b = 0;
   f->last_backbone_B = 0;
   f->bb = {};
@@ -959,6 +968,62 @@ int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t
 }
 
 }  // extern "C"
+
+extern "C" int dart_model_set_mask_head(dart_model* m, const float* wq, const float* bq, const float* wf,
+                                        const float* bf) {
+  if (!m || !wq || !bq || !wf || !bf) return fail(DART_ERR_INVALID, "dart_model_set_mask_head: bad args");
+  const int D = m->D, F0 = m->F0;
+  float* scratch = nullptr;
+  if (cudaMalloc(&scratch, (size_t)std::max(D, F0) * D * sizeof(float)) != cudaSuccess)
+    return fail(DART_ERR_CUDA, "mask head upload scratch");
+  const float* ptrs[4] = {wq, bq, wf, bf};
+  WeightCursor c{ptrs, 4};
+  const bool ok = make_gemm(m, c, D, D, scratch, m->mask_q) && make_gemm(m, c, F0, D, scratch, m->mask_f);
+  const cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(scratch);
+  if (!ok || e != cudaSuccess) return fail(DART_ERR_CUDA, "mask head weight upload failed");
+  m->has_mask = true;
+  return DART_OK;
+}
+
+extern "C" int dart_mask_head(dart_model* m, const float* query_features, int32_t B, int32_t N, const float* l0,
+                              float* masks, void* stream) {
+  if (!m || !query_features || !l0 || !masks || B <= 0 || N <= 0) return fail(DART_ERR_INVALID, "dart_mask_head: bad args");
+  if (!m->has_mask) return fail(DART_ERR_INVALID, "dart_mask_head: no mask head uploaded (dart_model_set_mask_head)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int D = m->D, F0 = m->F0, T = m->T, Q = m->d.num_queries;
+  const size_t rows = (size_t)B * N * Q, tok = (size_t)B * T;
+  if (rows > m->mask_cap_rows || tok > m->mask_cap_tok) {
+    m->mask_ws.release();
+    m->mk_qf = (__half*)m->mask_ws.get(rows * D * 2);
+    m->mk_mq = (__half*)m->mask_ws.get(rows * D * 2);
+    m->mk_l0 = (__half*)m->mask_ws.get(tok * F0 * 2);
+    m->mk_mf = (__half*)m->mask_ws.get(tok * D * 2);
+    if (!m->mk_qf || !m->mk_mq || !m->mk_l0 || !m->mk_mf) {
+      m->mask_ws.release();
+      m->mask_cap_rows = m->mask_cap_tok = 0;
+      return fail(DART_ERR_CUDA, "mask head workspace allocation failed");
+    }
+    m->mask_cap_rows = rows;
+    m->mask_cap_tok = tok;
+  }
+  // mq = qf Wq + bq, mf = L0 Wf + bf (model.py:577-578), fp16 operands / fp32 accumulation
+  LAUNCH(cast_f32_to_f16(query_features, m->mk_qf, (long long)rows * D, s));
+  LAUNCH(cast_f32_to_f16(l0, m->mk_l0, (long long)tok * F0, s));
+  RUN(gemm(m, m->mk_qf, (int)rows, D, m->mask_q, EPI_F16, epi_out(m->mk_mq, D), s));
+  RUN(gemm(m, m->mk_l0, (int)tok, F0, m->mask_f, EPI_F16, epi_out(m->mk_mf, D), s));
+  // logits[b, c] = mq[b, c] mf[b]^T (model.py:579): mf[b] is the K-major "weight" of a GEMM
+  for (int b = 0; b < B; ++b) {
+    GemmW g;
+    g.w = m->mk_mf + (size_t)b * T * D;
+    g.b = nullptr;
+    g.N = T;
+    g.K = D;
+    if (!finish_gemmw(g)) return fail(DART_ERR_INVALID, "dart_mask_head: tokens must be a multiple of 32");
+    RUN(gemm(m, m->mk_mq + (size_t)b * N * Q * D, N * Q, D, g, EPI_F32, epi_out(masks + (size_t)b * N * Q * T, T), s));
+  }
+  return DART_OK;
+}
 
 extern "C" void dart_attention_force_safe(int32_t on) { g_attn_force_safe = on ? 1 : 0; }
 extern "C" void dart_attention_trace(int64_t* device_buf) { g_attn_trace = (long long*)device_buf; }

@@ -370,6 +370,10 @@ class _Handle:
         handle = ctypes.c_void_p()
         with torch.cuda.device(device):
             _native.check(lib.dart_model_create(ctypes.byref(desc), ptrs, len(arrays), ctypes.byref(handle)))
+            if model.has_mask_head and "mask.query_proj.w" in model.params:
+                mk = [np.ascontiguousarray(model.params[n], dtype=np.float32)
+                      for n in ("mask.query_proj.w", "mask.query_proj.b", "mask.feat_proj.w", "mask.feat_proj.b")]
+                _native.check(lib.dart_model_set_mask_head(handle, *[a.ctypes.data for a in mk]))
         self.ptr = handle
         self.device = device
         self.lib = lib
@@ -561,11 +565,42 @@ def encdec_forward(model: DetectorModel, fpn: FpnFeatures, text_batch: list[np.n
     return encdec_forward_device(model, l0, text, 1, len(text_batch))
 
 
-def mask_head_forward(model: DetectorModel, fpn: FpnFeatures, queries: RawQueryOutputs) -> np.ndarray:
-    """Mask logits are outside the detection-only path."""
+def mask_head_forward_device(model: DetectorModel, l0, query_features, B: int = 1):
+    """Device mask logits: l0 [B, T, F0] f32, query_features [B*N, Q, d] f32 (torch, cuda) ->
+    [B*N, Q, T] f32 = (qf Wq + bq)(L0[b] Wf + bf)^T (model.py:573-579)."""
+    import torch
+
     if not model.has_mask_head:
         raise MaskHeadRemovedError("mask head removed: this model is detection-only")
-    raise NotImplementedError("the mask head is out of scope for the B200 detection path")
+    cfg = model.config
+    dev = _device()
+    h = native_handle(model, dev)
+    items = int(query_features.shape[0])
+    if items % B:
+        raise ValueError("query feature batch is not a multiple of the image batch")
+    out = torch.empty((items, cfg.num_queries, cfg.tokens), device=dev, dtype=torch.float32)
+    _native.check(h.lib.dart_mask_head(h.ptr, query_features.contiguous().data_ptr(), B, items // B,
+                                       l0.contiguous().data_ptr(), out.data_ptr(), _stream_ptr(dev)))
+    return out
+
+
+def mask_head_forward(model: DetectorModel, fpn: FpnFeatures, queries: RawQueryOutputs) -> np.ndarray:
+    """Per-query mask logits over the level-0 token grid [N, queries, tokens] (model.py:573-579),
+    computed on the GPU (fp16 operands, fp32 accumulation); float64 host array like the reference."""
+    import torch
+
+    if not model.has_mask_head:
+        raise MaskHeadRemovedError("mask head removed: this model is detection-only")
+    cfg = model.config
+    dev = _device()
+    l0 = fpn.device_levels[0] if isinstance(fpn, FpnFeatures) else torch.from_numpy(
+        np.ascontiguousarray(fpn.levels[0], dtype=np.float32))
+    l0 = l0.to(device=dev, dtype=torch.float32).reshape(1, cfg.tokens, cfg.fpn_dims[0])
+    qf = getattr(queries, "d_query_features", None)
+    if qf is None:
+        qf = torch.from_numpy(np.ascontiguousarray(queries.query_features, dtype=np.float32))
+    qf = qf.to(device=dev, dtype=torch.float32)
+    return mask_head_forward_device(model, l0, qf, 1).double().cpu().numpy()
 
 
 # ---------------------------------------------------------------------------- structural edits

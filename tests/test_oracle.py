@@ -123,3 +123,15 @@ def test_rope_matches_complex_rotation():
     y = O.rope(x, cos, sin)
     np.testing.assert_allclose(y[:, 0::2], z.real, atol=1e-12)
     np.testing.assert_allclose(y[:, 1::2], z.imag, atol=1e-12)
+
+
+def test_mask_head_matches_reference_golden():
+    """Mask head restatement (model.py:573-579) vs the reference's own outputs (golden M):
+    mask weights bit-exact, logits from the reference's L0 / query features to 1e-12."""
+    g = load_golden("M")
+    P = O.build_params(cfg_from(g), with_mask_head=True)
+    got = [hashlib.blake2b(np.asarray(P[n], dtype=np.float64).tobytes(), digest_size=8).hexdigest()
+           for n in ("mask.query_proj.w", "mask.query_proj.b", "mask.feat_proj.w", "mask.feat_proj.b")]
+    assert got == [str(x) for x in g["mask_param_checksums"]]
+    m = O.mask_head(P, g["L0"], g["query_features"])
+    np.testing.assert_allclose(m, g["masks"], rtol=1e-12, atol=1e-12)
