@@ -235,6 +235,127 @@ __global__ void __launch_bounds__(WARPS * 32, HD == 16 ? 6 : 1) flash_attn_kerne
   }
 }
 
+// Short-key attention for the encoder's text cross-attention (hd 16, <= 32 text tokens,
+// reference model.py:518 via _mha :491-502): one CTA = 64 query rows of one item x ALL heads,
+// so the query rows are read once as full 512-byte lines and the class's text K / V
+// (32 x heads*16) are staged once per CTA instead of once per (row block, head).  Warp w: 16
+// rows (w & 3) x half of the heads (w >> 2); per head S = Q_h K_h^T (4 mma.sync), exact softmax
+// over the 32 keys in registers (quad shuffles), O_h = P V_h (4 mma.sync), written back over
+// Q_h in shared memory, then one coalesced store of the output tile.
+constexpr int XS_ROWS = 64, XS_LK = 32, XS_PITCH = 256 + 8;
+
+__global__ void __launch_bounds__(256, 3) xattn_short_kernel(AttnArgs a) {
+  extern __shared__ __align__(128) __half smem_xs[];
+  __half* sQ = smem_xs;                          // [XS_ROWS][XS_PITCH]
+  __half* sK = sQ + XS_ROWS * XS_PITCH;          // [XS_LK][XS_PITCH]
+  __half* sV = sK + XS_LK * XS_PITCH;            // [XS_LK][XS_PITCH]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int z = blockIdx.y, q0 = blockIdx.x * XS_ROWS;
+  const int E = a.heads * 16, CH = E / 8;
+  const int zkv = a.kv_batch_mod > 0 ? z % a.kv_batch_mod : z;
+  for (int idx = tid; idx < XS_LK * CH; idx += 256) {
+    const int r = idx / CH, c = idx % CH;
+    const bool ok = r < a.Lk;
+    const long long kr = (long long)zkv * a.k_batch_stride + (long long)r * a.k_tok_stride + c * 8;
+    const long long vr = (long long)zkv * a.v_batch_stride + (long long)r * a.v_tok_stride + c * 8;
+    cp_async16(smem_u32(&sK[r * XS_PITCH + c * 8]), ok ? a.k + kr : a.k, ok);
+    cp_async16(smem_u32(&sV[r * XS_PITCH + c * 8]), ok ? a.v + vr : a.v, ok);
+  }
+  for (int idx = tid; idx < XS_ROWS * CH; idx += 256) {
+    const int r = idx / CH, c = idx % CH;
+    const int qi = q0 + r;
+    const bool ok = qi < a.Lq;
+    const long long qo = (long long)z * a.q_batch_stride + (long long)qi * a.q_tok_stride + c * 8;
+    cp_async16(smem_u32(&sQ[r * XS_PITCH + c * 8]), ok ? a.q + qo : a.q, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const float c = a.scale_log2;
+  const int t = lane & 3, g = lane >> 2;
+  __half* rowbase = sQ + ((warp & 3) * 16) * XS_PITCH;
+  const int hh = (a.heads + 1) >> 1, h_lo = (warp >> 2) * hh, h_hi = min(a.heads, h_lo + hh);
+#pragma unroll 1
+  for (int h = h_lo; h < h_hi; ++h) {
+    uint32_t qa[4];
+    ldmatrix_x4(qa, smem_u32(&rowbase[(lane & 15) * XS_PITCH + h * 16 + (lane >> 4) * 8]));
+    float s[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int np = 0; np < 2; ++np) {
+      uint32_t b[4];
+      const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+      const int dim = h * 16 + ((lane >> 3) & 1) * 8;
+      ldmatrix_x4(b, smem_u32(&sK[key * XS_PITCH + dim]));
+      mma16816(s[2 * np], qa, b);
+      mma16816(s[2 * np + 1], qa, b + 2);
+    }
+    if (a.Lk < XS_LK) {
+#pragma unroll
+      for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (n * 8 + 2 * t + (e & 1) >= a.Lk) s[n][e] = -INFINITY;
+    }
+    float mx0 = fmax3f(s[0][0], s[0][1], s[1][0]), mx1 = fmax3f(s[0][2], s[0][3], s[1][2]);
+    mx0 = fmax3f(mx0, s[1][1], s[2][0]);
+    mx1 = fmax3f(mx1, s[1][3], s[2][2]);
+    mx0 = fmax3f(mx0, s[2][1], s[3][0]);
+    mx1 = fmax3f(mx1, s[2][3], s[3][2]);
+    mx0 = fmaxf(mx0, s[3][1]);
+    mx1 = fmaxf(mx1, s[3][3]);
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float nb0 = -mx0 * c, nb1 = -mx1 * c;
+    uint32_t pa[2][4];
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const __half2 h01 = __floats2half2_rn(fast_exp2(fmaf(s[n][0], c, nb0)), fast_exp2(fmaf(s[n][1], c, nb0)));
+      const __half2 h23 = __floats2half2_rn(fast_exp2(fmaf(s[n][2], c, nb1)), fast_exp2(fmaf(s[n][3], c, nb1)));
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);  // sum what P.V multiplies
+      l0 += f01.x + f01.y;
+      l1 += f23.x + f23.y;
+      pa[n >> 1][(n & 1) * 2 + 0] = *reinterpret_cast<const uint32_t*>(&h01);
+      pa[n >> 1][(n & 1) * 2 + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    float o[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t b[4];
+      ldmatrix_x4_trans(b, smem_u32(&sV[(ks * 16 + (lane & 15)) * XS_PITCH + h * 16 + (lane >> 4) * 8]));
+      mma16816(o[0], pa[ks], b);
+      mma16816(o[1], pa[ks], b + 2);
+    }
+    const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+    __syncwarp();  // every lane has read Q_h of these rows (ldmatrix above) before it is overwritten
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      *reinterpret_cast<uint32_t*>(&rowbase[g * XS_PITCH + h * 16 + n * 8 + 2 * t]) =
+          pack_half2(o[n][0] * inv0, o[n][1] * inv0);
+      *reinterpret_cast<uint32_t*>(&rowbase[(g + 8) * XS_PITCH + h * 16 + n * 8 + 2 * t]) =
+          pack_half2(o[n][2] * inv1, o[n][3] * inv1);
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < XS_ROWS * CH; idx += 256) {
+    const int r = idx / CH, cc = idx % CH;
+    const int qi = q0 + r;
+    if (qi < a.Lq)
+      *reinterpret_cast<uint4*>(a.o + (long long)z * a.o_batch_stride + (long long)qi * a.o_tok_stride + cc * 8) =
+          *reinterpret_cast<const uint4*>(&sQ[r * XS_PITCH + cc * 8]);
+  }
+}
+
 template <int HD>
 int launch(const AttnArgs& a, cudaStream_t stream) {
   constexpr int WARPS = 4;
@@ -252,8 +373,30 @@ int launch(const AttnArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
+bool attention_short_supported(const AttnArgs& a, int head_dim) {
+  // below ~2 waves of 64-row CTAs the per-(row block, head) kernel's finer grid wins (N=4: 19 vs 23 us)
+  const long long ctas = (long long)((a.Lq + XS_ROWS - 1) / XS_ROWS) * a.batch;
+  return head_dim == 16 && a.win == 0 && ctas >= 1000 && a.Lk >= 1 && a.Lk <= XS_LK && a.heads * 16 <= 256 &&
+         a.head_stride_q == 16 && a.head_stride_k == 16 && a.head_stride_v == 16 && a.head_stride_o == 16 &&
+         a.q_tok_stride % 8 == 0 && a.k_tok_stride % 8 == 0 && a.v_tok_stride % 8 == 0 && a.o_tok_stride % 8 == 0;
+}
+
+int attention_short(const AttnArgs& a, cudaStream_t stream) {
+  constexpr int SMEM = (XS_ROWS + 2 * XS_LK) * XS_PITCH * 2;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(xattn_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  dim3 grid((a.Lq + XS_ROWS - 1) / XS_ROWS, a.batch);
+  xattn_short_kernel<<<grid, 256, SMEM, stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
 int attention(const AttnArgs& a, int head_dim, cudaStream_t stream) {
   if (a.Lq <= 0 || a.batch <= 0) return 0;
+  if (attention_short_supported(a, head_dim)) return attention_short(a, stream);
   switch (head_dim) {
     case 16: return launch<16>(a, stream);
     case 32: return launch<32>(a, stream);

@@ -81,7 +81,9 @@ struct AttnArgs {
   int kv_batch_mod;      // > 0: K/V batch item = z % kv_batch_mod (class-shared image, per-class text)
   long long img_stride_q, img_stride_k, img_stride_v, img_stride_o;
 };
+// attention() dispatches short-key (text cross-attention) calls to the all-heads-per-CTA kernel.
 int attention(const AttnArgs& a, int head_dim, cudaStream_t stream);
+bool attention_short_supported(const AttnArgs& a, int head_dim);
 
 // tcgen05 flash attention over contiguous row blocks of a token-major QKV buffer.
 struct AttnTcArgs {

@@ -171,6 +171,7 @@ def ref_attention(q, k, v):
 
 
 @pytest.mark.parametrize("hd,Lq,Lk,heads,batch", [(80, 576, 576, 16, 2), (80, 5184, 5184, 2, 1), (16, 5184, 5184, 4, 2),
+                                                  (16, 5184, 32, 16, 13), (16, 4000, 20, 16, 17),
                                                   (16, 201, 5184, 16, 3), (16, 5184, 32, 16, 2), (16, 201, 201, 16, 2),
                                                   (16, 64, 64, 4, 1), (16, 17, 8, 4, 1)])
 def test_attention_dense(lib, hd, Lq, Lk, heads, batch):

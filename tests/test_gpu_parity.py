@@ -221,3 +221,20 @@ def hashlib_image(img):
     import hashlib
 
     return hashlib.blake2b(img.tobytes(), digest_size=16).hexdigest()
+
+
+def test_many_classes_class_shared_text_attention():
+    """16 classes at full width select the all-heads text cross-attention kernel (class-shared
+    image rows, per-class text K/V); the golden classes inside the batch keep their parity."""
+    g = load_golden("B")
+    model = model_for(g)
+    image = scene_for("B", model.config)
+    fpn = D.backbone_forward(model, image)
+    names = [str(n) for n in g["names"]]
+    extra = [f"class{i:02d}" for i in range(13)]
+    allnames = extra[:7] + names + extra[7:]
+    raw = D.encdec_forward(model, fpn, D.text_encode(model, allnames).stack(allnames))
+    sl = slice(7, 7 + len(names))
+    assert np.abs(raw.boxes[sl] - g["boxes"]).max() < 1.02e-2
+    assert np.abs(raw.score_logits[sl] - g["score_logits"]).max() < 4.0e-2
+    assert np.abs(raw.presence_logits[sl] - g["presence_logits"]).max() < 4.0e-2
