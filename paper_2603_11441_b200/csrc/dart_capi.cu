@@ -145,9 +145,12 @@ struct GemmW {
   __half* w = nullptr;  // [N, K] fp16
   float* b = nullptr;   // [N]
   int N = 0, K = 0;
-  CUtensorMap tmap[4];  // box rows 256 / 128 / 64 / 32 (index = box_slot(rows)), built where N allows
+  CUtensorMap tmap[6];  // box rows 256 / 128 / 64 / 32 / 96 / 80 (index = box_slot(rows)), built where N allows
 };
-inline int box_slot(int rows) { return rows == 256 ? 0 : rows == 128 ? 1 : rows == 64 ? 2 : 3; }
+constexpr int kBoxRows[6] = {256, 128, 64, 32, 96, 80};
+inline int box_slot(int rows) {
+  return rows == 256 ? 0 : rows == 128 ? 1 : rows == 64 ? 2 : rows == 32 ? 3 : rows == 96 ? 4 : 5;
+}
 struct LNW {
   float* g = nullptr;
   float* b = nullptr;
@@ -280,7 +283,7 @@ bool upload_wT(dart_model* m, const float* h, int in, int out, __half* dst, int 
 
 bool finish_gemmw(GemmW& g) {
   bool any = false;
-  for (int rows = 256; rows >= 32; rows >>= 1) {  // W box rows = plan.bn / plan.cg
+  for (int rows : kBoxRows) {  // W box rows = plan.bn / plan.cg
     if (g.N % rows) continue;
     if (!make_tmap(&g.tmap[box_slot(rows)], g.w, g.K, g.N, g.K, rows)) return false;
     any = true;

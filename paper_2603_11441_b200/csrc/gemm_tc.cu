@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // (box 32x32, 64B swizzle).  Outputs leave through per-warp smem chunks and TMA bulk stores.
   using L = GemmSmem<BN, STAGES, EPI, CG>;
   constexpr bool RESID = L::RESID;
-  constexpr int CPW = BN / 64;  // 32-column chunks per epilogue warp and tile
+  static_assert(BN % 32 == 0, "32-column epilogue chunks");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
@@ -266,17 +266,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 16; ++i) mbar_init(&rfull[i], 1);
     fence_barrier_init();
-  }
-  if (EPI == EPI_QKV_ROPE && warp >= 4) {
-    // small per-coordinate RoPE tables from the [T, hd/2] tables: row angles of token (c, 0)
-    // (pairs < hd/4) and column angles of token (0, c) (pairs >= hd/4)
-    float2* rs = reinterpret_cast<float2*>(smem + L::ROPE_OFF);
-    const int g = epi.rope_grid, q = epi.rope_hd >> 2, half = epi.rope_hd >> 1;
-    for (int i = threadIdx.x - 128; i < 2 * g * q; i += GEMM_THREADS - 128) {
-      const int which = i / (g * q), c = (i / q) % g, f = i % q;
-      const size_t src = which == 0 ? (size_t)c * g * half + f : (size_t)c * half + q + f;
-      rs[(which * ROPE_MAX_GRID + c) * ROPE_PAD + f] = make_float2(epi.rope_cos[src], epi.rope_sin[src]);
-    }
   }
   if (warp == 2) tmem_alloc_cg<L::TMEM_COLS, CG>(tmem_slot);
   tc_fence_before();
@@ -348,16 +337,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    if constexpr (EPI == EPI_QKV_ROPE) {
+      // small per-coordinate RoPE tables from the [T, hd/2] tables: row angles of token (c, 0)
+      // (pairs < hd/4) and column angles of token (0, c) (pairs >= hd/4).  Filled by the
+      // epilogue warps only, while the producer / MMA warps already run the first tile.
+      float2* rs = reinterpret_cast<float2*>(smem + L::ROPE_OFF);
+      const int g = epi.rope_grid, q = epi.rope_hd >> 2, hh = epi.rope_hd >> 1;
+      for (int i = threadIdx.x - 128; i < 2 * g * q; i += GEMM_THREADS - 128) {
+        const int which = i / (g * q), c = (i / q) % g, f = i % q;
+        const size_t src = which == 0 ? (size_t)c * g * hh + f : (size_t)c * hh + q + f;
+        rs[(which * ROPE_MAX_GRID + c) * ROPE_PAD + f] = make_float2(__ldg(epi.rope_cos + src), __ldg(epi.rope_sin + src));
+      }
+      named_bar_sync(1, GEMM_THREADS - 128);
+    }
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * 2048;  // 2 x 4 KB per warp
     uint64_t* rbar = rfull + (warp - 4) * 2;
     const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
     // residual chunk g of this warp -> smem buffer g & 1 (lane 0 issues; one chunk ahead)
+    const int cpw = (BN - half * 32 + 63) / 64;  // 32-column chunks of this warp per tile
     auto resid_load = [&](int g) {
-      const int t = cl + (g / CPW) * ncl;
+      const int t = cl + (g / cpw) * ncl;
       if (t >= num_tiles) return;
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
-      const int cc = (t % num_n) * BN + ((g % CPW) * 2 + half) * 32;
+      const int cc = (t % num_n) * BN + ((g % cpw) * 2 + half) * 32;
       mbar_arrive_expect_tx(&rbar[g & 1], 32 * 32 * 4);
       tma_load_2d(bufs + (g & 1) * 1024, &tmC, &rbar[g & 1], cc, rr);
     };
@@ -530,6 +533,13 @@ int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, con
 }
 
 GemmPlan g_forced{0, 0};  // dart_gemm_force_plan (tests / A-B measurement); bn 0 = automatic
+// relative per-column efficiency of the 192 / 160-wide CTA-pair tiles (operand re-reads grow
+// as the tile narrows); DART_GEMM_EFF192 / DART_GEMM_EFF160 override for A/B measurement
+double env_or(const char* n, double d) {
+  const char* e = getenv(n);
+  return e ? atof(e) : d;
+}
+double g_eff192 = env_or("DART_GEMM_EFF192", 0.80), g_eff160 = env_or("DART_GEMM_EFF160", 0.70);  // measured: 192 and 160 lose to 256 on every DART shape
 
 }  // namespace
 
@@ -549,12 +559,12 @@ GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
   GemmPlan best{0, 1};
   double best_cost = 0;
   for (int cg = 2; cg >= 1; --cg) {
-    for (int bn = 256; bn >= 64; bn >>= 1) {
-      if (N % bn) continue;
+    for (int bn : {256, 192, 160, 128, 64}) {
+      if (N % bn || (cg == 1 && (bn == 192 || bn == 160))) continue;
       const long long tiles = (long long)((M + BM * cg - 1) / (BM * cg)) * (N / bn);
       const long long units = num_sms / cg;
       const long long waves = (tiles + units - 1) / units;
-      const double eff = bn == 256 ? 1.0 : bn == 128 ? 0.66 : 0.45;
+      const double eff = bn == 256 ? 1.0 : bn == 192 ? g_eff192 : bn == 160 ? g_eff160 : bn == 128 ? 0.66 : 0.45;
       const double cost = (double)waves * bn / eff * (cg == 2 ? 0.97 : 1.0);
       if (best.bn == 0 || cost < best_cost) {
         best = GemmPlan{bn, cg};
@@ -586,6 +596,8 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC,
   if (plan.cg == 2) {
     switch (BN) {
       case 256: return dispatch_epi<256, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 192: return dispatch_epi<192, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 160: return dispatch_epi<160, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
       case 128: return dispatch_epi<128, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
       case 64: return dispatch_epi<64, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
     }

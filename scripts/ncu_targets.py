@@ -13,17 +13,24 @@ lib = _native.load()
 st = torch.cuda.current_stream().cuda_stream
 which = sys.argv[1:] or ["fc1", "out", "encfc1", "att16", "att80", "att80w"]
 calls = []
+inv = 100.0 ** (-torch.arange(20, dtype=torch.float64) / 20)
+rr = torch.arange(72, dtype=torch.float64).repeat_interleave(72)
+cc = torch.arange(72, dtype=torch.float64).repeat(72)
+ang = torch.cat([rr[:, None] * inv, cc[:, None] * inv], 1)
+cos, sin = torch.cos(ang).float().cuda().contiguous(), torch.sin(ang).float().cuda().contiguous()
 for name, (M, N, K, epi) in {"fc1": (5184, 5120, 1280, 1), "out": (5184, 1280, 1280, 3),
-                             "encfc1": (20736, 1024, 256, 1)}.items():
+                             "encfc1": (20736, 1024, 256, 1), "qkv": (5184, 3840, 1280, 4),
+                             "fc2": (5184, 1280, 5120, 3)}.items():
     if name not in which:
         continue
     A = torch.randn(M, K, device="cuda").half()
     W = (torch.randn(N, K, device="cuda") / math.sqrt(K)).half()
     bias = torch.zeros(N, device="cuda")
     out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi == 3 else torch.float16)
-    calls.append((name, lambda A=A, W=W, bias=bias, out=out, M=M, N=N, K=K, epi=epi: _native.check(
-        lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N, K, epi, None, None,
-                      0, 0, 0, st))))
+    rc, rs = (cos.data_ptr(), sin.data_ptr()) if epi == 4 else (None, None)
+    calls.append((name, lambda A=A, W=W, bias=bias, out=out, M=M, N=N, K=K, epi=epi, rc=rc, rs=rs: _native.check(
+        lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N, K, epi, rc, rs,
+                      5184, 80, 2560 if epi == 4 else 0, st))))
 for name, (B, H, L, hd) in {"att16": (4, 16, 5184, 16), "att80": (1, 16, 5184, 80),
                             "att80w": (9, 16, 576, 80)}.items():
     if name not in which:

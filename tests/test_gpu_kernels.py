@@ -79,7 +79,7 @@ def test_gemm_epilogues(lib, epi):
         assert rel_err(out, ref) < 1e-5 and rel_err(out2, ref) < 2e-3
 
 
-PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (128, 2), (64, 2)]
+PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (192, 2), (160, 2), (128, 2), (64, 2)]
 
 
 @pytest.mark.parametrize("bn,cg", PLANS)
@@ -87,10 +87,8 @@ PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (128, 2), (64, 2)]
 def test_gemm_forced_plans(lib, bn, cg, epi):
     """Every tile plan (1-SM 128 x bn and CTA-pair 256 x bn tiles) and epilogue, with M and N tails
     that leave partial 256-row tiles and several waves."""
-    if epi == 3 and bn > 128:
-        pytest.skip("the residual epilogue stages 128 x bn fp32 in smem: bn <= 128")
     T, E = 576, 1280
-    M, N, K = (1700, 3840, 1280) if epi == 4 else (1333, 1536, 320)
+    M, N, K = (1700, 3840, 1280) if epi == 4 else (5000, 6 * bn, 320)
     g = torch.Generator(device="cuda").manual_seed(bn * 10 + cg + epi)
     A = torch.randn(M, K, device="cuda", generator=g).half()
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
