@@ -194,6 +194,73 @@ class Detector:
             cur.wait_stream(p["s_bb"])
             cur.wait_stream(p["s_dec"])
 
+    # ------------------------------------------------------------------ CUDA graphs
+    def _graph_pipeline(self, B: int):
+        """Two captured CUDA graphs G_0 / G_1 of one pipelined step each: G_k runs the backbone of
+        the batch in input buffer k into slot k (stream 0) concurrently with the enc-dec +
+        post-processing of slot 1-k (stream 1, the previous batch), joined at the end.  Replaying
+        G_0, G_1, G_0, ... is the two-stream inter-frame pipeline with every launch of a step in
+        one graph (no per-kernel launch gaps)."""
+        import torch
+
+        gp = getattr(self, "_gpipe", None)
+        if gp is not None and gp["B"] == B:
+            return gp
+        p = self._pipeline(B)
+        S = self.model.config.image_size
+        inb = [torch.zeros((B, S, S, 3), device=self.device, dtype=torch.float32) for _ in range(2)]
+        slots, h_dec = p["slots"], p["h_dec"]
+        s_bb, s_dec = p["s_bb"], p["s_dec"]
+
+        def step(k):
+            cur = torch.cuda.current_stream(self.device)
+            s_bb.wait_stream(cur)
+            s_dec.wait_stream(cur)
+            self._enqueue_backbone(self.handle, inb[k], slots[k], s_bb.cuda_stream)
+            self._enqueue_decode(h_dec, slots[1 - k], B, s_dec.cuda_stream, slots[1 - k]["l0"].data_ptr())
+            cur.wait_stream(s_bb)
+            cur.wait_stream(s_dec)
+
+        side = torch.cuda.Stream(device=self.device)
+        with torch.cuda.stream(side):  # eager warm-up: workspaces and kernel attributes exist before capture
+            for k in (0, 1, 0, 1):
+                step(k)
+        torch.cuda.synchronize(self.device)
+        graphs = []
+        for k in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                step(k)
+            graphs.append(g)
+        gp = {"B": B, "inb": inb, "graphs": graphs, "t": 0, "slots": slots}
+        self._gpipe = gp
+        return gp
+
+    def detect_device_graph(self, images):
+        """One pipelined step through the captured graphs: the batch (device [B, S, S, 3]) is
+        copied into input buffer k and G_k replayed on the current stream.  Returns the slot
+        buffers of the PREVIOUS batch (decoded in this step); the first call returns the
+        warm-up slot.  No host sync."""
+        B = int(images.shape[0])
+        gp = self._graph_pipeline(B)
+        k = gp["t"] & 1
+        gp["t"] += 1
+        gp["inb"][k].copy_(images)
+        gp["graphs"][k].replay()
+        return gp["slots"][1 - k]
+
+    def graph_drain(self):
+        """Decode the last batch fed to detect_device_graph (eager, current stream); returns its
+        slot buffers."""
+        import torch
+
+        gp = self._gpipe
+        k = (gp["t"] - 1) & 1
+        p = self._pipeline(gp["B"])
+        self._enqueue_decode(p["h_dec"], gp["slots"][k], gp["B"], torch.cuda.current_stream(self.device).cuda_stream,
+                             gp["slots"][k]["l0"].data_ptr())
+        return gp["slots"][k]
+
     def detect_stream(self, batches):
         """Generator over host (NumPy / CPU torch) or device image batches [B, S, S, 3]: yields
         one list of per-image detection lists per batch, in order, with the backbone of batch

@@ -53,3 +53,27 @@ def test_forked_handle_same_outputs():
     for it, n in enumerate(ref["kc"].tolist()):  # kept lists (entries past the count are scratch)
         assert torch.equal(got["kq"][it, :n], ref["kq"][it, :n])
         assert torch.equal(got["ks"][it, :n], ref["ks"][it, :n])
+
+
+def test_graph_pipeline_matches_detect():
+    """CUDA-graph replay of the pipelined step: image t's detections (returned one step later)
+    equal the eager one-stream path."""
+    model, names, cfg, imgs = _setup(4)
+    det = Detector(model, names, cfg)
+    serial = []
+    for im in imgs:
+        b = det.detect_device(torch.from_numpy(im[None]).cuda())
+        serial.append({k: v.clone() for k, v in det.result_tensors(b).items()})
+    got = []
+    for i, im in enumerate(imgs):
+        b = det.detect_device_graph(torch.from_numpy(im[None]).cuda())
+        if i > 0:
+            got.append({k: v.clone() for k, v in det.result_tensors(b).items()})
+    b = det.graph_drain()
+    got.append({k: v.clone() for k, v in det.result_tensors(b).items()})
+    torch.cuda.synchronize()
+    for ref, g in zip(serial, got):
+        for k in ("flags", "kc", "pp", "boxes"):
+            assert torch.equal(g[k], ref[k]), k
+        for it, n in enumerate(ref["kc"].tolist()):
+            assert torch.equal(g["kq"][it, :n], ref["kq"][it, :n])
