@@ -215,9 +215,13 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       if (lane == 0 && a.softmax_only != 1) {
         constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
         constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, L::ON) | (1u << 16);  // B (V) MN-major
-        auto issue_s = [&](int gg, uint32_t sq) {
+        // the K-ready wait of S(gg) can be hoisted off the P-ready -> P.V -> S critical path
+        auto wait_k = [&](int gg) {
+          wait_sel<SPIN & 1>(&k_full[gg % STAGES], (gg / STAGES) & 1, 3000000 + gg, a.dbg);
+        };
+        auto issue_s = [&](int gg, uint32_t sq, bool k_waited) {
           const int st = gg % STAGES;
-          wait_sel<SPIN & 1>(&k_full[st], (gg / STAGES) & 1, 3000000 + gg, a.dbg);
+          if (!k_waited) wait_k(gg);
           if (a.trace && blockIdx.x == 0 && gg >= 2 && gg - 2 < 256) a.trace[1536 + gg - 2] = clock64();
           tc_fence_after();
           const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
@@ -235,13 +239,22 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
           mbar_wait_dbg(&q_full[qb], (m_it >> 1) & 1, 4000000 + m_it, a.dbg);
           tc_fence_after();
-          for (int j = 0; j < NS && j < nkv; ++j) issue_s(m_g + j, sq);
+          for (int j = 0; j < NS && j < nkv; ++j) issue_s(m_g + j, sq, false);
           for (int j = 0; j < nkv; ++j, ++m_g) {
             const int sb = m_g % NS, st = m_g % STAGES;
-            wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
-            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = clock64();
-            wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
-            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1024 + m_g] = clock64();
+            if constexpr (LEAN) {
+              // V(g) and K(g+NS) have normally landed long before P(g): wait for them first,
+              // so that once P(g) is ready nothing but MMA issue separates it from S(g+NS)
+              wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
+              if (j + NS < nkv) wait_k(m_g + NS);
+              wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
+              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = a.trace[1024 + m_g] = clock64();
+            } else {
+              wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
+              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = clock64();
+              wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
+              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1024 + m_g] = clock64();
+            }
             tc_fence_after();
             const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
 #pragma unroll
@@ -256,7 +269,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
               umma_commit(&v_empty[st]);
               umma_commit(&o_done[sb]);
             }
-            if (j + NS < nkv) issue_s(m_g + NS, sq);
+            if (j + NS < nkv) issue_s(m_g + NS, sq, LEAN);
             if (!LEAN && j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
             if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[768 + m_g] = clock64();
           }
