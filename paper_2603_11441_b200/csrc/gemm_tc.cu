@@ -37,12 +37,15 @@ struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x 2 staging buffers of 4 KB (32x32 fp32)
-  static constexpr int ROPE_OFF = EPI_OFF + 16 * 4096;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
+  static constexpr bool RESID = EPI == EPI_F32_RESID;
+  // staging buffers per epilogue warp; 4 for the residual epilogue (3 chunks prefetched) measured
+  // slower: the extra 64 KB costs two operand stages (out-proj 24.8 -> 27.1 us, fc2 63.4 -> 80 us)
+  static constexpr int NBUF = 2;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x NBUF staging buffers of 4 KB (32x32 fp32)
+  static constexpr int ROPE_OFF = EPI_OFF + 8 * NBUF * 4096;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
   static constexpr int ROPE_BYTES = EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0;
   static constexpr int BAR_OFF = ROPE_OFF + ROPE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1 KB alignment slack
-  static constexpr bool RESID = EPI == EPI_F32_RESID;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + 1 KB alignment slack
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static_assert(TOTAL <= 227 * 1024, "shared memory budget");
 };
@@ -239,8 +242,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rfull = tempty + 2;  // [8 warps][2 buffers]: residual chunk landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 16);
+  uint64_t* rfull = tempty + 2;  // [8 warps][NBUF buffers]: residual chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 8 * L::NBUF);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8 * CG);
     }
-    for (int i = 0; i < 16; ++i) mbar_init(&rfull[i], 1);
+    for (int i = 0; i < 8 * L::NBUF; ++i) mbar_init(&rfull[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_cg<L::TMEM_COLS, CG>(tmem_slot);
@@ -351,20 +354,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       named_bar_sync(1, GEMM_THREADS - 128);
     }
     const int quarter = warp & 3, half = (warp - 4) >> 2;
-    float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * 2048;  // 2 x 4 KB per warp
-    uint64_t* rbar = rfull + (warp - 4) * 2;
+    constexpr int NBUF = L::NBUF;
+    float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * NBUF * 1024;  // NBUF x 4 KB per warp
+    uint64_t* rbar = rfull + (warp - 4) * NBUF;
     const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
-    // residual chunk g of this warp -> smem buffer g & 1 (lane 0 issues; one chunk ahead)
+    // residual chunk g of this warp -> smem buffer g % NBUF (lane 0 issues; NBUF-1 chunks ahead)
     const int cpw = (BN - half * 32 + 63) / 64;  // 32-column chunks of this warp per tile
     auto resid_load = [&](int g) {
       const int t = cl + (g / cpw) * ncl;
       if (t >= num_tiles) return;
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
       const int cc = (t % num_n) * BN + ((g % cpw) * 2 + half) * 32;
-      mbar_arrive_expect_tx(&rbar[g & 1], 32 * 32 * 4);
-      tma_load_2d(bufs + (g & 1) * 1024, &tmC, &rbar[g & 1], cc, rr);
+      mbar_arrive_expect_tx(&rbar[g % NBUF], 32 * 32 * 4);
+      tma_load_2d(bufs + (g % NBUF) * 1024, &tmC, &rbar[g % NBUF], cc, rr);
     };
-    if (RESID && lane == 0) resid_load(0);
+    if (RESID && lane == 0)
+      for (int i = 0; i < NBUF - 1; ++i) resid_load(i);
     int it = 0, g = 0;
     for (int tile = cl; tile < num_tiles; tile += ncl, ++it) {
       const int acc = it & 1;
@@ -386,11 +391,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
 #pragma unroll 1
       for (int c = half * 32; c < BN; c += 64, ++g) {
-        float* buf = bufs + (g & 1) * 1024;
+        float* buf = bufs + (g % NBUF) * 1024;
         if (lane == 0) {
           if (RESID) {
-            bulk_wait_read0();  // store g-1 has read buffer (g+1)&1
-            resid_load(g + 1);
+            bulk_wait_read0();  // store g-1 has read buffer (g-1) % NBUF = (g+NBUF-1) % NBUF
+            resid_load(g + NBUF - 1);
           } else {
             bulk_wait_read1();  // store g-2 has read this buffer
           }
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           continue;
         }
         if constexpr (RESID) {
-          mbar_wait(&rbar[g & 1], (g >> 1) & 1);
+          mbar_wait(&rbar[g % NBUF], (g / NBUF) & 1);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float4* sp = slot32(buf, lane, q);
@@ -507,7 +512,8 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
 template <int BN, int EPI, int CG>
 constexpr int stages_for() {
   constexpr int stage = BM * BK * 2 + (BN / CG) * BK * 2;
-  constexpr int fixed = 16 * 4096 + (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) + 256 + 1024;
+  constexpr int fixed = 8 * 2 * 4096 +
+                        (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) + 512 + 1024;
   constexpr int n = (227 * 1024 - fixed) / stage;
   return n > 8 ? 8 : n;
 }
