@@ -114,7 +114,8 @@ int dart_mask_head(dart_model* m, const float* query_features, int32_t B, int32_
  * dart_gemm_plan: the tile plan dart_gemm / the model forwards use for (M, N, epi) on this GPU
  *   (bn = tile width, cg = 1: 128-row tiles per SM, 2: 256-row tiles per CTA pair).
  * dart_gemm_force_plan: force (bn, cg) for every later GEMM whose N allows it (tests and A/B
- *   measurement); bn = 0 restores the automatic plan.
+ *   measurement); bn = 0 restores the automatic plan.  With DART_SPLITK=1 in the environment the
+ *   model path runs residual GEMMs with K >= 4096 (backbone fc2) split-K (measured slower; A/B only).
  * dart_attention: o = softmax(q k^T / sqrt(hd)) v, fp16 in/out, tokens `*_tok_stride`
  *   elements apart, heads hd apart, batch items `*_batch_stride` apart; win > 0 selects the
  *   windowed token map over a grid x grid token image (batch = images * (grid/win)^2). */
@@ -123,6 +124,9 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
               int32_t rope_cols, void* stream);
 void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
 void dart_gemm_force_plan(int32_t bn, int32_t cg);
+/* Tests: s = 2 makes later dart_gemm residual calls (epi 3, K/64 even) run split-K (two K halves
+ * per tile on different CTA pairs, deterministic adds); s = 1 restores the default. */
+void dart_gemm_force_splitk(int32_t s);
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
                    int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,
                    int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,

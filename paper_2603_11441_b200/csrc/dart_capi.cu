@@ -100,6 +100,10 @@ bool tc_attention_enabled() {
 
 // Tests: route every tcgen05 attention item through the max-tracking (overflow-safe) pass too.
 int g_attn_force_safe = 0;
+// split-K for long-K residual GEMMs: measured slower on B200 (fc2 64.5 -> 68.4 us: the half-1
+// epilogue waits behind half 0's), so opt-in (DART_SPLITK=1) for A/B measurement only
+int g_splitk_enabled = getenv("DART_SPLITK") != nullptr;
+int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 long long* g_attn_trace = nullptr;
 
 // tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
@@ -248,8 +252,11 @@ struct dart_model {
     __half *l0h, *h, *q, *kv, *o, *hid, *dkv, *text, *tkv, *dh, *dq, *dkvs, *do_, *dhid;
   } ed{};
   int64_t launches = 0;
+  int* splitk_flags = nullptr;  // per handle (a fork gets its own): split-K tile flags
+  int splitk_cap = 0;
 
   ~dart_model() {
+    if (splitk_flags) cudaFree(splitk_flags);
     bb_ws.release();
     ed_ws.release();
     mask_ws.release();
@@ -382,6 +389,23 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
   CUtensorMap tc, td;
   if (!make_out_maps(epi, e, M, W.N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
   const GemmPlan plan = gemm_plan(M, W.N, epi, m->num_sms);
+  // long-K residual GEMMs (backbone fc2, K = 4E), opt-in: two K halves per tile on different CTA
+  // pairs (deterministic half-0-then-half-1 residual adds) to halve the wave-quantisation tail
+  if (epi == EPI_F32_RESID && W.K >= 4096 && (W.K / 64) % 2 == 0 && g_splitk_enabled) {
+    const int tiles = ((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (W.N / plan.bn);
+    if (!m->splitk_flags || tiles > m->splitk_cap) {
+      if (m->splitk_flags) cudaFree(m->splitk_flags);
+      m->splitk_cap = tiles < 4096 ? 4096 : tiles;
+      if (cudaMalloc(&m->splitk_flags, m->splitk_cap * sizeof(int)) != cudaSuccess) {
+        m->splitk_flags = nullptr;
+        return fail(DART_ERR_CUDA, "split-K flag allocation failed");
+      }
+    }
+    if (cudaMemsetAsync(m->splitk_flags, 0, tiles * sizeof(int), s) != cudaSuccess)
+      return fail(DART_ERR_CUDA, "split-K flag reset failed");
+    e.splitk = 2;
+    e.tile_flags = m->splitk_flags;
+  }
   int rc = gemm_tc(ta, W.tmap[box_slot(plan.bn / plan.cg)], &tc, &td, M, W.N, W.K, plan, epi, e, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
@@ -692,6 +716,8 @@ int dart_model_fork(const dart_model* parent, dart_model** out) {
   f->bb = {};
   f->ed = {};
   f->launches = 0;
+  f->splitk_flags = nullptr;
+  f->splitk_cap = 0;
   *out = f;
   return DART_OK;
 }
@@ -921,6 +947,15 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.dbg_noload = getenv("DART_GEMM_NOLOAD") != nullptr;
   CUtensorMap td;
   if (!make_out_maps(epi, e, M, N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
+  if (g_gemm_splitk == 2 && epi == EPI_F32_RESID && (K / 64) % 2 == 0) {  // tests: split-K residual path
+    static int* flags = nullptr;
+    if (!flags && cudaMalloc(&flags, 65536 * sizeof(int)) != cudaSuccess) return fail(DART_ERR_CUDA, "flags");
+    const int tiles = ((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (N / plan.bn);
+    if (tiles > 65536) return fail(DART_ERR_INVALID, "dart_gemm: too many split-K tiles");
+    cudaMemsetAsync(flags, 0, tiles * sizeof(int), (cudaStream_t)stream);
+    e.splitk = 2;
+    e.tile_flags = flags;
+  }
   int rc = gemm_tc(ta, tb, &tc, &td, M, N, K, plan, epi, e, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
@@ -936,6 +971,7 @@ void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg)
 }
 
 void dart_gemm_force_plan(int32_t bn, int32_t cg) { gemm_force_plan(bn, cg); }
+void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
                    int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,

@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
-  const int nk = K / BK;
+  const int SK = RESID ? epi.splitk : 1;  // K slices per tile (work unit = tile x slice)
+  const int num_units = num_tiles * SK;
+  const int nk = K / BK / SK;             // k-blocks per unit
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -281,14 +283,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cl; tile < num_tiles; tile += ncl) {
+      for (int unit = cl; unit < num_units; unit += ncl) {
+        const int tile = unit / SK, kb0 = (unit % SK) * nk;
         const int m0 = (tile / num_n) * BM * CG + rank * BM;
         const int n0 = (tile % num_n) * BN + rank * L::B_ROWS;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb0 + nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
-          if (epi.dbg_noload && (tile != cl || kb >= STAGES)) {
+          if (epi.dbg_noload && (unit != cl || kb >= STAGES)) {
             if (rank == 0) mbar_arrive(&full[stage]);
           } else if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cl; tile < num_tiles; tile += ncl, ++it) {
+      for (int unit = cl; unit < num_units; unit += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -361,8 +364,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // residual chunk g of this warp -> smem buffer g % NBUF (lane 0 issues; NBUF-1 chunks ahead)
     const int cpw = (BN - half * 32 + 63) / 64;  // 32-column chunks of this warp per tile
     auto resid_load = [&](int g) {
-      const int t = cl + (g / cpw) * ncl;
-      if (t >= num_tiles) return;
+      const int u = cl + (g / cpw) * ncl;
+      if (u >= num_units) return;
+      const int t = u / SK;
+      if (SK > 1 && u % SK == 1 && g % cpw == 0) {  // half 1 reads what half 0 of this tile stored
+        volatile int* f = epi.tile_flags + t;
+        while (*f < 8 * CG) __nanosleep(64);
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
       const int cc = (t % num_n) * BN + ((g % cpw) * 2 + half) * 32;
       mbar_arrive_expect_tx(&rbar[g % NBUF], 32 * 32 * 4);
@@ -371,7 +381,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (RESID && lane == 0)
       for (int i = 0; i < NBUF - 1; ++i) resid_load(i);
     int it = 0, g = 0;
-    for (int tile = cl; tile < num_tiles; tile += ncl, ++it) {
+    for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+      const int tile = unit / SK, kh = unit % SK;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (tile / num_n) * BM * CG + rank * BM;
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
-        epilogue_bias_act<EPI>(v, n0 + c, epi);
+        if (kh == 0) epilogue_bias_act<EPI>(v, n0 + c, epi);  // split-K: bias once (half 0)
         if (EPI == EPI_QKV_ROPE && n0 + c < epi.rope_cols) rope_chunk(v, n0 + c, epi.rope_hd, rt, ct);
         if ((EPI == EPI_F32 && epi.wm_scatter) || EPI == EPI_F32_F16) {  // row scatter / 2 outputs: plain stores
           chunk_store_f32(buf, v, reinterpret_cast<float*>(epi.out), epi.ldo, row0, n0 + c, M, epi);
@@ -461,6 +472,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tma_store_commit();
         }
       }
+      if (SK > 1 && kh == 0) {  // half 0 of a split-K tile: publish once this warp's stores landed
+        if (lane == 0) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(epi.tile_flags + tile, 1);
+        }
+        __syncwarp();
+      }
     }
     if (lane == 0) bulk_wait_all();  // output writes landed before the CTA retires
   }
@@ -484,7 +504,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID ? epi.splitk : 1);
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   if constexpr (CG == 1) {
@@ -590,6 +610,8 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC,
   if (M <= 0) return 0;
   const int BN = plan.bn;
   if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
+  if (epi.splitk != 1 && (epi_mode != EPI_F32_RESID || epi.splitk != 2 || (K / BK) % 2 != 0 || !epi.tile_flags))
+    return (int)cudaErrorInvalidValue;
   if (epi_mode == EPI_QKV_ROPE && (epi.rope_grid <= 0 || epi.rope_grid > ROPE_MAX_GRID ||
                                    epi.rope_grid * epi.rope_grid != epi.rope_T || epi.rope_hd % 4 != 0 ||
                                    epi.rope_hd / 4 > ROPE_MAX_Q))

@@ -35,6 +35,12 @@ struct GemmEpi {
   int wm_win = 0;
   int wm_scatter = 0;
   int dbg_noload = 0;  // microbenchmarks only: after the first ring fill, stages are re-used without TMA
+  // Split-K residual GEMM (EPI_F32_RESID only): splitk = 2 runs each output tile as two K halves
+  // on different CTA pairs; half 0 does out += bias + acc0, half 1 waits for half 0's tile flag
+  // (tile_flags[tile] == 16: all epilogue warps of the pair have stored) and does out += acc1.
+  // Deterministic order, no workspace; tile_flags must be zeroed before the launch.
+  int splitk = 1;
+  int* tile_flags = nullptr;
 };
 
 // window-major row index <-> token index within one image
@@ -100,8 +106,8 @@ struct AttnTcArgs {
   long long* trace = nullptr;  // microbenchmark: CTA 0 clock64 stamps [7][256] of the first 256 tiles
 };
 constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
-int attention_tc_kv_tile(int head_dim);
-void attention_tc_set_variant(int v);  // microbenchmarks (DART_FA_VARIANT otherwise)  // 192 (hd 80), 96 (hd 16), 0 = unsupported
+int attention_tc_kv_tile(int head_dim);  // key tile of the selected variant (64 hd 80, 96 hd 16), 0 = unsupported
+void attention_tc_set_variant(int v);  // microbenchmarks (DART_FA_VARIANT otherwise)
 bool attention_tc_supported(int head_dim, int Lkv);
 // tmQ: 2-D map over the Q buffer [items*Lq, cols] fp16, box {16, 128}, 32B swizzle;
 // tmKV: map over the K/V buffer [items*Lkv, cols], box {16, kv_tile}.

@@ -15,6 +15,8 @@ st = torch.cuda.current_stream()
 plan = os.environ.get("DART_GEMM_PLAN")
 if plan:
     lib.dart_gemm_force_plan(*[int(x) for x in plan.split(",")])
+if os.environ.get("DART_GEMM_SPLITK"):
+    lib.dart_gemm_force_splitk(int(os.environ["DART_GEMM_SPLITK"]))
 
 
 def bench(fn, reps=30):

@@ -82,6 +82,34 @@ def test_gemm_epilogues(lib, epi):
 PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (192, 2), (160, 2), (128, 2), (64, 2)]
 
 
+@pytest.mark.parametrize("bn,cg", [(256, 2), (128, 2), (256, 1), (64, 1)])
+@pytest.mark.parametrize("M,N,K", [(5184, 1280, 5120), (1333, 768, 640), (300, 256, 128)])
+def test_gemm_split_k_residual(lib, bn, cg, M, N, K):
+    """Split-K residual epilogue: out += bias + A W^T as two K halves (half 0 adds bias + acc0,
+    half 1 waits for half 0's tile flag and adds acc1); equal to fp32 torch and deterministic."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(N, device="cuda", generator=g)
+    x0 = torch.randn(M, N, device="cuda", generator=g)
+    ref = x0 + A.float() @ W.float().T + bias
+    outs = []
+    lib.dart_gemm_force_plan(bn, cg)
+    lib.dart_gemm_force_splitk(2)
+    try:
+        for _ in range(2):
+            out = x0.clone()
+            _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N, K,
+                                        3, None, None, 0, 0, 0, stream()))
+            outs.append(out)
+        torch.cuda.synchronize()
+    finally:
+        lib.dart_gemm_force_splitk(1)
+        lib.dart_gemm_force_plan(0, 0)
+    assert rel_err(outs[0], ref) < 2e-3
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("bn,cg", PLANS)
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 5])
 def test_gemm_forced_plans(lib, bn, cg, epi):
