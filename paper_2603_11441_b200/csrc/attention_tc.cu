@@ -441,387 +441,6 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// fa_dec_kernel: S decoupled from P.  TMEM = 2 S buffers | one P buffer (fp16, BKV/2 columns) |
-// O (HD columns, no ones block: the softmax keeps the row sums in registers).  A softmax warp
-// releases S(g) (s_free) as soon as it has loaded it, so the MMA issuer puts S(g+2) on the
-// tensor pipe while P(g) is still being computed; P.V(g) follows P-ready.  The P buffer is
-// rewritten only after P.V(g-1) completed (pv_done), which the softmax observes long before it
-// has P(g) ready.  This removes the P.V -> S chain that gated every tile of fa_tc_kernel.
-// hd 16: 2x96 + 48 + 16 = 256 TMEM columns, hd 80: 2x64 + 32 + 80 = 240: two CTAs per SM.
-template <int HD, int BKV, int STAGES>
-struct DecCfg {
-  static constexpr int NS = 2;
-  static constexpr int NB = HD / 16;
-  static constexpr int PCOL = NS * BKV;
-  static constexpr int OCOL = PCOL + BKV / 2;
-  static constexpr int TMEM_NEED = OCOL + HD;
-  static constexpr int TMEM = TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
-  static_assert(TMEM * 2 <= 512, "two CTAs per SM");
-  static constexpr int THREADS = 192;
-  static constexpr int Q_BLOCK = BQ * 32;
-  static constexpr int KV_BLOCK = BKV * 32;
-  static constexpr int Q_BYTES = NB * Q_BLOCK;
-  static constexpr int K_BYTES = NB * KV_BLOCK;
-  static constexpr int OFF_K = 2 * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
-  static constexpr int OFF_BAR = OFF_V + STAGES * K_BYTES;
-  static constexpr int NBARS = 4 + 4 * STAGES + 2 * NS + 3;
-  static constexpr int OFF_OVF = OFF_BAR + NBARS * 8 + 16;
-  static constexpr int OVF_WORDS = ATTN_TC_MAX_LOCAL_ITEMS / 32;
-  static constexpr int TOTAL = OFF_OVF + OVF_WORDS * 4 + 1024;
-  static_assert(TOTAL * 2 <= 227 * 1024, "shared memory budget");
-};
-
-template <int HD, int BKV, int STAGES, int NPOLY>
-__global__ void __launch_bounds__(192, 2)
-    fa_dec_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
-  using L = DecCfg<HD, BKV, STAGES>;
-  constexpr int NS = L::NS;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* q_full = bars;                 // 2
-  uint64_t* q_empty = bars + 2;            // 2
-  uint64_t* k_full = bars + 4;             // STAGES
-  uint64_t* k_empty = k_full + STAGES;     // STAGES
-  uint64_t* v_full = k_empty + STAGES;     // STAGES
-  uint64_t* v_empty = v_full + STAGES;     // STAGES
-  uint64_t* s_full = v_empty + STAGES;     // NS
-  uint64_t* s_free = s_full + NS;          // NS
-  uint64_t* p_full = s_free + NS;          // 1
-  uint64_t* pv_done = p_full + 1;          // 1
-  uint64_t* item_done = pv_done + 1;       // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_done + 1);
-  uint32_t* ovf = reinterpret_cast<uint32_t*>(smem + L::OFF_OVF);
-
-  const int warp = warp_id(), lane = lane_id();
-  const int q_tiles = (a.Lq + BQ - 1) / BQ;
-  const int n_items = q_tiles * a.heads * a.items;
-  const int nkv = a.Lkv / BKV;
-  const int n_local = (int)blockIdx.x < n_items ? (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-
-  if (warp == 1 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmKV);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
-    }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 4);
-    }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
-    mbar_init(item_done, 1);
-    fence_barrier_init();
-  }
-  for (int i = threadIdx.x; i < L::OVF_WORDS; i += blockDim.x) ovf[i] = 0u;
-  if (warp == 0) tmem_alloc<L::TMEM>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  int p_it = 0, p_g = 0, pv_g = 0;  // producer (Q/K thread, V thread)
-  int m_gs = 0, m_gp = 0, m_qs = 0;  // MMA issuer: S tiles, P.V tiles, items whose S started
-  int s_g = 0, s_it = 0;             // softmax
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) {
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
-      uint32_t any = a.force_safe;
-      for (int i = 0; i < L::OVF_WORDS; ++i) any |= ovf[i];
-      if (!any) break;
-    }
-    auto todo = [&](int local) {
-      return pass == 0 || a.force_safe || ((ovf[local >> 5] >> (local & 31)) & 1u);
-    };
-    auto next_todo = [&](int local) {
-      while (local < n_local && !todo(local)) ++local;
-      return local;
-    };
-    if (warp == 0) {
-      if (lane < 2) {
-        const bool do_qk = lane == 0;
-        for (int local = next_todo(0); local < n_local; local = next_todo(local + 1)) {
-          const int item = blockIdx.x + local * gridDim.x;
-          const int qt = item % q_tiles;
-          const int h = (item / q_tiles) % a.heads;
-          const int z = item / (q_tiles * a.heads) + a.z_base;
-          const int row0 = z * a.Lkv;
-          if (do_qk) {
-            const int qb = p_it & 1;
-            mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, a.dbg);
-            mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
-            for (int b = 0; b < L::NB; ++b)
-              tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
-                          z * a.Lq + qt * BQ);
-            ++p_it;
-          }
-          for (int j = 0; j < nkv; ++j) {
-            if (do_qk) {
-              const int st = p_g % STAGES;
-              mbar_wait_dbg(&k_empty[st], ((p_g / STAGES) & 1) ^ 1, 2000000 + p_g, a.dbg);
-              mbar_arrive_expect_tx(&k_full[st], L::K_BYTES);
-              for (int b = 0; b < L::NB; ++b)
-                tma_load_2d(smem + L::OFF_K + st * L::K_BYTES + b * L::KV_BLOCK, &tmKV, &k_full[st],
-                            a.k_col + h * HD + b * 16, row0 + j * BKV);
-              ++p_g;
-            } else {
-              const int st = pv_g % STAGES;
-              mbar_wait_dbg(&v_empty[st], ((pv_g / STAGES) & 1) ^ 1, 2500000 + pv_g, a.dbg);
-              mbar_arrive_expect_tx(&v_full[st], L::K_BYTES);
-              for (int b = 0; b < L::NB; ++b)
-                tma_load_2d(smem + L::OFF_V + st * L::K_BYTES + b * L::KV_BLOCK, &tmKV, &v_full[st],
-                            a.v_col + h * HD + b * 16, row0 + j * BKV);
-              ++pv_g;
-            }
-          }
-        }
-      }
-      __syncwarp();
-    } else if (warp == 1) {
-      if (lane == 0) {
-        constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
-        constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, HD) | (1u << 16);  // B (V) MN-major
-        int s_loc = next_todo(0), s_j = 0;
-        auto issue_s = [&]() {  // S for tile m_gs = (s_loc, s_j)
-          const int qb = m_qs & 1, sb = m_gs % NS, st = m_gs % STAGES;
-          if (s_j == 0) mbar_wait_dbg(&q_full[qb], (m_qs >> 1) & 1, 4000000 + m_qs, a.dbg);
-          if (m_gs >= NS) mbar_wait_dbg(&s_free[sb], ((m_gs / NS) - 1) & 1, 3500000 + m_gs, a.dbg);
-          mbar_wait_dbg(&k_full[st], (m_gs / STAGES) & 1, 3000000 + m_gs, a.dbg);
-          tc_fence_after();
-          const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
-          const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
-#pragma unroll
-          for (int b = 0; b < L::NB; ++b)
-            umma_f16(tmem + sb * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
-                     desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
-          umma_commit(&s_full[sb]);
-          if (a.trace && blockIdx.x == 0 && m_gs >= 2 && m_gs - 2 < 256) a.trace[1536 + m_gs - 2] = clock64();
-          ++m_gs;
-          if (++s_j == nkv) {
-            s_j = 0;
-            ++m_qs;
-            s_loc = next_todo(s_loc + 1);
-          }
-        };
-        while (s_loc < n_local && m_gs < m_gp + NS) issue_s();
-        for (int local = next_todo(0); local < n_local; local = next_todo(local + 1)) {
-          for (int j = 0; j < nkv; ++j, ++m_gp) {
-            if (s_loc < n_local) issue_s();  // S(g + NS): needs only S(g) loaded by the softmax
-            const int st = m_gp % STAGES;
-            mbar_wait_dbg(&v_full[st], (m_gp / STAGES) & 1, 6000000 + m_gp, a.dbg);
-            if (a.trace && blockIdx.x == 0 && m_gp < 256) a.trace[1024 + m_gp] = clock64();
-            mbar_wait_dbg(p_full, m_gp & 1, 5000000 + m_gp, a.dbg);
-            if (a.trace && blockIdx.x == 0 && m_gp < 256) a.trace[512 + m_gp] = clock64();
-            tc_fence_after();
-            const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::K_BYTES);
-#pragma unroll
-            for (int kc = 0; kc < BKV / 16; ++kc)
-              umma_f16_ts(tmem + L::OCOL, tmem + L::PCOL + kc * 8, desc_sw32(sv + kc * 512, L::KV_BLOCK, 256), idesc_pv,
-                          (j | kc) != 0);
-            umma_commit(pv_done);
-            if (j == nkv - 1) umma_commit(item_done);
-            if (a.trace && blockIdx.x == 0 && m_gp < 256) a.trace[768 + m_gp] = a.trace[1280 + m_gp] = clock64();
-          }
-        }
-      }
-      __syncwarp();
-    } else {
-      const int quarter = warp & 3;
-      const int r = quarter * 32 + lane;
-      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-      const float c = a.scale_log2;
-      for (int local = next_todo(0); local < n_local; local = next_todo(local + 1)) {
-        const int item = blockIdx.x + local * gridDim.x;
-        const int qt = item % q_tiles;
-        const int h = (item / q_tiles) % a.heads;
-        const int z = item / (q_tiles * a.heads) + a.z_base;
-        float m_ref = -INFINITY, nb = 0.f, cr = 0.f, br = 0.f;
-        uint64_t l2 = f2_pack(0.f, 0.f);  // row sum, two partial lanes
-        for (int j = 0; j < nkv; ++j, ++s_g) {
-          const int sb = s_g % NS;
-          mbar_wait_dbg(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, a.dbg);
-          tc_fence_after();
-          if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[s_g] = clock64();
-          if (warp == 2 && lane == 0) {
-            mbar_arrive(&k_empty[s_g % STAGES]);                // S(g) consumed K(g)
-            if (j == nkv - 1) mbar_arrive(&q_empty[s_it & 1]);  // last S of the item read Q
-          }
-          float v[BKV];
-          tmem_ld_cols<BKV>(lane_base + sb * BKV, v);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_free[sb]);
-          uint32_t p[BKV / 2];
-          float f_rescale = 1.f;
-          bool rescale = false;
-          if (pass == 0) {
-            if (j == 0) {
-              float pm[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k) pm[k] = v[k];
-#pragma unroll
-              for (int i = 8; i < BKV; i += 16)
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  pm[k] = i + 8 + k < BKV ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
-              m_ref = fmaxf(fmax3f(pm[0], pm[1], pm[2]), fmax3f(fmax3f(pm[3], pm[4], pm[5]), pm[6], pm[7]));
-              nb = -m_ref * c;
-              cr = c * (1.0f / EXP_R);
-              br = (nb - EXP_XMIN) * (1.0f / EXP_R);
-            }
-            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
-#pragma unroll
-            for (int i = 0; i < BKV / 2; ++i) {
-              float x0, x1;
-              if ((i & 7) < NPOLY / 2) {
-                exp2_poly2_sat(v[2 * i], v[2 * i + 1], cr, br, x0, x1);
-              } else {
-                f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
-                x0 = fast_exp2(x0);
-                x1 = fast_exp2(x1);
-              }
-              l2 = fadd2(l2, f2_pack(x0, x1));
-              p[i] = pack_half2(x0, x1);
-            }
-          } else {
-            float pm[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) pm[k] = v[k];
-#pragma unroll
-            for (int i = 8; i < BKV; i += 16)
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                pm[k] = i + 8 + k < BKV ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
-            const float mx = fmaxf(fmax3f(pm[0], pm[1], pm[2]), fmax3f(fmax3f(pm[3], pm[4], pm[5]), pm[6], pm[7]));
-            if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {
-              const float m_new = fmaxf(m_ref, mx);
-              if (j > 0) {
-                rescale = true;
-                f_rescale = fast_exp2((m_ref - m_new) * c);
-              }
-              m_ref = m_new;
-            }
-            nb = -m_ref * c;
-            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
-            uint64_t add = f2_pack(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < BKV / 2; ++i) {
-              float x0, x1;
-              f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
-              x0 = fast_exp2(x0);
-              x1 = fast_exp2(x1);
-              add = fadd2(add, f2_pack(x0, x1));
-              p[i] = pack_half2(x0, x1);
-            }
-            // O and l are rescaled below, once P.V(g-1) has completed
-            l2 = rescale ? ffma2(l2, f2_pack(f_rescale, f_rescale), add) : fadd2(l2, add);
-          }
-          // P buffer free and O complete up to tile g-1 once P.V(g-1) is done
-          if (s_g > 0) {
-            mbar_wait_dbg(pv_done, (s_g - 1) & 1, 8000000 + s_g, a.dbg);
-            tc_fence_after();
-            if (warp == 2 && lane == 0) mbar_arrive(&v_empty[(s_g - 1) % STAGES]);  // V(g-1) consumed
-          }
-          if (rescale) {  // max-tracking pass only (warp-uniform): O *= 2^((m_old - m_new) c)
-#pragma unroll 1
-            for (int ch = 0; ch < HD / 16; ++ch) {
-              float o[16];
-              tmem_ld16(lane_base + L::OCOL + ch * 16, o);
-              tmem_ld_wait();
-              uint32_t u[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * f_rescale);
-              tmem_st16(lane_base + L::OCOL + ch * 16, u);
-            }
-          }
-          tmem_st_cols<BKV / 2>(lane_base + L::PCOL, p);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(p_full);
-          if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[256 + s_g] = clock64();
-        }
-        // epilogue: O / l -> fp16 rows of the output
-        mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, a.dbg);
-        tc_fence_after();
-        ++s_it;
-        float l0, l1;
-        f2_unpack(l2, l0, l1);
-        const float lsum = l0 + l1;
-        const int qrow = qt * BQ + r;
-        __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
-        bool bad = !(fabsf(lsum) < INFINITY);
-        const float inv = 1.f / lsum;
-#pragma unroll 1
-        for (int ch = 0; ch < HD / 8; ++ch) {
-          float o[8];
-          tmem_ld8(lane_base + L::OCOL + ch * 8, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) bad |= !(fabsf(o[i]) < INFINITY);
-          if (qrow < a.Lq) {
-            uint4 w;
-            w.x = pack_half2(o[0] * inv, o[1] * inv);
-            w.y = pack_half2(o[2] * inv, o[3] * inv);
-            w.z = pack_half2(o[4] * inv, o[5] * inv);
-            w.w = pack_half2(o[6] * inv, o[7] * inv);
-            reinterpret_cast<uint4*>(dst + ch * 8)[0] = w;
-          }
-        }
-        if (pass == 0 && __any_sync(0xffffffffu, bad && qrow < a.Lq) && lane == 0)
-          atomicOr(&ovf[local >> 5], 1u << (local & 31));
-        tc_fence_before();  // O reads done before the next item's first P.V (after its P-ready)
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<L::TMEM>(tmem);
-  }
-}
-
-template <int HD, int BKV, int STAGES, int NPOLY>
-int launch_dec(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
-  using Lay = DecCfg<HD, BKV, STAGES>;
-  auto kern = fa_dec_kernel<HD, BKV, STAGES, NPOLY>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
-  const long long per_z = (long long)((a.Lq + BQ - 1) / BQ) * a.heads;
-  const long long max_grid = (long long)num_sms * 2;
-  int zchunk = a.items;
-  while (zchunk > 1 && (per_z * zchunk + max_grid - 1) / max_grid > ATTN_TC_MAX_LOCAL_ITEMS) zchunk = (zchunk + 1) / 2;
-  for (int z0 = 0; z0 < a.items; z0 += zchunk) {
-    AttnTcArgs b = a;
-    b.items = a.items - z0 < zchunk ? a.items - z0 : zchunk;
-    b.z_base = a.z_base + z0;
-    const long long items = per_z * b.items;
-    const int grid = (int)(items < max_grid ? items : max_grid);
-    kern<<<grid, Lay::THREADS, Lay::TOTAL, stream>>>(tmQ, tmKV, b);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return (int)e;
-  }
-  return 0;
-}
-
 // Kernel variants per head dim; variant 0 is the production choice, the others exist for A/B
 // measurement (DART_FA_VARIANT, scripts/bench_attn.py).
 template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN>
@@ -866,13 +485,6 @@ int fa_variant() {
   X(0, 80, 64, 3, 2, 2, 1, 0, 0, 1) \
   X(1, 80, 64, 3, 2, 2, 1, 0, 0, 0) \
   X(2, 80, 64, 3, 2, 2, 1, 4, 0, 1)
-// fa_dec_kernel variants: (variant, HD, BKV, STAGES, NPOLY)
-#define DART_FADEC_VARIANTS(X) \
-  X(20, 80, 64, 3, 0)          \
-  X(21, 80, 64, 3, 4)          \
-  X(20, 16, 96, 4, 6)          \
-  X(21, 16, 96, 4, 8)          \
-  X(22, 16, 96, 4, 4)
 #define DART_FA16_VARIANTS(X)      \
   X(0, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
   X(1, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
@@ -887,16 +499,14 @@ int fa_variant() {
 // (scripts/probes/mma_rate.cu), so the 6 P.V steps of a 96-key tile plus S, commits and waits
 // make a ~600-clk per-tile MMA chain (scripts/trace_attn.py timelines) that S(g+2) sits behind.
 // Staging P in shared memory or in separate TMEM buffers (S released at load time) was slower
-// (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.
+// (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.  A decoupled
+// variant at 96-key tiles (2 S buffers | one P buffer | O without the ones block, row sums in
+// registers; git history "fa_dec_kernel") was correct but also slower: N=20 2.67-2.78 vs 2.41 ms.
 int kv_tile_of(int hd, int var) {
 #define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
   if (hd == HD && var == V) return BKV;
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
-#undef X
-#define X(V, HD, BKV, ST, NP) \
-  if (hd == HD && var == V) return BKV;
-  DART_FADEC_VARIANTS(X)
 #undef X
   if (hd == 80) return 64;
   if (hd == 16) return 96;
@@ -921,10 +531,6 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
   if (head_dim == HD && var == V) return launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN>(tmQ, tmKV, a, num_sms, stream);
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
-#undef X
-#define X(V, HD, BKV, ST, NP) \
-  if (head_dim == HD && var == V) return launch_dec<HD, BKV, ST, NP>(tmQ, tmKV, a, num_sms, stream);
-  DART_FADEC_VARIANTS(X)
 #undef X
   if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0, 1>(tmQ, tmKV, a, num_sms, stream);
   if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0, 1>(tmQ, tmKV, a, num_sms, stream);
