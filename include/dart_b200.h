@@ -75,6 +75,19 @@ int32_t dart_expected_weight_count(const dart_model_desc* desc);
  * DART_FLAG_* bits. */
 int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
                   void* stream);
+/* The backbone in stages, for callers that re-run part of it (the reference's pruning search,
+ * pruning.py:154-204, memoises the activations entering each block):
+ * dart_backbone_embed: images -> x [B*T, E] fp32 (patch embedding; x rows in the engine's
+ *   window-major order: window-major row r of image b is token wm_to_token(r));
+ * dart_backbone_blocks: x <- blocks [b0, b1) applied in place, attn_on / mlp_on HOST int32
+ *   arrays of num_blocks sub-block enables (NULL: the handle's own flags);
+ * dart_backbone_fpn: x -> L0 / L1 / L2 (token-major) + finiteness flag bits (OR-ed in).
+ * dart_backbone == embed + blocks(0, num_blocks) + fpn. */
+int dart_backbone_embed(dart_model* m, const float* images, int32_t B, float* x, int32_t* flags, void* stream);
+int dart_backbone_blocks(dart_model* m, float* x, int32_t B, int32_t b0, int32_t b1, const int32_t* attn_on,
+                         const int32_t* mlp_on, void* stream);
+int dart_backbone_fpn(dart_model* m, const float* x, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
+                      void* stream);
 
 /* Class-batched encoder-decoder for B images x N classes.
  *   l0    [B, T, F0] float32 level-0 features, or NULL to reuse the last dart_backbone output

@@ -9,6 +9,7 @@ here, never on the GPU box.  The fixtures are what pins the oracle restatement
 
   A  SPEC toy profile (`toy_config(seed=0)`), 64^2, names car/person/dog (+8-class list)
   M  A with the mask head (mask_head_forward outputs)
+  P  greedy sub-block pruning on A's model (plan + every round's candidate losses)
   B  small-1008: full-width ViT-H/14 kernels at 4 blocks (globals 1,3), 6+6 enc-dec, 3 classes
   C  full ViT-H/14 DART 1008^2, 4 classes (person, car, dog, bicycle)
 
@@ -165,8 +166,43 @@ def make_mask(name: str, cfg, scene: SceneSpec, names):
     print(f"{name}: wrote {path}; masks {masks.shape}")
 
 
+def make_prune(name: str, cfg, seeds, k: int):
+    """Pruning golden: the reference's greedy_prune (pruning.py:207-248) on the
+    toy model with a small calibration set, plus every candidate loss of every round (for
+    margin-aware plan comparison) from its own _CalibEvaluator."""
+    from dart import pruning as PR
+
+    model = M.build_model(cfg, with_mask_head=False)
+    calib = [generate_scene(SceneSpec(seed=s, num_classes=3))[0] for s in seeds]
+    plan = PR.greedy_prune(model, calib, k, memoize=True)
+    # replay the search to record the full loss table of each round
+    prot = PR.protected_sub_blocks(cfg.global_block_indices)
+    cands = PR.candidate_sub_blocks(model, prot)
+    ev = PR._CalibEvaluator(model, calib, PR.reference_features(model, calib), memoize=True)
+    rounds = []
+    for step in plan.steps:
+        rounds.append([[c.block, PR.KINDS.index(c.kind), ev.loss(c)] for c in cands])
+        cands.remove(step.sub_block)
+        ev.accept(step.sub_block)
+    out = {
+        "config_json": np.array(json.dumps(cfg.to_dict())),
+        "weights_checksum": np.array(M.weights_checksum(model)),
+        "calib_seeds": np.array(list(seeds)),
+        "plan_json": np.array(PR.plan_to_json(plan)),
+        "plan_id": np.array(plan.plan_id()),
+        "round_losses": np.array([r + [[np.nan] * 3] * (len(rounds[0]) - len(r)) for r in rounds],
+                                 dtype=np.float64),  # [k, n_cand, 3] (block, kind, loss), NaN-padded
+    }
+    path = os.path.join(OUT, f"golden_{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: wrote {path}; plan {[(s.sub_block.block, s.sub_block.kind) for s in plan.steps]}")
+
+
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "A"
+    if which == "P":
+        make_prune("P", M.toy_config(seed=0), (11, 12, 13), k=5)
+        return
     if which == "M":
         make_mask("M", M.toy_config(seed=0), SceneSpec(seed=1, num_classes=3), ["car", "person", "dog"])
         return

@@ -26,6 +26,9 @@ EXPORTS = (
     "dart_model_fork",
     "dart_expected_weight_count",
     "dart_backbone",
+    "dart_backbone_embed",
+    "dart_backbone_blocks",
+    "dart_backbone_fpn",
     "dart_encdec",
     "dart_postprocess",
     "dart_model_set_mask_head",
@@ -99,6 +102,12 @@ def load() -> ctypes.CDLL:
     lib.dart_expected_weight_count.restype = I32
     lib.dart_backbone.argtypes = [P, P, I32, P, P, P, P, P]
     lib.dart_backbone.restype = ctypes.c_int
+    lib.dart_backbone_embed.argtypes = [P, P, I32, P, P, P]
+    lib.dart_backbone_embed.restype = ctypes.c_int
+    lib.dart_backbone_blocks.argtypes = [P, P, I32, I32, I32, P, P, P]
+    lib.dart_backbone_blocks.restype = ctypes.c_int
+    lib.dart_backbone_fpn.argtypes = [P, P, I32, P, P, P, P, P]
+    lib.dart_backbone_fpn.restype = ctypes.c_int
     lib.dart_encdec.argtypes = [P, P, I32, P, I32, P, P, P, P, P]
     lib.dart_encdec.restype = ctypes.c_int
     lib.dart_postprocess.argtypes = [P, P, P, P, I32, I32, F64, F64, F64, I32, P, P, P, P, P, P, P]

@@ -727,26 +727,31 @@ void dart_reset_launch_count(dart_model* m) {
   if (m) m->launches = 0;
 }
 
-int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
-                  void* stream) {
-  if (!m || !images || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone: bad args");
-  cudaStream_t s = (cudaStream_t)stream;
-  RUN(ensure_backbone_ws(m, B));
+}  // extern "C"
+
+namespace {
+
+// Backbone stages on a caller-chosen residual stream x [B*T, E] fp32 in window-major row order
+// (each 24x24 window a contiguous block; global attention, LN and the MLP are order-invariant,
+// the patchify / RoPE / FPN kernels map rows to tokens).
+int bb_embed(dart_model* m, const float* images, int B, float* x, int32_t* flags, cudaStream_t s) {
+  auto& w = m->bb;
+  const int rows = B * m->T, win = m->d.window_size;
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t), s) != cudaSuccess) return fail(DART_ERR_CUDA, "flags memset");
+  LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, win, flags, s));
+  return gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(x, m->E), s);
+}
+
+int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* attn_on, const int32_t* mlp_on,
+              cudaStream_t s) {
   const int T = m->T, E = m->E, H = m->H, hd = m->hd, G = m->G;
   const int rows = B * T;
   auto& w = m->bb;
-  // patch embedding (im2col fused with the [0,1] range check) + GEMM
-  // The residual stream is kept in window-major row order (windows = contiguous 576-row
-  // blocks); global attention, LayerNorm and the MLP are order-invariant, RoPE and the
-  // FPN map rows back to true tokens.
   const int win = m->d.window_size, nwin = (G / win) * (G / win);
-  LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, win, flags, s));
-  RUN(gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(w.x, E), s));
-  for (int b = 0; b < m->d.num_blocks; ++b) {
+  for (int b = b0; b < b1; ++b) {
     const BlockW& bw = m->blocks[b];
-    if (m->d.attn_enabled[b]) {
-      LAUNCH(layernorm_f32_to_f16(w.x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
+    if (attn_on ? attn_on[b] : m->d.attn_enabled[b]) {
+      LAUNCH(layernorm_f32_to_f16(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
       GemmEpi e = epi_out(w.qkv, 3 * E);
       e.rope_cos = m->rope_cos;
       e.rope_sin = m->rope_sin;
@@ -781,16 +786,22 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
       } else {
         RUN(attn(m, a, hd, s));
       }
-      RUN(gemm(m, w.ao, rows, E, bw.out, EPI_F32_RESID, epi_out(w.x, E), s));
+      RUN(gemm(m, w.ao, rows, E, bw.out, EPI_F32_RESID, epi_out(x, E), s));
     }
-    if (m->d.mlp_enabled[b]) {
-      LAUNCH(layernorm_f32_to_f16(w.x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
+    if (mlp_on ? mlp_on[b] : m->d.mlp_enabled[b]) {
+      LAUNCH(layernorm_f32_to_f16(x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
       RUN(gemm(m, w.h, rows, E, bw.fc1, EPI_F16_RELU, epi_out(w.hid, 4 * E), s));
-      RUN(gemm(m, w.hid, rows, 4 * E, bw.fc2, EPI_F32_RESID, epi_out(w.x, E), s));
+      RUN(gemm(m, w.hid, rows, 4 * E, bw.fc2, EPI_F32_RESID, epi_out(x, E), s));
     }
   }
-  // FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
-  LAUNCH(cast_f32_to_f16(w.x, w.h, (long long)rows * E, s));
+  return DART_OK;
+}
+
+// FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
+int bb_fpn(dart_model* m, const float* x, int B, float* l0, float* l1, float* l2, int32_t* flags, cudaStream_t s) {
+  auto& w = m->bb;
+  const int rows = B * m->T, E = m->E, G = m->G, win = m->d.window_size;
+  LAUNCH(cast_f32_to_f16(x, w.h, (long long)rows * E, s));
   GemmEpi e0 = epi_out(l0, m->F0);  // rows scattered back to token-major order
   e0.out2 = w.l0h;
   e0.ldo2 = m->F0;
@@ -798,15 +809,50 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
   e0.wm_win = win;
   e0.wm_scatter = 1;
   RUN(gemm(m, w.h, rows, E, m->fpn[0], EPI_F32_F16, e0, s));
-  LAUNCH(pool_tokens(w.x, w.pool1, B, G, E, 2, win, s));
+  LAUNCH(pool_tokens(x, w.pool1, B, G, E, 2, win, s));
   RUN(gemm(m, w.pool1, rows / 4, E, m->fpn[1], EPI_F32, epi_out(l1, m->F1), s));
-  LAUNCH(pool_tokens(w.x, w.pool2, B, G, E, 4, win, s));
+  LAUNCH(pool_tokens(x, w.pool2, B, G, E, 4, win, s));
   RUN(gemm(m, w.pool2, rows / 16, E, m->fpn[2], EPI_F32, epi_out(l2, m->F2), s));
   LAUNCH(finite_check(l0, (long long)rows * m->F0, flags, DART_FLAG_NONFINITE, s));
   LAUNCH(finite_check(l1, (long long)rows / 4 * m->F1, flags, DART_FLAG_NONFINITE, s));
   LAUNCH(finite_check(l2, (long long)rows / 16 * m->F2, flags, DART_FLAG_NONFINITE, s));
   m->last_backbone_B = B;
   return DART_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
+                  void* stream) {
+  if (!m || !images || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  RUN(ensure_backbone_ws(m, B));
+  RUN(bb_embed(m, images, B, m->bb.x, flags, s));
+  RUN(bb_blocks(m, m->bb.x, B, 0, m->d.num_blocks, nullptr, nullptr, s));
+  return bb_fpn(m, m->bb.x, B, l0, l1, l2, flags, s);
+}
+
+int dart_backbone_embed(dart_model* m, const float* images, int32_t B, float* x, int32_t* flags, void* stream) {
+  if (!m || !images || B <= 0 || !x || !flags) return fail(DART_ERR_INVALID, "dart_backbone_embed: bad args");
+  RUN(ensure_backbone_ws(m, B));
+  return bb_embed(m, images, B, x, flags, (cudaStream_t)stream);
+}
+
+int dart_backbone_blocks(dart_model* m, float* x, int32_t B, int32_t b0, int32_t b1, const int32_t* attn_on,
+                         const int32_t* mlp_on, void* stream) {
+  if (!m || !x || B <= 0 || b0 < 0 || b1 > m->d.num_blocks || b0 > b1)
+    return fail(DART_ERR_INVALID, "dart_backbone_blocks: bad args");
+  RUN(ensure_backbone_ws(m, B));
+  return bb_blocks(m, x, B, b0, b1, attn_on, mlp_on, (cudaStream_t)stream);
+}
+
+int dart_backbone_fpn(dart_model* m, const float* x, int32_t B, float* l0, float* l1, float* l2, int32_t* flags,
+                      void* stream) {
+  if (!m || !x || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone_fpn: bad args");
+  RUN(ensure_backbone_ws(m, B));
+  return bb_fpn(m, x, B, l0, l1, l2, flags, (cudaStream_t)stream);
 }
 
 int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
