@@ -12,6 +12,7 @@ device->host copy of the kept detections.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -150,7 +151,9 @@ class Detector:
         p = {
             "B": B,
             "h_dec": self.handle.fork(),
-            "s_bb": torch.cuda.Stream(device=self.device),
+            # DART_PIPE_PRIORITY=1: the backbone stream (the pipeline's critical path) gets the
+            # higher CUDA stream priority (A/B measurement)
+            "s_bb": torch.cuda.Stream(device=self.device, priority=-1 if os.environ.get("DART_PIPE_PRIORITY") else 0),
             "s_dec": torch.cuda.Stream(device=self.device),
             "slots": [self._alloc_slot(B) for _ in range(2)],
             "ev_bb": [torch.cuda.Event() for _ in range(2)],
