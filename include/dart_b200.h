@@ -137,6 +137,10 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
               int32_t rope_cols, void* stream);
 void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
 void dart_gemm_force_plan(int32_t bn, int32_t cg);
+/* y = LayerNorm(x) per row (population variance, eps 1e-6; reference tensors.py:215-227), fp32 in,
+ * fp16 (out_f16 = 1) or fp32 out; dim in {32, 64, 128, 256, 512, 1024, 1280}. */
+int dart_layernorm(const float* x, const float* gamma, const float* beta, void* y, int32_t rows, int32_t dim,
+                   int32_t out_f16, void* stream);
 /* Tests: s = 2 makes later dart_gemm residual calls (epi 3, K/64 even) run split-K (two K halves
  * per tile on different CTA pairs, deterministic adds); s = 1 restores the default. */
 void dart_gemm_force_splitk(int32_t s);

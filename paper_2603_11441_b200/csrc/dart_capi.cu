@@ -1017,6 +1017,15 @@ void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg)
 }
 
 void dart_gemm_force_plan(int32_t bn, int32_t cg) { gemm_force_plan(bn, cg); }
+
+int dart_layernorm(const float* x, const float* gamma, const float* beta, void* y, int32_t rows, int32_t dim,
+                   int32_t out_f16, void* stream) {
+  if (!x || !gamma || !beta || !y || rows <= 0) return fail(DART_ERR_INVALID, "dart_layernorm: bad args");
+  const int rc = out_f16 ? layernorm_f32_to_f16(x, gamma, beta, (__half*)y, rows, dim, dim, dim, (cudaStream_t)stream)
+                         : layernorm_f32_to_f32(x, gamma, beta, (float*)y, rows, dim, (cudaStream_t)stream);
+  if (rc) return fail(DART_ERR_CUDA, std::string("layernorm: ") + cudaGetErrorString((cudaError_t)rc));
+  return DART_OK;
+}
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,

@@ -5,6 +5,8 @@
 //   finiteness flag                      reference model.py:161-166
 //   text-row gather (embedding cache)    reference model.py:462-484
 //   box / score / presence heads         reference model.py:528-532, sigmoid model.py:351-353
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -13,47 +15,69 @@ namespace {
 
 constexpr float LN_EPS = 1e-6f;
 
-// One warp per row; VPL values per lane.  VPL % 4 == 0: float4 loads of columns
-// 128*i + 4*lane .. +3 (fully coalesced 512 B per warp instruction) and 8-byte fp16 stores.
-template <int VPL, typename OutT>
+// One warp per RPW rows (RPW = 1 or 2: both rows' loads in flight before either reduction);
+// VPL values per lane.  VPL % 4 == 0: float4 loads of columns 128*i + 4*lane .. +3 (fully
+// coalesced 512 B per warp instruction) and 8-byte fp16 stores.  Two-pass (mean, then centred
+// variance) in fp32, population variance, eps 1e-6 (reference tensors.py:215-227).
+template <int VPL, typename OutT, int RPW = 1>
 __global__ void layernorm_vec_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                      const float* __restrict__ beta, OutT* __restrict__ y, int rows, int ld_in,
                                      int ld_out) {
   constexpr int V4 = VPL / 4;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ld_in);
-  float4 v[V4];
-  float s = 0.f;
+  if (row0 >= rows) return;
+  float4 v[RPW][V4];
+  float s[RPW];
 #pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    v[i] = xr[32 * i + lane];
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  for (int r = 0; r < RPW; ++r) {
+    s[r] = 0.f;
+    const int row = row0 + r < rows ? row0 + r : row0;
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ld_in);
+#pragma unroll
+    for (int i = 0; i < V4; ++i) v[r][i] = xr[32 * i + lane];
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
-  const float mu = s * (1.0f / (32 * VPL));
-  float q = 0.f;
+  for (int r = 0; r < RPW; ++r)
 #pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
-    q += (a * a + b * b) + (c * c + d * d);
+    for (int i = 0; i < V4; ++i) s[r] += (v[r][i].x + v[r][i].y) + (v[r][i].z + v[r][i].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) s[r] += __shfl_xor_sync(0xffffffff, s[r], o);
+  float mu[RPW], q[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    mu[r] = s[r] * (1.0f / (32 * VPL));
+    q[r] = 0.f;
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const float a = v[r][i].x - mu[r], b = v[r][i].y - mu[r], c = v[r][i].z - mu[r], d = v[r][i].w - mu[r];
+      q[r] += (a * a + b * b) + (c * c + d * d);
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
-  const float rstd = 1.0f / sqrtf(q * (1.0f / (32 * VPL)) + LN_EPS);
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) q[r] += __shfl_xor_sync(0xffffffff, q[r], o);
   const float4* g4 = reinterpret_cast<const float4*>(gamma);
   const float4* b4 = reinterpret_cast<const float4*>(beta);
 #pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    const float4 g = __ldg(g4 + 32 * i + lane), b = __ldg(b4 + 32 * i + lane);
-    const float r0 = (v[i].x - mu) * rstd * g.x + b.x, r1 = (v[i].y - mu) * rstd * g.y + b.y;
-    const float r2 = (v[i].z - mu) * rstd * g.z + b.z, r3 = (v[i].w - mu) * rstd * g.w + b.w;
-    if constexpr (sizeof(OutT) == 2) {
-      reinterpret_cast<uint2*>(y + (size_t)row * ld_out)[32 * i + lane] = make_uint2(pack_half2(r0, r1), pack_half2(r2, r3));
-    } else {
-      reinterpret_cast<float4*>(y + (size_t)row * ld_out)[32 * i + lane] = make_float4(r0, r1, r2, r3);
+  for (int r = 0; r < RPW; ++r) {
+    if (row0 + r >= rows) break;
+    const float rstd = 1.0f / sqrtf(q[r] * (1.0f / (32 * VPL)) + LN_EPS);
+    const size_t row = (size_t)(row0 + r);
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const float4 g = __ldg(g4 + 32 * i + lane), b = __ldg(b4 + 32 * i + lane);
+      const float4 w = v[r][i];
+      const float r0 = (w.x - mu[r]) * rstd * g.x + b.x, r1 = (w.y - mu[r]) * rstd * g.y + b.y;
+      const float r2 = (w.z - mu[r]) * rstd * g.z + b.z, r3 = (w.w - mu[r]) * rstd * g.w + b.w;
+      if constexpr (sizeof(OutT) == 2) {
+        reinterpret_cast<uint2*>(y + row * ld_out)[32 * i + lane] = make_uint2(pack_half2(r0, r1), pack_half2(r2, r3));
+      } else {
+        reinterpret_cast<float4*>(y + row * ld_out)[32 * i + lane] = make_float4(r0, r1, r2, r3);
+      }
     }
   }
 }
@@ -97,12 +121,26 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
   }
 }
 
+int env_int(const char* n, int d) {
+  const char* e = getenv(n);
+  return e ? atoi(e) : d;
+}
+// LayerNorm launch shape (A/B: DART_LN_WARPS warps per block, DART_LN_RPW rows per warp)
+int g_ln_warps = env_int("DART_LN_WARPS", 4), g_ln_rpw = env_int("DART_LN_RPW", 1);  // measured best (scripts/bench_ln.py)
+
 template <typename OutT>
 int ln_dispatch(const float* x, const float* g, const float* b, OutT* y, int rows, int dim, int ld_in, int ld_out,
                 cudaStream_t st) {
   if (rows <= 0) return 0;
-  const int warps = 8;
+  const int warps = g_ln_warps;
+  const int rpw = g_ln_rpw;
   dim3 grid((rows + warps - 1) / warps);
+  if (rpw == 2 && (dim == 256 || dim == 1280)) {
+    dim3 g2((rows + 2 * warps - 1) / (2 * warps));
+    if (dim == 256) layernorm_vec_kernel<8, OutT, 2><<<g2, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out);
+    else layernorm_vec_kernel<40, OutT, 2><<<g2, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out);
+    return (int)cudaGetLastError();
+  }
   switch (dim) {
     case 32: layernorm_kernel<1, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
     case 64: layernorm_kernel<2, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;

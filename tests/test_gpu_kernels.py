@@ -296,3 +296,18 @@ def test_attention_tcgen05_forced_safe_pass(lib, items, L, hd):
     ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
     assert float((o1.float() - ref).abs().max()) < 1e-2
     assert float((o2.float() - ref).abs().max()) < 1e-2
+
+
+@pytest.mark.parametrize("rows,dim,f16", [(5184, 1280, 1), (20736, 256, 1), (777, 256, 0), (1001, 1280, 1), (33, 64, 1)])
+def test_layernorm(lib, rows, dim, f16):
+    """LayerNorm (population variance, eps 1e-6; reference tensors.py:215-227) vs fp32 torch."""
+    g = torch.Generator(device="cuda").manual_seed(rows + dim)
+    x = torch.randn(rows, dim, device="cuda", generator=g) * 3 + 1.5
+    gamma = torch.randn(dim, device="cuda", generator=g)
+    beta = torch.randn(dim, device="cuda", generator=g)
+    y = torch.empty(rows, dim, device="cuda", dtype=torch.float16 if f16 else torch.float32)
+    _native.check(lib.dart_layernorm(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), rows, dim, f16,
+                                     stream()))
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.layer_norm(x, (dim,), gamma, beta, eps=1e-6)
+    assert float((y.float() - ref).abs().max()) < (1e-2 if f16 else 1e-4)
