@@ -406,7 +406,11 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
     e.splitk = 2;
     e.tile_flags = m->splitk_flags;
   }
-  int rc = gemm_tc(ta, W.tmap[box_slot(plan.bn / plan.cg)], &tc, &td, M, W.N, W.K, plan, epi, e, m->num_sms, s);
+  const int half_rows = plan.bn / 2 / plan.cg;  // tail-halves B box (tiles of the last wave split in two)
+  const CUtensorMap* tb2 = (half_rows == 128 || half_rows == 64 || half_rows == 32) && W.N % half_rows == 0
+                               ? &W.tmap[box_slot(half_rows)]
+                               : nullptr;
+  int rc = gemm_tc(ta, W.tmap[box_slot(plan.bn / plan.cg)], tb2, &tc, &td, M, W.N, W.K, plan, epi, e, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
 }
@@ -1002,7 +1006,10 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
     e.splitk = 2;
     e.tile_flags = flags;
   }
-  int rc = gemm_tc(ta, tb, &tc, &td, M, N, K, plan, epi, e, sms, (cudaStream_t)stream);
+  CUtensorMap tb2;
+  const int half_rows = plan.bn / 2 / plan.cg;
+  const bool has_b2 = half_rows >= 32 && make_tmap(&tb2, W, K, N, K, half_rows);
+  int rc = gemm_tc(ta, tb, has_b2 ? &tb2 : nullptr, &tc, &td, M, N, K, plan, epi, e, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }

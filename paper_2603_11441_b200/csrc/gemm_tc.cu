@@ -229,8 +229,8 @@ constexpr int GEMM_THREADS = 384;
 template <int BN, int STAGES, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int M, int N,
-                   int K, GemmEpi epi) {
+                   const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                   const __grid_constant__ CUtensorMap tmD, int M, int N, int K, GemmEpi epi) {
   // tmC: fp32 [M, N] output / residual map (box 32x32, 128B swizzle); tmD: fp16 [M, N] output map
   // (box 32x32, 64B swizzle).  Outputs leave through per-warp smem chunks and TMA bulk stores.
   using L = GemmSmem<BN, STAGES, EPI, CG>;
@@ -253,12 +253,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
   const int SK = RESID ? epi.splitk : 1;  // K slices per tile (work unit = tile x slice)
-  const int num_units = num_tiles * SK;
+  const int TF = epi.tail_full;           // tail halves: units >= TF are BN/2-wide halves of a tile
+  const int num_units = TF > 0 ? TF + 2 * (num_tiles - TF) : num_tiles * SK;
   const int nk = K / BK / SK;             // k-blocks per unit
+  // unit -> (tile, K slice, n half or -1 for a full-width unit)
+  auto decode = [&](int u, int& tile, int& kh, int& nh) {
+    if (TF > 0 && u >= TF) {
+      tile = TF + ((u - TF) >> 1);
+      nh = (u - TF) & 1;
+      kh = 0;
+    } else {
+      tile = u / SK;
+      kh = u % SK;
+      nh = -1;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (TF > 0) tma_prefetch_desc(&tmB2);
     if (RESID || EPI == EPI_F32) tma_prefetch_desc(&tmC);
     if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
@@ -284,9 +298,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = cl; unit < num_units; unit += ncl) {
-        const int tile = unit / SK, kb0 = (unit % SK) * nk;
+        int tile, kh, nh;
+        decode(unit, tile, kh, nh);
+        const int kb0 = kh * nk;
+        const bool hu = nh >= 0;
         const int m0 = (tile / num_n) * BM * CG + rank * BM;
-        const int n0 = (tile % num_n) * BN + rank * L::B_ROWS;
+        const int n0 = (tile % num_n) * BN + (hu ? nh * (BN / 2) + rank * (L::B_ROWS / 2) : rank * L::B_ROWS);
+        const CUtensorMap* mb = hu ? &tmB2 : &tmB;
+        const uint32_t bytes = hu ? L::A_BYTES + L::B_BYTES / 2 : L::STAGE_BYTES;
         for (int kb = kb0; kb < kb0 + nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
@@ -294,13 +313,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (epi.dbg_noload && (unit != cl || kb >= STAGES)) {
             if (rank == 0) mbar_arrive(&full[stage]);
           } else if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], bytes);
             tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-            tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
+            tma_load_2d(sb, mb, &full[stage], kb * BK, n0);
           } else {
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
             tma_load_2d_cg2(sa, &tmA, &full[stage], kb * BK, m0);
-            tma_load_2d_cg2(sb, &tmB, &full[stage], kb * BK, n0);
+            tma_load_2d_cg2(sb, mb, &full[stage], kb * BK, n0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -311,11 +330,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(BM * CG, BN);
+      constexpr uint32_t idesc_full = umma_idesc_f16(BM * CG, BN);
+      constexpr uint32_t idesc_half = umma_idesc_f16(BM * CG, BN / 2);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+        const uint32_t idesc = (TF > 0 && unit >= TF) ? idesc_half : idesc_full;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -362,31 +383,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* rbar = rfull + (warp - 4) * NBUF;
     const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
     // residual chunk g of this warp -> smem buffer g % NBUF (lane 0 issues; NBUF-1 chunks ahead)
-    const int cpw = (BN - half * 32 + 63) / 64;  // 32-column chunks of this warp per tile
-    auto resid_load = [&](int g) {
-      const int u = cl + (g / cpw) * ncl;
-      if (u >= num_units) return;
-      const int t = u / SK;
-      if (SK > 1 && u % SK == 1 && g % cpw == 0) {  // half 1 reads what half 0 of this tile stored
+    // residual prefetch iterator: (unit, chunk) of the next chunk this warp will process
+    int pf_u = cl, pf_c = 0;
+    auto resid_load = [&](int g) {  // prefetch the iterator's chunk into buffer g % NBUF, advance
+      if (pf_u >= num_units) return;
+      int t, kh, nh;
+      decode(pf_u, t, kh, nh);
+      const int bne = nh >= 0 ? BN / 2 : BN;
+      if (SK > 1 && kh == 1 && pf_c == 0) {  // split-K half 1 reads what half 0 of this tile stored
         volatile int* f = epi.tile_flags + t;
         while (*f < 8 * CG) __nanosleep(64);
         __threadfence();
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
-      const int cc = (t % num_n) * BN + ((g % cpw) * 2 + half) * 32;
+      const int cc = (t % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0) + (pf_c * 2 + half) * 32;
       mbar_arrive_expect_tx(&rbar[g % NBUF], 32 * 32 * 4);
       tma_load_2d(bufs + (g % NBUF) * 1024, &tmC, &rbar[g % NBUF], cc, rr);
+      if (++pf_c == (bne - half * 32 + 63) / 64) {
+        pf_c = 0;
+        pf_u += ncl;
+      }
     };
     if (RESID && lane == 0)
       for (int i = 0; i < NBUF - 1; ++i) resid_load(i);
     int it = 0, g = 0;
     for (int unit = cl; unit < num_units; unit += ncl, ++it) {
-      const int tile = unit / SK, kh = unit % SK;
+      int tile, kh, nh;
+      decode(unit, tile, kh, nh);
+      const int bn_eff = nh >= 0 ? BN / 2 : BN;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (tile / num_n) * BM * CG + rank * BM;
-      const int n0 = (tile % num_n) * BN;
+      const int n0 = (tile % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0);
       const int row0 = m0 + quarter * 32;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -401,7 +430,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ct = rope_s + (ROPE_MAX_GRID + tc) * ROPE_PAD;
       }
 #pragma unroll 1
-      for (int c = half * 32; c < BN; c += 64, ++g) {
+      for (int c = half * 32; c < bn_eff; c += 64, ++g) {
         float* buf = bufs + (g % NBUF) * 1024;
         if (lane == 0) {
           if (RESID) {
@@ -415,7 +444,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
-        if (c + 64 >= BN) {
+        if (c + 64 >= bn_eff) {
           // all of this warp's accumulator columns are in registers: hand TMEM back early
           tc_fence_before();
           __syncwarp();
@@ -494,8 +523,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 template <int BN, int STAGES, int EPI, int CG>
-int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, const CUtensorMap& tD, int M,
-                int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
+                const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES, EPI, CG>;
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG>;
   static bool configured = false;
@@ -508,7 +537,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   if constexpr (CG == 1) {
-    kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(tA, tB, tC, tD, M, N, K, epi);
+    kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(tA, tB, tB2, tC, tD, M, N, K, epi);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -522,7 +551,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, M, N, K, epi);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tB2, tC, tD, M, N, K, epi);
     if (e != cudaSuccess) return (int)e;
   }
   return (int)cudaGetLastError();
@@ -539,26 +568,28 @@ constexpr int stages_for() {
 }
 
 template <int BN, int EPI, int CG>
-int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC, const CUtensorMap& tD, int M,
-                   int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
-  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
+                   const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
 }
 
 template <int BN, int CG>
-int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
-                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2,
+                 const CUtensorMap& tC, const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms,
+                 cudaStream_t stream) {
   switch (epi_mode) {
-    case EPI_F16: return launch_planned<BN, EPI_F16, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
-    case EPI_F16_RELU: return launch_planned<BN, EPI_F16_RELU, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
-    case EPI_F32: return launch_planned<BN, EPI_F32, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
-    case EPI_F32_RESID: return launch_planned<BN, EPI_F32_RESID, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
-    case EPI_QKV_ROPE: return launch_planned<BN, EPI_QKV_ROPE, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
-    case EPI_F32_F16: return launch_planned<BN, EPI_F32_F16, CG>(tA, tB, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F16: return launch_planned<BN, EPI_F16, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F16_RELU: return launch_planned<BN, EPI_F16_RELU, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32: return launch_planned<BN, EPI_F32, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_RESID: return launch_planned<BN, EPI_F32_RESID, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_QKV_ROPE: return launch_planned<BN, EPI_QKV_ROPE, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_F16: return launch_planned<BN, EPI_F32_F16, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
   }
   return (int)cudaErrorInvalidValue;
 }
 
 GemmPlan g_forced{0, 0};  // dart_gemm_force_plan (tests / A-B measurement); bn 0 = automatic
+int g_tail_halves = getenv("DART_NO_TAIL_HALVES") == nullptr;
 // relative per-column efficiency of the 192 / 160-wide CTA-pair tiles (operand re-reads grow
 // as the tile narrows); DART_GEMM_EFF192 / DART_GEMM_EFF160 override for A/B measurement
 double env_or(const char* n, double d) {
@@ -605,8 +636,10 @@ GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
 
 void gemm_force_plan(int bn, int cg) { g_forced = GemmPlan{bn, cg == 2 ? 2 : 1}; }
 
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, const CUtensorMap* tD, int M, int N,
-            int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2, const CUtensorMap* tC,
+            const CUtensorMap* tD, int M, int N, int K, GemmPlan plan, int epi_mode, const GemmEpi& epi_in, int num_sms,
+            cudaStream_t stream) {
+  GemmEpi epi = epi_in;
   if (M <= 0) return 0;
   const int BN = plan.bn;
   if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
@@ -621,19 +654,28 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC,
   if ((f32_out && !tC) || (f16_out && !tD)) return (int)cudaErrorInvalidValue;
   const CUtensorMap& c = tC ? *tC : tA;
   const CUtensorMap& d = tD ? *tD : tA;
+  const CUtensorMap& b2 = tB2 ? *tB2 : tB;
+  // tail halves: when the tiles leave a last wave at most half full, run it as half-width units
+  epi.tail_full = 0;
+  if (tB2 && g_tail_halves && epi.splitk == 1 && (BN == 256 || BN == 128)) {
+    const int tiles = ((M + BM * plan.cg - 1) / (BM * plan.cg)) * (N / BN);
+    const int units = num_sms / plan.cg;
+    const int rem = tiles % units;
+    if (tiles > units && rem > 0 && 2 * rem <= units) epi.tail_full = tiles - rem;
+  }
   if (plan.cg == 2) {
     switch (BN) {
-      case 256: return dispatch_epi<256, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 192: return dispatch_epi<192, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 160: return dispatch_epi<160, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 128: return dispatch_epi<128, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 64: return dispatch_epi<64, 2>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 256: return dispatch_epi<256, 2>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 192: return dispatch_epi<192, 2>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 160: return dispatch_epi<160, 2>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 128: return dispatch_epi<128, 2>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 64: return dispatch_epi<64, 2>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
     }
   } else {
     switch (BN) {
-      case 256: return dispatch_epi<256, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 128: return dispatch_epi<128, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
-      case 64: return dispatch_epi<64, 1>(epi_mode, tA, tB, c, d, M, N, K, epi, num_sms, stream);
+      case 256: return dispatch_epi<256, 1>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 128: return dispatch_epi<128, 1>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
+      case 64: return dispatch_epi<64, 1>(epi_mode, tA, tB, b2, c, d, M, N, K, epi, num_sms, stream);
     }
   }
   return (int)cudaErrorInvalidValue;

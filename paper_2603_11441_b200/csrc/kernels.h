@@ -41,6 +41,9 @@ struct GemmEpi {
   // Deterministic order, no workspace; tile_flags must be zeroed before the launch.
   int splitk = 1;
   int* tile_flags = nullptr;
+  // Tail halves: the first tail_full tiles (a whole number of waves) run as BN-wide units, the
+  // remaining tiles as two BN/2-wide units each, so the last wave is half as long (0 = off).
+  int tail_full = 0;
 };
 
 // window-major row index <-> token index within one image
@@ -65,8 +68,10 @@ void gemm_force_plan(int bn, int cg);  // bn 0: automatic
 // Output maps over out [M, N] (row stride ldo), box {32, 32}: tC fp32 with 128B swizzle
 // (EPI_F32 / EPI_F32_F16 without wm_scatter, and the EPI_F32_RESID residual), tD fp16 with 64B
 // swizzle (EPI_F16, EPI_F16_RELU, EPI_QKV_ROPE); the unused one may be null.
-int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tC, const CUtensorMap* tD, int M, int N,
-            int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms, cudaStream_t stream);
+// tB2: W map with box {64, plan.bn / 2 / plan.cg} for the tail-halves units (may be null: no tail halves).
+int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2, const CUtensorMap* tC,
+            const CUtensorMap* tD, int M, int N, int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms,
+            cudaStream_t stream);
 
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {

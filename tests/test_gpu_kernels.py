@@ -112,11 +112,19 @@ def test_gemm_split_k_residual(lib, bn, cg, M, N, K):
 
 @pytest.mark.parametrize("bn,cg", PLANS)
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 5])
-def test_gemm_forced_plans(lib, bn, cg, epi):
+@pytest.mark.parametrize("shape", ["waves", "tail"])
+def test_gemm_forced_plans(lib, bn, cg, epi, shape):
     """Every tile plan (1-SM 128 x bn and CTA-pair 256 x bn tiles) and epilogue, with M and N tails
-    that leave partial 256-row tiles and several waves."""
+    that leave partial 256-row tiles and several waves.  "tail": the DART shapes whose last wave
+    is at most half full (5184 x 1280: 105 CTA-pair tiles; 5184 x 3840: 315), which run that wave
+    as half-width units."""
     T, E = 576, 1280
-    M, N, K = (1700, 3840, 1280) if epi == 4 else (5000, 6 * bn, 320)
+    if shape == "tail":
+        M, N, K = (5184, 3840, 1280) if epi == 4 else (5184, 1280, 640)
+        if N % bn:
+            pytest.skip("bn does not divide N")
+    else:
+        M, N, K = (1700, 3840, 1280) if epi == 4 else (5000, 6 * bn, 320)
     g = torch.Generator(device="cuda").manual_seed(bn * 10 + cg + epi)
     A = torch.randn(M, K, device="cuda", generator=g).half()
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
