@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       }
       __syncwarp();
     } else if (warp == 1) {
-      if (lane == 0 && a.softmax_only != 1) {
+      if (a.softmax_only != 1) {  // the whole warp runs the issue loop (converged); one lane issues
         constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
         constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, L::ON) | (1u << 16);  // B (V) MN-major
         // the K-ready wait of S(gg) can be hoisted off the P-ready -> P.V -> S critical path
@@ -222,15 +222,15 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         auto issue_s = [&](int gg, uint32_t sq, bool k_waited) {
           const int st = gg % STAGES;
           if (!k_waited) wait_k(gg);
-          if (a.trace && blockIdx.x == 0 && gg >= 2 && gg - 2 < 256) a.trace[1536 + gg - 2] = clock64();
+          if (a.trace && blockIdx.x == 0 && lane == 0 && gg >= 2 && gg - 2 < 256) a.trace[1536 + gg - 2] = clock64();
           tc_fence_after();
           const uint32_t sk = smem_u32(smem + L::OFF_K + st * L::K_BYTES);
 #pragma unroll
           for (int b = 0; b < L::NB; ++b)
-            umma_f16(tmem + (gg % NS) * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
+            umma_f16_w(tmem + (gg % NS) * BKV, desc_sw32(sq + b * L::Q_BLOCK, 16, 256),
                      desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
-          if constexpr (!LEAN) umma_commit(&k_empty[st]);
-          umma_commit(&s_full[gg % NS]);
+          if constexpr (!LEAN) umma_commit_w(&k_empty[st]);
+          umma_commit_w(&s_full[gg % NS]);
         };
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
@@ -248,30 +248,30 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
               wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
               if (j + NS < nkv) wait_k(m_g + NS);
               wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
-              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = a.trace[1024 + m_g] = clock64();
+              if (a.trace && blockIdx.x == 0 && lane == 0 && m_g < 256) a.trace[512 + m_g] = a.trace[1024 + m_g] = clock64();
             } else {
               wait_sel<SPIN & 1>(&p_full[sb], (m_g / NS) & 1, 5000000 + m_g, a.dbg);
-              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[512 + m_g] = clock64();
+              if (a.trace && blockIdx.x == 0 && lane == 0 && m_g < 256) a.trace[512 + m_g] = clock64();
               wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, a.dbg);
-              if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1024 + m_g] = clock64();
+              if (a.trace && blockIdx.x == 0 && lane == 0 && m_g < 256) a.trace[1024 + m_g] = clock64();
             }
             tc_fence_after();
             const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
 #pragma unroll
             for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
-              umma_f16_ts(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16), desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
+              umma_f16_ts_w(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16), desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
                           idesc_pv, (j | kc) != 0);
-            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[1280 + m_g] = clock64();
+            if (a.trace && blockIdx.x == 0 && lane == 0 && m_g < 256) a.trace[1280 + m_g] = clock64();
             if constexpr (LEAN) {
-              if (pass == 1) umma_commit(&o_done[m_g1++ % NS]);
-              if (j == nkv - 1) umma_commit(item_done);
+              if (pass == 1) umma_commit_w(&o_done[m_g1++ % NS]);
+              if (j == nkv - 1) umma_commit_w(item_done);
             } else {
-              umma_commit(&v_empty[st]);
-              umma_commit(&o_done[sb]);
+              umma_commit_w(&v_empty[st]);
+              umma_commit_w(&o_done[sb]);
             }
             if (j + NS < nkv) issue_s(m_g + NS, sq, LEAN);
-            if (!LEAN && j == nkv - 1) umma_commit(&q_empty[qb]);  // every MMA reading this Q buffer issued
-            if (a.trace && blockIdx.x == 0 && m_g < 256) a.trace[768 + m_g] = clock64();
+            if (!LEAN && j == nkv - 1) umma_commit_w(&q_empty[qb]);  // every MMA reading this Q buffer issued
+            if (a.trace && blockIdx.x == 0 && lane == 0 && m_g < 256) a.trace[768 + m_g] = clock64();
           }
           ++m_it;
         }
@@ -482,14 +482,18 @@ int fa_variant() {
 
 // Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16).
 #define DART_FA80_VARIANTS(X)      \
-  X(0, 80, 64, 3, 2, 2, 1, 0, 0, 1) \
-  X(1, 80, 64, 3, 2, 2, 1, 0, 0, 0) \
-  X(2, 80, 64, 3, 2, 2, 1, 4, 0, 1)
+  X(0, 80, 64, 3, 2, 2, 1, 0, 0, 0) \
+  X(1, 80, 64, 3, 2, 2, 1, 0, 0, 1) \
+  X(2, 80, 64, 3, 2, 2, 1, 4, 0, 0)
 #define DART_FA16_VARIANTS(X)      \
-  X(0, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
-  X(1, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
-  X(2, 16, 96, 4, 2, 2, 1, 8, 0, 1) \
-  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 1)
+  X(0, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
+  X(1, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
+  X(2, 16, 96, 4, 2, 2, 1, 8, 0, 0) \
+  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 0)
+// Variant 0 issues MMAs from the converged warp 1 (warp-collective umma_*_w, one elected lane):
+// the per-MMA issue path shrank from ~77 to ~40 clk (no per-lane R2UR waterfall), which took hd 80
+// global attention 217 -> 193 us and windowed 36.5 -> 33.2 us (scripts/ab_attn.py); with it the
+// commit-per-tile protocol (LEAN = 0) beats the lean one (LEAN = 1: 210 / 35.6 us; hd 16 equal).
 // Measured on B200 (scripts/bench_attn.py, hd 16 enc self-attention N=80 = 80x16 heads x 5184^2;
 // box-to-box spread ~8%): variant 0 8.7-9.4 ms; NPOLY 8 9.7, NPOLY 4 9.1; 2 column slices
 // 9.6-10.5; 64-key tiles with 3 S buffers 11.0; 48-key tiles at 4 CTAs/SM 11.1-11.7; one CTA/SM
@@ -532,8 +536,8 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
 #undef X
-  if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0, 1>(tmQ, tmKV, a, num_sms, stream);
-  if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0, 1>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 80) return launch_v<80, 64, 3, 2, 2, 1, 0, 0, 0>(tmQ, tmKV, a, num_sms, stream);
+  if (head_dim == 16) return launch_v<16, 96, 4, 2, 2, 1, 6, 0, 0>(tmQ, tmKV, a, num_sms, stream);
   return (int)cudaErrorInvalidValue;
 }
 

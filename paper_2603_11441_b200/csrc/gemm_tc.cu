@@ -66,16 +66,18 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMa
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1)
       : "memory");
 }
+// Issued by the converged MMA warp: one elected lane (see umma_f16_w in common.cuh).
 template <int CG>
 __device__ __forceinline__ void umma_f16_cg(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   if constexpr (CG == 1) {
-    umma_f16(tmem_d, a_desc, b_desc, idesc, accumulate);
+    umma_f16_w(tmem_d, a_desc, b_desc, idesc, accumulate);
   } else {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
   }
 }
@@ -83,10 +85,12 @@ __device__ __forceinline__ void umma_f16_cg(uint32_t tmem_d, uint64_t a_desc, ui
 template <int CG>
 __device__ __forceinline__ void umma_commit_cg(uint64_t* bar) {
   if constexpr (CG == 1) {
-    umma_commit(bar);
+    umma_commit_w(bar);
   } else {
     asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
             smem_u32(bar)),
         "h"((uint16_t)3)
         : "memory");
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // the whole (converged) warp runs the issue loop; one elected lane issues
       constexpr uint32_t idesc_full = umma_idesc_f16(BM * CG, BN);
       constexpr uint32_t idesc_half = umma_idesc_f16(BM * CG, BN / 2);
       int stage = 0;
