@@ -137,6 +137,11 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
               int32_t rope_cols, void* stream);
 void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
 void dart_gemm_force_plan(int32_t bn, int32_t cg);
+/* Fused enc-dec MLP (reference _mlp_forward, model.py:505-508, d = 256, hidden 1024):
+ * x[M, 256] += relu(h W1^T + b1) W2^T + b2, h fp16 [M, 256], W1 fp16 [1024, 256], W2 fp16 [256, 1024]
+ * (both [out, in]), x fp32; the hidden activations never leave the SM (TMEM). */
+int dart_mlp_fused(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x, int32_t M,
+                   void* stream);
 /* y = LayerNorm(x) per row (population variance, eps 1e-6; reference tensors.py:215-227), fp32 in,
  * fp16 (out_f16 = 1) or fp32 out; dim in {32, 64, 128, 256, 512, 1024, 1280}. */
 int dart_layernorm(const float* x, const float* gamma, const float* beta, void* y, int32_t rows, int32_t dim,

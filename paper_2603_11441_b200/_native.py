@@ -37,6 +37,7 @@ EXPORTS = (
     "dart_gemm_plan",
     "dart_gemm_force_plan",
     "dart_layernorm",
+    "dart_mlp_fused",
     "dart_gemm_force_splitk",
     "dart_attention_force_safe",
     "dart_attention_trace",
@@ -125,6 +126,8 @@ def load() -> ctypes.CDLL:
     lib.dart_gemm_force_plan.restype = None
     lib.dart_layernorm.argtypes = [P, P, P, P, I32, I32, I32, P]
     lib.dart_layernorm.restype = ctypes.c_int
+    lib.dart_mlp_fused.argtypes = [P, P, P, P, P, P, I32, P]
+    lib.dart_mlp_fused.restype = ctypes.c_int
     lib.dart_gemm_force_splitk.argtypes = [I32]
     lib.dart_gemm_force_splitk.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,

@@ -526,6 +526,278 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused enc-dec MLP (reference _mlp_forward, model.py:505-508, inside _encdec_single :519/:527):
+//   x += relu(h W1 + b1) W2 + b2      h [M, 256] fp16, hidden 1024, x [M, 256] fp32 residual
+// on a CTA pair (256-row units).  The hidden activations never leave the SM: fc1 runs in eight
+// 128-unit slices into two ping-pong TMEM regions, the epilogue warps turn each slice into
+// relu(. + b1) fp16 packed in place (the A operand of the TS-form fc2 MMA), and fc2 accumulates
+// all eight slices into a 256-column fp32 accumulator that the residual epilogue adds to x.
+// TMEM per CTA: [0,128) / [128,256) fc1 slices, [256,512) fc2.  P of a slice: hidden units 64h..64h+63
+// packed into columns [64h, 64h+32) of the slice (written by the warp that read those columns).
+// The MMA order fc1(0) fc1(1) fc2(0) fc1(2) fc2(1) ... fc1(7) fc2(6) fc2(7) lets the conversion of
+// slice e overlap fc1(e+1); an in-order tensor pipe guarantees fc2(e) has read P(e) before
+// fc1(e+2) overwrites the region.
+namespace mlpf {
+constexpr int D = 256, HID = 1024, SL = 128, NSL = HID / SL;  // model dims, hidden slice, slices
+constexpr int A_BYTES = BM * D * 2;                            // resident h rows of this CTA (64 KB)
+constexpr int RING_BYTES = 16384;                              // one W1 (8 KB) or W2 (16 KB) k-block
+constexpr int STAGES = 6;
+constexpr int OFF_RING = A_BYTES;
+constexpr int OFF_EPI = OFF_RING + STAGES * RING_BYTES;
+constexpr int OFF_BAR = OFF_EPI + 16 * 4096;
+constexpr int TOTAL = OFF_BAR + 512 + 1024;
+static_assert(TOTAL <= 227 * 1024, "shared memory budget");
+}  // namespace mlpf
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    mlp_fused_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
+                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmX, int M,
+                     const float* __restrict__ b1, const float* __restrict__ b2) {
+  using namespace mlpf;
+  constexpr int CG = 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* a_full = empty + STAGES;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* s_full = a_empty + 1;   // [2] fc1 slice accumulated
+  uint64_t* p_full = s_full + 2;    // [2] slice converted to P (8 epilogue warps x 2 CTAs)
+  uint64_t* o_full = p_full + 2;    // fc2 accumulator complete
+  uint64_t* o_empty = o_full + 1;   // fc2 accumulator drained by the residual epilogue
+  uint64_t* rfull = o_empty + 1;    // [8 warps][2] residual chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 16);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int rank = (int)cluster_ctarank();
+  const int cl = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int num_units = (M + BM * CG - 1) / (BM * CG);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmH);
+    tma_prefetch_desc(&tmW1);
+    tma_prefetch_desc(&tmW2);
+    tma_prefetch_desc(&tmX);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8 * CG);
+    }
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 8 * CG);
+    for (int i = 0; i < 16; ++i) mbar_init(&rfull[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_cg<512, CG>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // Ring sequence per unit: W1(0) W1(1) W2(0) W1(2) W2(1) ... W1(7) W2(6) W2(7); W1(e) = 4 k-blocks
+  // (K = 256), W2(e) = 2 k-blocks (K = 128 hidden units of slice e).
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      auto ring = [&](const CUtensorMap* map, int c0, int c1, uint32_t bytes) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+        tma_load_2d_cg2(smem + OFF_RING + stage * RING_BYTES, map, &full[stage], c0, c1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+        const int m0 = unit * BM * CG + rank * BM;
+        mbar_wait(a_empty, (it & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(a_full, 2 * A_BYTES);
+        for (int kb = 0; kb < D / BK; ++kb) tma_load_2d_cg2(smem + kb * (BM * BK * 2), &tmH, a_full, kb * BK, m0);
+        auto w1 = [&](int e) {
+          for (int kb = 0; kb < D / BK; ++kb) ring(&tmW1, kb * BK, e * SL + rank * (SL / 2), (SL / 2) * BK * 2);
+        };
+        auto w2 = [&](int e) {
+          for (int kb = 0; kb < SL / BK; ++kb) ring(&tmW2, e * SL + kb * BK, rank * (D / 2), (D / 2) * BK * 2);
+        };
+        w1(0);
+        for (int e = 1; e < NSL; ++e) {
+          w1(e);
+          w2(e - 1);
+        }
+        w2(NSL - 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // converged warp, one elected lane issues
+      constexpr uint32_t idesc1 = umma_idesc_f16(BM * CG, SL);
+      constexpr uint32_t idesc2 = umma_idesc_f16(BM * CG, D);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      auto next = [&]() {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        return smem_u32(smem + OFF_RING + stage * RING_BYTES);
+      };
+      auto release = [&]() {
+        umma_commit_cg<CG>(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+        mbar_wait(a_full, it & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(smem);
+        auto fc1 = [&](int e) {  // slice e -> TMEM region e & 1
+          for (int kb = 0; kb < D / BK; ++kb) {
+            const uint64_t da = umma_desc_sw128(a0 + kb * (BM * BK * 2)), db = umma_desc_sw128(next());
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_f16_cg<CG>(tmem + (e & 1) * SL, da + 2 * k, db + 2 * k, idesc1, (kb | k) != 0);
+            release();
+          }
+          umma_commit_cg<CG>(&s_full[e & 1]);
+          if (e == NSL - 1) umma_commit_cg<CG>(a_empty);
+        };
+        auto fc2 = [&](int e) {  // A = P(e) (fp16 packed in region e & 1), accumulate into [256, 512)
+          const int use = it * (NSL / 2) + (e >> 1);  // uses of region e & 1 so far
+          mbar_wait(&p_full[e & 1], use & 1);
+          if (e == 0) mbar_wait(o_empty, (it & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < SL / BK; ++kb) {
+            const uint64_t db = umma_desc_sw128(next());
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // P of hidden units [64 kb + 16 k, +16) sits at columns 64 kb + 8 k (each epilogue warp
+              // packs its 64 units into the first half of its own 64 columns)
+              const uint32_t pa = tmem + (e & 1) * SL + kb * 64 + k * 8;
+              if constexpr (CG == 2) {
+                asm volatile(
+                    "{\n\t.reg .pred p, el;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "elect.sync _|el, 0xffffffff;\n\t"
+                    "@el tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                    "r"(pa), "l"(db + 2 * k), "r"(idesc2), "r"((e | kb | k) != 0 ? 1u : 0u));
+              }
+            }
+            release();
+          }
+          if (e == NSL - 1) umma_commit_cg<CG>(o_full);
+        };
+        fc1(0);
+        for (int e = 1; e < NSL; ++e) {
+          fc1(e);
+          fc2(e - 1);
+        }
+        fc2(NSL - 1);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    float* bufs = reinterpret_cast<float*>(smem + OFF_EPI) + (warp - 4) * 2048;
+    uint64_t* rbar = rfull + (warp - 4) * 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    int it = 0, g = 0;  // g: residual chunks processed by this warp
+    for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+      const int row0 = unit * BM * CG + rank * BM + quarter * 32;
+      // residual chunk 0 of this unit, prefetched while the slices are converted
+      auto resid_load = [&](int chunk, int gg) {
+        mbar_arrive_expect_tx(&rbar[gg & 1], 32 * 32 * 4);
+        tma_load_2d(bufs + (gg & 1) * 1024, &tmX, &rbar[gg & 1], (chunk * 2 + half) * 32, row0);
+      };
+      if (lane == 0) {
+        bulk_wait_read0();
+        resid_load(0, g);
+      }
+      // slices: relu(acc + b1) -> fp16 pairs written over the slice's first half (own columns)
+      for (int e = 0; e < NSL; ++e) {
+        const int use = it * (NSL / 2) + (e >> 1);
+        mbar_wait(&s_full[e & 1], use & 1);
+        tc_fence_after();
+        const uint32_t rb = lane_base + (e & 1) * SL;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {  // this warp: hidden units [64 * half, 64 * half + 64) of the slice
+          const int col = half * 64 + c * 32;
+          float v[32];
+          tmem_ld32(rb + col, v);
+          tmem_ld_wait();
+          const float4* bb = reinterpret_cast<const float4*>(b1 + e * SL + col);
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 bq = __ldg(bb + q);
+            pk[2 * q] = pack_half2(fmaxf(v[4 * q] + bq.x, 0.f), fmaxf(v[4 * q + 1] + bq.y, 0.f));
+            pk[2 * q + 1] = pack_half2(fmaxf(v[4 * q + 2] + bq.z, 0.f), fmaxf(v[4 * q + 3] + bq.w, 0.f));
+          }
+          tmem_st16(rb + half * 64 + c * 16, pk);  // packed P of units [col, col+32): own columns only
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&p_full[e & 1]);
+      }
+      // residual epilogue: x += acc2 + b2 (this warp: 32-column chunks half, half + 2, ...)
+      mbar_wait(o_full, it & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c, ++g) {
+        const int col = (c * 2 + half) * 32;
+        float* buf = bufs + (g & 1) * 1024;
+        if (lane == 0 && c < 3) {
+          bulk_wait_read0();
+          resid_load(c + 1, g + 1);
+        }
+        __syncwarp();
+        float v[32];
+        tmem_ld32(lane_base + 256 + col, v);
+        tmem_ld_wait();
+        if (c == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(o_empty);
+        }
+        const float4* bb = reinterpret_cast<const float4*>(b2 + col);
+        mbar_wait(&rbar[g & 1], (g >> 1) & 1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 bq = __ldg(bb + q);
+          float4* sp = slot32(buf, lane, q);
+          float4 x = *sp;
+          x.x += v[4 * q] + bq.x;
+          x.y += v[4 * q + 1] + bq.y;
+          x.z += v[4 * q + 2] + bq.z;
+          x.w += v[4 * q + 3] + bq.w;
+          *sp = x;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmX, buf, col, row0);
+          tma_store_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_cg<512, CG>(tmem);
+  }
+}
+
 template <int BN, int STAGES, int EPI, int CG>
 int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
@@ -603,6 +875,33 @@ double env_or(const char* n, double d) {
 double g_eff192 = env_or("DART_GEMM_EFF192", 0.80), g_eff160 = env_or("DART_GEMM_EFF160", 0.70);  // measured: 192 and 160 lose to 256 on every DART shape
 
 }  // namespace
+
+int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX, int M,
+              const float* b1, const float* b2, int num_sms, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mlpf::TOTAL);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  const int units = (M + 255) / 256, pairs = num_sms / 2;
+  const int grid = (units < pairs ? units : pairs) * 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = mlpf::TOTAL;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_fused_kernel, tH, tW1, tW2, tX, M, b1, b2);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaGetLastError();
+}
 
 int gemm_bn_for(int N) {
   if (N % 256 == 0) return 256;

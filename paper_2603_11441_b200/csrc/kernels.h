@@ -73,6 +73,12 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2
             const CUtensorMap* tD, int M, int N, int K, GemmPlan plan, int epi_mode, const GemmEpi& epi, int num_sms,
             cudaStream_t stream);
 
+// Fused enc-dec MLP: x[M,256] += relu(h W1^T + b1) W2^T + b2 with W1 [1024, 256], W2 [256, 1024]
+// fp16 K-major, hidden activations kept in TMEM.  tH: box {64, 128} over h [M, 256];
+// tW1: box {64, 64} over W1; tW2: box {64, 128} over W2; tX: fp32 box {32, 32} 128B swizzle over x.
+int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX, int M,
+              const float* b1, const float* b2, int num_sms, cudaStream_t stream);
+
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {
   const __half* q;

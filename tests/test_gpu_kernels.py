@@ -319,3 +319,23 @@ def test_layernorm(lib, rows, dim, f16):
     torch.cuda.synchronize()
     ref = torch.nn.functional.layer_norm(x, (dim,), gamma, beta, eps=1e-6)
     assert float((y.float() - ref).abs().max()) < (1e-2 if f16 else 1e-4)
+
+
+@pytest.mark.parametrize("M", [300, 5184, 20736, 41472 + 77])
+def test_mlp_fused(lib, M):
+    """Fused enc-dec MLP (hidden activations in TMEM): x += relu(h W1^T + b1) W2^T + b2 vs fp32 torch
+    with the same fp16 rounding of h, the weights and the hidden activations."""
+    g = torch.Generator(device="cuda").manual_seed(M)
+    h = torch.randn(M, 256, device="cuda", generator=g).half()
+    w1 = (torch.randn(1024, 256, device="cuda", generator=g) / 16).half()
+    w2 = (torch.randn(256, 1024, device="cuda", generator=g) / 32).half()
+    b1 = torch.randn(1024, device="cuda", generator=g) * 0.1
+    b2 = torch.randn(256, device="cuda", generator=g) * 0.1
+    x = torch.randn(M, 256, device="cuda", generator=g)
+    hid = torch.relu(h.float() @ w1.float().T + b1).half().float()
+    ref = x + hid @ w2.float().T + b2
+    out = x.clone()
+    _native.check(lib.dart_mlp_fused(h.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                                     out.data_ptr(), M, stream()))
+    torch.cuda.synchronize()
+    assert rel_err(out, ref) < 2e-3
