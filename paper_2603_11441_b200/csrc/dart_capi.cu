@@ -162,6 +162,7 @@ struct LNW {
 };
 struct AttnW {
   GemmW q, kv, out;
+  GemmW qkv;  // self-attention: [q | kv] rows in one [3d, d] weight (one GEMM reads LN1(x) once)
 };
 struct BlockW {
   LNW ln1, ln2;
@@ -343,6 +344,17 @@ bool make_attn(dart_model* m, WeightCursor& c, int d, float* scratch, AttnW& a, 
     if (!a.kv.w || !upload_wT(m, kvw, d, 2 * d, a.kv.w, d, 0, scratch)) return false;
     a.kv.b = upload_f32(m, kvb, 2 * d);
     if (!a.kv.b || !finish_gemmw(a.kv)) return false;
+    // fused self-attention projection: rows [0, d) = q, [d, 3d) = k | v
+    a.qkv.N = 3 * d;
+    a.qkv.K = d;
+    a.qkv.w = dev_alloc<__half>(m, (size_t)3 * d * d);
+    a.qkv.b = dev_alloc<float>(m, 3 * d);
+    if (!a.qkv.w || !a.qkv.b) return false;
+    if (cudaMemcpy(a.qkv.w, a.q.w, (size_t)d * d * 2, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(a.qkv.w + (size_t)d * d, a.kv.w, (size_t)2 * d * d * 2, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(a.qkv.b, a.q.b, d * 4, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(a.qkv.b + d, a.kv.b, 2 * d * 4, cudaMemcpyDeviceToDevice) != cudaSuccess || !finish_gemmw(a.qkv))
+      return false;
   }
   return make_gemm(m, c, d, d, scratch, a.out);
 }
@@ -488,7 +500,7 @@ int ensure_encdec_ws(dart_model* m, int B, int N) {
   e.e = (float*)w.get(rows * D * 4);
   e.h = (__half*)w.get(rows * D * 2);
   e.q = (__half*)w.get(rows * D * 2);
-  e.kv = (__half*)w.get(rows * 2 * D * 2);
+  e.kv = (__half*)w.get(rows * 3 * D * 2);  // self-attention [q | k | v]
   e.o = (__half*)w.get(rows * D * 2);
   e.hid = (__half*)w.get(rows * 4 * D * 2);
   e.dkv = (__half*)w.get(rows * nd * 2 * D * 2);
@@ -499,7 +511,7 @@ int ensure_encdec_ws(dart_model* m, int B, int N) {
   e.qf = (float*)w.get(drows * D * 4);
   e.dh = (__half*)w.get(drows * D * 2);
   e.dq = (__half*)w.get(drows * D * 2);
-  e.dkvs = (__half*)w.get(drows * 2 * D * 2);
+  e.dkvs = (__half*)w.get(drows * 3 * D * 2);
   e.do_ = (__half*)w.get(drows * D * 2);
   e.dhid = (__half*)w.get(drows * 4 * D * 2);
   void* all[] = {e.e1, e.l0h, e.e, e.h, e.q, e.kv, e.o, e.hid, e.dkv, e.text, e.tkv, e.qd0, e.qd, e.qf,
@@ -530,8 +542,29 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
   const int D = m->D, H = m->H, hd = D / H;
   const int rows = sp.items * sp.Lq;
   LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
-  RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
   const int Lk = sp.kv16 == nullptr ? sp.Lq : sp.Lk;
+  if (sp.kv16 == nullptr && w.qkv.w) {  // self-attention: one [q | k | v] GEMM into kv (3D wide)
+    RUN(gemm(m, h, rows, D, w.qkv, EPI_F16, epi_out(kv, 3 * D), s));
+    if (tc_attention_enabled() && attention_tc_supported(hd, Lk)) {
+      m->launches++;
+      RUN(attn_tc(kv, 3 * D, 0, kv, 3 * D, D, 2 * D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
+    } else {
+      AttnArgs a = attn_base(H, hd);
+      a.q = kv;
+      a.k = kv + D;
+      a.v = kv + 2 * D;
+      a.q_tok_stride = a.k_tok_stride = a.v_tok_stride = 3 * D;
+      a.q_batch_stride = a.k_batch_stride = a.v_batch_stride = (long long)sp.Lq * 3 * D;
+      a.o = o;
+      a.o_tok_stride = D;
+      a.o_batch_stride = (long long)sp.Lq * D;
+      a.Lq = a.Lk = sp.Lq;
+      a.batch = sp.items;
+      RUN(attn(m, a, hd, s));
+    }
+    return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+  }
+  RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
   if (tc_attention_enabled() && sp.kv_mod == 0 && attention_tc_supported(hd, Lk) &&
       (sp.kv16 == nullptr || sp.kv_batch_stride == (long long)Lk * sp.kv_tok_stride)) {
     // tcgen05 path: encoder self-attention (T x T) and decoder cross-attention (201 x T)
