@@ -163,9 +163,9 @@ int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32_t heads, i
 /* Tests: on != 0 makes every later tcgen05 attention launch re-run all of its items through the
  * max-tracking softmax pass (the path items take when the fixed-reference pass overflows). */
 void dart_attention_force_safe(int32_t on);
-/* Microbenchmarks: device int64[7 * 256] receiving CTA 0's clock64 stamps of its first 256 key
+/* Microbenchmarks: device int64[11 * 256] receiving CTA 0's clock64 stamps of its first 256 key
  * tiles (S ready, P written, P seen by the MMA issuer, MMAs issued, V ready, P.V issued, next K
- * ready); NULL disables. */
+ * ready, then P done per softmax warp 2..5); NULL disables. */
 void dart_attention_trace(int64_t* device_buf);
 /* Microbenchmarks: select the tcgen05 attention kernel variant (0 = production). */
 void dart_attention_variant(int32_t v);

@@ -393,7 +393,10 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           __syncwarp();
           if (lane == 0 && a.softmax_only != 1) mbar_arrive(&p_full[sb]);
           if (pass == 1) ++s_g1;
-          if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[256 + s_g] = clock64();
+          if (a.trace && blockIdx.x == 0 && lane == 0 && s_g < 256) {
+            if (warp == 2) a.trace[256 + s_g] = clock64();
+            a.trace[1792 + (warp - 2) * 256 + s_g] = clock64();  // P done, per softmax warp
+          }
         }
         // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
         // part, part + SPLIT, ...

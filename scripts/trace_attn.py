@@ -16,15 +16,20 @@ items, L, H = (4, 5184, 16) if hd == 16 else (1, 5184, 16)
 E = H * hd
 qkv = torch.randn(items * L, 3 * E, device="cuda").half()
 o = torch.empty(items * L, E, device="cuda", dtype=torch.float16)
-tr = torch.zeros(7 * 256, dtype=torch.int64, device="cuda")
+tr = torch.zeros(11 * 256, dtype=torch.int64, device="cuda")
 run = lambda: _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, st.cuda_stream))
 run()
 lib.dart_attention_trace(tr.data_ptr())
 run()
 torch.cuda.synchronize()
 lib.dart_attention_trace(None)
-t = tr.cpu().numpy().reshape(7, 256).astype(np.int64)
-s_ready, p_done, p_seen, issued, v_ok, pv_issued, k_ok = t
+t = tr.cpu().numpy().reshape(11, 256).astype(np.int64)
+s_ready, p_done, p_seen, issued, v_ok, pv_issued, k_ok = t[:7]
+pw = t[7:11]  # P done per softmax warp 2..5
+if pw.any():
+    print("per-warp P-done minus warp 2 (warps 3, 4, 5), tiles 10..30:")
+    for g in range(10, 30):
+        print(g, [int(pw[w][g] - pw[0][g]) for w in (1, 2, 3)])
 base = s_ready[0]
 print("tile  S_ready  P_done(soft)  P_seen(mma)  issued   | soft_work  mma_react  issue  S_gap")
 for g in range(1, 40):
