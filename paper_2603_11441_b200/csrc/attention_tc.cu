@@ -116,6 +116,11 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   const int q_tiles = (a.Lq + BQ - 1) / BQ;
   const int n_items = q_tiles * a.heads * a.items;
   const int nkv = a.Lkv / BKV;
+  // TMA and MMA warps (SMSPs 0 / 1).  The tcgen05.mma stream costs its SMSP issue time, which the
+  // softmax warp sharing that SMSP loses; the second CTA of an SM (blocks are placed round-robin,
+  // so blockIdx >= grid/2) swaps the two roles to put its MMA issue on the other SMSP.
+  const bool swap_roles = (int)blockIdx.x * 2 >= (int)gridDim.x;
+  const int w_load = swap_roles ? 1 : 0, w_mma = swap_roles ? 0 : 1;
 
   if (warp == 1 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
     auto todo = [&](int local) {
       return pass == 0 || a.force_safe || ((ovf[local >> 5] >> (local & 31)) & 1u);
     };
-    if (warp == 0) {
+    if (warp == w_load) {
       if (lane < (LEAN ? 2 : 1) && a.softmax_only != 1) {
         const bool do_qk = lane == 0, do_v = !LEAN || lane == 1;
         int local = 0;
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         }
       }
       __syncwarp();
-    } else if (warp == 1) {
+    } else if (warp == w_mma) {
       if (a.softmax_only != 1) {  // the whole warp runs the issue loop (converged); one lane issues
         constexpr uint32_t idesc_s = umma_idesc_f16(BQ, BKV);
         constexpr uint32_t idesc_pv = umma_idesc_f16(BQ, L::ON) | (1u << 16);  // B (V) MN-major
