@@ -41,8 +41,10 @@ struct GemmSmem {
   // staging buffers per epilogue warp; 4 for the residual epilogue (3 chunks prefetched) measured
   // slower: the extra 64 KB costs two operand stages (out-proj 24.8 -> 27.1 us, fc2 63.4 -> 80 us)
   static constexpr int NBUF = 2;
-  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x NBUF staging buffers of 4 KB (32x32 fp32)
-  static constexpr int ROPE_OFF = EPI_OFF + 8 * NBUF * 4096;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
+  // staging buffer per chunk: 32x32 fp32 (4 KB), or 32x32 fp16 (2 KB) for the fp16-only epilogues
+  static constexpr int BUF_BYTES = (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) ? 2048 : 4096;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x NBUF staging buffers
+  static constexpr int ROPE_OFF = EPI_OFF + 8 * NBUF * BUF_BYTES;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
   static constexpr int ROPE_BYTES = EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0;
   static constexpr int BAR_OFF = ROPE_OFF + ROPE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + 1 KB alignment slack
@@ -383,7 +385,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     constexpr int NBUF = L::NBUF;
-    float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * NBUF * 1024;  // NBUF x 4 KB per warp
+    constexpr int BUF_F = L::BUF_BYTES / 4;  // staging buffer size in floats
+    float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * NBUF * BUF_F;
     uint64_t* rbar = rfull + (warp - 4) * NBUF;
     const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
     // residual chunk g of this warp -> smem buffer g % NBUF (lane 0 issues; NBUF-1 chunks ahead)
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
       const int cc = (t % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0) + (pf_c * 2 + half) * 32;
       mbar_arrive_expect_tx(&rbar[g % NBUF], 32 * 32 * 4);
-      tma_load_2d(bufs + (g % NBUF) * 1024, &tmC, &rbar[g % NBUF], cc, rr);
+      tma_load_2d(bufs + (g % NBUF) * BUF_F, &tmC, &rbar[g % NBUF], cc, rr);
       if (++pf_c == (bne - half * 32 + 63) / 64) {
         pf_c = 0;
         pf_u += ncl;
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
 #pragma unroll 1
       for (int c = half * 32; c < bn_eff; c += 64, ++g) {
-        float* buf = bufs + (g % NBUF) * 1024;
+        float* buf = bufs + (g % NBUF) * BUF_F;
         if (lane == 0) {
           if (RESID) {
             bulk_wait_read0();  // store g-1 has read buffer (g-1) % NBUF = (g+NBUF-1) % NBUF
@@ -837,7 +840,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
 template <int BN, int EPI, int CG>
 constexpr int stages_for() {
   constexpr int stage = BM * BK * 2 + (BN / CG) * BK * 2;
-  constexpr int fixed = 8 * 2 * 4096 +
+  constexpr int fixed = 8 * 2 * ((EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) ? 2048 : 4096) +
                         (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) + 512 + 1024;
   constexpr int n = (227 * 1024 - fixed) / stage;
   return n > 8 ? 8 : n;
