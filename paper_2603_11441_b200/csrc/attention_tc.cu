@@ -10,16 +10,27 @@
 //              and K / V tiles of BKV keys in a STAGES-deep ring with separate K and V
 //              barriers (K is released as soon as S = QK^T has consumed it).  Operands are
 //              16-dim column blocks with 32-byte swizzle.
-//   warp 1     MMA issuer (one thread):  S_j = Q K_j^T -> TMEM (double buffered, BKV cols)
+//   warp 1     MMA issuer (whole warp, elect.sync inside each issue so the descriptors stay
+//              warp-uniform):        S_j = Q K_j^T -> TMEM (NS-buffered, BKV cols)
 //                                        O  += P_j [V_j | 1]  (A = P read from TMEM, B = V in
 //                                        smem, MN-major; the ones block makes column HD of O
 //                                        the softmax row sum on the tensor core)
+//              The second half of the grid swaps the TMA and MMA warps (warp 0 <-> 1) so
+//              the two CTAs on an SM put their MMA issuers on different SM sub-partitions.
 //   warps 2-5  softmax: one thread per query row (TMEM lane quarter = warp & 3).  The whole
-//              S tile is loaded into registers once, row max by an 8-way max3 tree, P = 2^x of
-//              the FFMA-scaled scores written back over S as packed fp16.  NPOLY of every 16
-//              exponentials run as a degree-3 polynomial on the FMA pipe (exp2_poly) instead of
-//              MUFU, balancing the two pipes (MUFU = 16/clk/SM is the hd-16 roof).  O is
-//              rescaled lazily, only when the running max grows by more than 2^8 (P <= 256).
+//              S tile is loaded into registers once and P = 2^x of the FFMA-scaled scores is
+//              written back over S as packed fp16.
+//              Pass 0 (every item): fixed-reference softmax -- the reference max m is the row
+//              max of the FIRST key tile only (8-way max3 tree), later tiles are exponentiated
+//              against it with no max tracking and no O rescale.  NPOLY of every 16
+//              exponentials run as a saturating degree-3 polynomial on the FMA pipe
+//              (exp2_poly2_sat) instead of MUFU, balancing the two pipes (MUFU = 16/clk/SM is
+//              the hd-16 roof).  A later score more than 2^16 above m overflows the fp16 P to
+//              inf; the epilogue sees a non-finite row sum and flags the item in the smem
+//              overflow bitmask instead of storing a wrong row.
+//              Pass 1 (flagged items only, or all with force_safe): max-tracking softmax that
+//              rescales O whenever the running max grows by more than 2^8 (P <= 256), MUFU
+//              exponentials only.  Both passes give softmax(x) exactly up to fp16 rounding of P.
 #include "common.cuh"
 #include "kernels.h"
 
