@@ -66,6 +66,19 @@ int dart_model_create(const dart_model_desc* desc, const float* const* weights, 
 int dart_model_fork(const dart_model* parent, dart_model** out);
 void dart_model_destroy(dart_model* m);
 
+/* Backbone arithmetic discipline of this handle (forks copy it), for the precision study
+ * (reference pipeline.py:318-367, tensors.py:111-170):
+ *   0  fp16 operands, fp32 tensor-core accumulation, fp32 residual stream (default, the
+ *      detection path);
+ *   1  fp16 storage: every backbone GEMM output and the residual stream after each add are
+ *      rounded to fp16 (the reference's FP16_ACCUM_FP32 storage discipline);
+ *   2  fp16 storage and fp16 accumulation on the tensor core (tcgen05 D format f16): the
+ *      FP16_ACCUM_FP16 negative control.
+ * Applies to the backbone's GEMMs (patch embed, QKV, out-proj, MLP, FPN); attention and the
+ * enc-dec keep fp32 accumulation.  DART_ERR_INVALID for other values. */
+int dart_model_set_precision(dart_model* m, int32_t precision);
+int32_t dart_model_get_precision(const dart_model* m);
+
 /* Number of parameter tensors dart_model_create expects for `desc`. */
 int32_t dart_expected_weight_count(const dart_model_desc* desc);
 
@@ -149,6 +162,9 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
 /* Tests: s = 2 makes later dart_gemm residual calls (epi 3, K/64 even) run split-K (two K halves
  * per tile on different CTA pairs, deterministic adds); s = 1 restores the default. */
 void dart_gemm_force_splitk(int32_t s);
+/* Tests: later dart_gemm calls use precision discipline p (see dart_model_set_precision:
+ * 1 fp16 storage, 2 fp16 storage + fp16 accumulation); 0 restores the default. */
+void dart_gemm_force_precision(int32_t p);
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,
                    int32_t Lk, int32_t hd, int32_t q_tok_stride, int32_t kv_tok_stride, int32_t o_tok_stride,
                    int64_t q_batch_stride, int64_t kv_batch_stride, int64_t o_batch_stride, int32_t win,

@@ -10,6 +10,7 @@ here, never on the GPU box.  The fixtures are what pins the oracle restatement
   A  SPEC toy profile (`toy_config(seed=0)`), 64^2, names car/person/dog (+8-class list)
   M  A with the mask head (mask_head_forward outputs)
   P  greedy sub-block pruning on A's model (plan + every round's candidate losses)
+  S  precision study on A's model (pipeline.py:342-367): mean L0 cosine per depth and half mode
   B  small-1008: full-width ViT-H/14 kernels at 4 blocks (globals 1,3), 6+6 enc-dec, 3 classes
   C  full ViT-H/14 DART 1008^2, 4 classes (person, car, dog, bicycle)
 
@@ -198,8 +199,34 @@ def make_prune(name: str, cfg, seeds, k: int):
     print(f"{name}: wrote {path}; plan {[(s.sub_block.block, s.sub_block.kind) for s in plan.steps]}")
 
 
+def make_study(name: str, cfg, seeds, depths):
+    """Precision-study golden: the reference's precision_study
+    (pipeline.py:342-367) -- mean level-0 cosine vs its FP32 path for FP16_ACCUM_FP32 and
+    FP16_ACCUM_FP16 at each truncation depth -- plus the FP32 level-0 features themselves."""
+    model = M.build_model(cfg, with_mask_head=False)
+    images = [generate_scene(SceneSpec(seed=s, num_classes=3))[0] for s in seeds]
+    rep = PL.precision_study(model, images, list(depths))
+    l0 = np.stack([np.stack([M.backbone_forward(M.truncate_model(model, d), img, FP32).levels[0] for img in images])
+                   for d in depths])
+    out = {
+        "config_json": np.array(json.dumps(cfg.to_dict())),
+        "weights_checksum": np.array(M.weights_checksum(model)),
+        "seeds": np.array(list(seeds)),
+        "depths": np.array(list(depths)),
+        "modes": np.array([m for _, m, _ in rep.rows]),
+        "cosines": np.array([[d, v] for d, _, v in rep.rows], dtype=np.float64),  # rows (depth, mean cosine)
+        "l0_fp32": l0.astype(np.float64),  # [depths, images, T, F0]
+    }
+    path = os.path.join(OUT, f"golden_{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: wrote {path}; rows {rep.rows}")
+
+
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "A"
+    if which == "S":
+        make_study("S", M.toy_config(seed=0), (21, 22, 23, 24, 25), (2, 4, 8))
+        return
     if which == "P":
         make_prune("P", M.toy_config(seed=0), (11, 12, 13), k=5)
         return

@@ -37,12 +37,14 @@ from .pipeline import (  # noqa: F401
     EmptyClassSetError,
     PipelineConfig,
     PipelineLevel,
+    PrecisionStudyReport,
     RunCounters,
     box_iou,
     chunk_count,
     detections_from_json,
     detections_to_json,
     postprocess,
+    precision_study,
     run_batched,
     run_batched_from_fpn,
     run_level,
@@ -50,4 +52,4 @@ from .pipeline import (  # noqa: F401
     run_shared,
 )
 from .scenes import SceneSpec, generate_scene, scene_images  # noqa: F401
-from .tensors import PrecisionMode, ShapeError  # noqa: F401
+from .tensors import PrecisionMode, ShapeError, cosine_similarity  # noqa: F401

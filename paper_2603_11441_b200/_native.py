@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdart_b200.so")
+# DART_LIB_PATH: A/B microbenchmarks of another build (the product path loads the in-tree library)
+LIB_PATH = os.environ.get("DART_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdart_b200.so")
 MAX_BLOCKS = 256
 
 DART_OK = 0
@@ -24,6 +25,8 @@ EXPORTS = (
     "dart_model_create",
     "dart_model_destroy",
     "dart_model_fork",
+    "dart_model_set_precision",
+    "dart_model_get_precision",
     "dart_expected_weight_count",
     "dart_backbone",
     "dart_backbone_embed",
@@ -39,6 +42,7 @@ EXPORTS = (
     "dart_layernorm",
     "dart_mlp_fused",
     "dart_gemm_force_splitk",
+    "dart_gemm_force_precision",
     "dart_attention_force_safe",
     "dart_attention_trace",
     "dart_attention_variant",
@@ -82,6 +86,26 @@ I32 = ctypes.c_int32
 F64 = ctypes.c_double
 
 
+class _Unbound:
+    """A symbol an older A/B build does not export: its binding is skipped."""
+
+    def __setattr__(self, key, value):
+        pass
+
+
+class _Tolerant:
+    """DART_LIB_PATH builds only: tolerate symbols added after that build."""
+
+    def __init__(self, lib):
+        object.__setattr__(self, "_lib", lib)
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._lib, name)
+        except AttributeError:
+            return _Unbound()
+
+
 def load() -> ctypes.CDLL:
     """Open the in-tree library once; raise if it was not built."""
     global _lib
@@ -93,6 +117,8 @@ def load() -> ctypes.CDLL:
             "(there is no CPU fallback for the DART B200 path)"
         )
     lib = ctypes.CDLL(LIB_PATH)
+    if os.environ.get("DART_LIB_PATH"):
+        lib = _Tolerant(lib)
     lib.dart_model_create.argtypes = [ctypes.POINTER(ModelDesc), ctypes.POINTER(ctypes.c_void_p), I32,
                                       ctypes.POINTER(ctypes.c_void_p)]
     lib.dart_model_create.restype = ctypes.c_int
@@ -100,6 +126,10 @@ def load() -> ctypes.CDLL:
     lib.dart_model_destroy.restype = None
     lib.dart_model_fork.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
     lib.dart_model_fork.restype = ctypes.c_int
+    lib.dart_model_set_precision.argtypes = [P, I32]
+    lib.dart_model_set_precision.restype = ctypes.c_int
+    lib.dart_model_get_precision.argtypes = [P]
+    lib.dart_model_get_precision.restype = I32
     lib.dart_expected_weight_count.argtypes = [ctypes.POINTER(ModelDesc)]
     lib.dart_expected_weight_count.restype = I32
     lib.dart_backbone.argtypes = [P, P, I32, P, P, P, P, P]
@@ -130,6 +160,8 @@ def load() -> ctypes.CDLL:
     lib.dart_mlp_fused.restype = ctypes.c_int
     lib.dart_gemm_force_splitk.argtypes = [I32]
     lib.dart_gemm_force_splitk.restype = None
+    lib.dart_gemm_force_precision.argtypes = [I32]
+    lib.dart_gemm_force_precision.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int64, I32, I32, P]
     lib.dart_attention.restype = ctypes.c_int

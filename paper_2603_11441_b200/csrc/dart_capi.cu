@@ -104,6 +104,7 @@ int g_attn_force_safe = 0;
 // epilogue waits behind half 0's), so opt-in (DART_SPLITK=1) for A/B measurement only
 int g_splitk_enabled = getenv("DART_SPLITK") != nullptr;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
+int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
 long long* g_attn_trace = nullptr;
 
@@ -254,6 +255,10 @@ struct dart_model {
     __half *l0h, *h, *q, *kv, *o, *hid, *dkv, *text, *tkv, *dh, *dq, *dkvs, *do_, *dhid;
   } ed{};
   int64_t launches = 0;
+  // backbone arithmetic discipline (dart_model_set_precision): 0 fp32 accumulate + fp32 residual,
+  // 1 fp16 storage (outputs and residual rounded to fp16), 2 fp16 storage + fp16 accumulation
+  int precision = 0;
+  bool in_backbone = false;  // set while a backbone stage issues its GEMMs
   int* splitk_flags = nullptr;  // per handle (a fork gets its own): split-K tile flags
   int splitk_cap = 0;
 
@@ -398,6 +403,10 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
   CUtensorMap ta;
   if (!make_tmap(&ta, A, W.K, M, lda, 128)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (A)");
   if (e.bias == nullptr) e.bias = W.b;
+  if (m->in_backbone && m->precision > 0) {
+    e.round_f16 = 1;
+    e.acc_f16 = m->precision == 2;
+  }
   m->launches++;
   CUtensorMap tc, td;
   if (!make_out_maps(epi, e, M, W.N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
@@ -637,7 +646,7 @@ int xmlp(dart_model* m, float* x, const LNW& ln, const GemmW& fc1, const GemmW& 
 extern "C" {
 
 const char* dart_last_error(void) { return g_last_error.c_str(); }
-const char* dart_version(void) { return "dart-b200 0.1 (sm_100a, tcgen05 GEMM + mma.sync flash attention)"; }
+const char* dart_version(void) { return "dart-b200 0.2 (sm_100a, tcgen05 GEMM + tcgen05 flash attention)"; }
 
 int32_t dart_expected_weight_count(const dart_model_desc* d) {
   if (!d) return -1;
@@ -776,6 +785,14 @@ int dart_model_fork(const dart_model* parent, dart_model** out) {
   return DART_OK;
 }
 
+int dart_model_set_precision(dart_model* m, int32_t precision) {
+  if (!m || precision < 0 || precision > 2) return fail(DART_ERR_INVALID, "dart_model_set_precision: precision must be 0, 1 or 2");
+  m->precision = precision;
+  return DART_OK;
+}
+
+int32_t dart_model_get_precision(const dart_model* m) { return m ? m->precision : -1; }
+
 int64_t dart_launch_count(const dart_model* m) { return m ? m->launches : 0; }
 void dart_reset_launch_count(dart_model* m) {
   if (m) m->launches = 0;
@@ -785,10 +802,18 @@ void dart_reset_launch_count(dart_model* m) {
 
 namespace {
 
+// Marks the GEMMs a backbone stage issues (they follow the handle's precision discipline).
+struct BackboneScope {
+  dart_model* m;
+  explicit BackboneScope(dart_model* mm) : m(mm) { m->in_backbone = true; }
+  ~BackboneScope() { m->in_backbone = false; }
+};
+
 // Backbone stages on a caller-chosen residual stream x [B*T, E] fp32 in window-major row order
 // (each 24x24 window a contiguous block; global attention, LN and the MLP are order-invariant,
 // the patchify / RoPE / FPN kernels map rows to tokens).
 int bb_embed(dart_model* m, const float* images, int B, float* x, int32_t* flags, cudaStream_t s) {
+  BackboneScope scope(m);
   auto& w = m->bb;
   const int rows = B * m->T, win = m->d.window_size;
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t), s) != cudaSuccess) return fail(DART_ERR_CUDA, "flags memset");
@@ -798,6 +823,7 @@ int bb_embed(dart_model* m, const float* images, int B, float* x, int32_t* flags
 
 int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* attn_on, const int32_t* mlp_on,
               cudaStream_t s) {
+  BackboneScope scope(m);
   const int T = m->T, E = m->E, H = m->H, hd = m->hd, G = m->G;
   const int rows = B * T;
   auto& w = m->bb;
@@ -853,6 +879,7 @@ int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* att
 
 // FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
 int bb_fpn(dart_model* m, const float* x, int B, float* l0, float* l1, float* l2, int32_t* flags, cudaStream_t s) {
+  BackboneScope scope(m);
   auto& w = m->bb;
   const int rows = B * m->T, E = m->E, G = m->G, win = m->d.window_size;
   LAUNCH(cast_f32_to_f16(x, w.h, (long long)rows * E, s));
@@ -1045,6 +1072,8 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.rope_hd = rope_hd > 0 ? rope_hd : 2;
   e.rope_cols = rope_cols;
   e.dbg_noload = getenv("DART_GEMM_NOLOAD") != nullptr;
+  e.round_f16 = g_gemm_precision > 0;
+  e.acc_f16 = g_gemm_precision == 2;
   CUtensorMap td;
   if (!make_out_maps(epi, e, M, N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
   if (g_gemm_splitk == 2 && epi == EPI_F32_RESID && (K / 64) % 2 == 0) {  // tests: split-K residual path
@@ -1084,6 +1113,7 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
   return DART_OK;
 }
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
+void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
 int dart_mlp_fused(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x, int32_t M,
                    void* stream) {

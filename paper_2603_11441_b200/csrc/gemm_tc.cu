@@ -141,6 +141,10 @@ __device__ __forceinline__ void rope_chunk(float* v, int col, int hd, const floa
   }
 }
 
+// fp16 storage rounding, saturating at +-65504 like the reference's half_round (tensors.py:99-109)
+__device__ __forceinline__ float sat_f16(float x) { return fminf(fmaxf(x, -65504.0f), 65504.0f); }
+__device__ __forceinline__ float round_f16(float x) { return __half2float(__float2half_rn(sat_f16(x))); }
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_bias_act(float* v, int col, const GemmEpi& e) {
   if (e.bias != nullptr) {
@@ -232,7 +236,9 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 constexpr int GEMM_THREADS = 384;
 
-template <int BN, int STAGES, int EPI, int CG>
+// PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
+// path's instantiations (PREC = false) carry none of that code.
+template <int BN, int STAGES, int EPI, int CG, bool PREC>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
@@ -336,8 +342,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (rank == 0) {  // the whole (converged) warp runs the issue loop; one elected lane issues
-      constexpr uint32_t idesc_full = umma_idesc_f16(BM * CG, BN);
-      constexpr uint32_t idesc_half = umma_idesc_f16(BM * CG, BN / 2);
+      const uint32_t dfmt = (PREC && epi.acc_f16) ? (1u << 4) : 0u;  // clear D = f32 -> f16 accumulator
+      const uint32_t idesc_full = umma_idesc_f16(BM * CG, BN) ^ dfmt;
+      const uint32_t idesc_half = umma_idesc_f16(BM * CG, BN / 2) ^ dfmt;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -451,6 +458,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
+        if ((PREC && epi.acc_f16)) {  // f16 accumulator: one value per 32-bit TMEM cell, low half
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            v[j] = __half2float(__ushort_as_half((unsigned short)(__float_as_uint(v[j]) & 0xFFFFu)));
+        }
         if (c + 64 >= bn_eff) {
           // all of this warp's accumulator columns are in registers: hand TMEM back early
           tc_fence_before();
@@ -465,6 +477,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         if (kh == 0) epilogue_bias_act<EPI>(v, n0 + c, epi);  // split-K: bias once (half 0)
         if (EPI == EPI_QKV_ROPE && n0 + c < epi.rope_cols) rope_chunk(v, n0 + c, epi.rope_hd, rt, ct);
+        if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (EPI == EPI_F32 || EPI == EPI_F32_F16) ? round_f16(v[j]) : sat_f16(v[j]);
+        }
         if ((EPI == EPI_F32 && epi.wm_scatter) || EPI == EPI_F32_F16) {  // row scatter / 2 outputs: plain stores
           chunk_store_f32(buf, v, reinterpret_cast<float*>(epi.out), epi.ldo, row0, n0 + c, M, epi);
           if (EPI == EPI_F32_F16)
@@ -481,6 +497,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             x.y += v[4 * q + 1];
             x.z += v[4 * q + 2];
             x.w += v[4 * q + 3];
+            if ((PREC && epi.round_f16)) x = make_float4(round_f16(x.x), round_f16(x.y), round_f16(x.z), round_f16(x.w));
             *sp = x;
           }
         } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_F16) {
@@ -801,11 +818,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BN, int STAGES, int EPI, int CG>
+template <int BN, int STAGES, int EPI, int CG, bool PREC>
 int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES, EPI, CG>;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG, PREC>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
@@ -849,7 +866,9 @@ constexpr int stages_for() {
 template <int BN, int EPI, int CG>
 int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
                    const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
-  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+  if (epi.acc_f16 || epi.round_f16)
+    return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG, true>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
 }
 
 template <int BN, int CG>

@@ -44,6 +44,12 @@ struct GemmEpi {
   // Tail halves: the first tail_full tiles (a whole number of waves) run as BN-wide units, the
   // remaining tiles as two BN/2-wide units each, so the last wave is half as long (0 = off).
   int tail_full = 0;
+  // Precision-study disciplines (reference tensors.py:111-170):
+  // acc_f16 = 1 accumulates in fp16 on the tensor core (D format f16 in TMEM, the negative
+  // control); round_f16 = 1 rounds every fp32 output (and the residual stream after the add)
+  // to fp16-representable values (fp16 storage).
+  int acc_f16 = 0;
+  int round_f16 = 0;
 };
 
 // window-major row index <-> token index within one image

@@ -21,7 +21,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from . import _native
-from .tensors import PrecisionMode, device_mode
+from .tensors import PrecisionMode, device_mode, precision_code
 
 LN_EPS = 1e-6
 TEXT_TABLE_ROWS = 1024
@@ -425,7 +425,7 @@ def backbone_forward_batch(model: DetectorModel, images, mode: PrecisionMode = P
     the device status flags.  `check=True` synchronises and raises like the reference."""
     import torch
 
-    device_mode(mode)
+    code = precision_code(mode)
     cfg = model.config
     dev = _device()
     h = native_handle(model, dev)
@@ -443,8 +443,12 @@ def backbone_forward_batch(model: DetectorModel, images, mode: PrecisionMode = P
     l1 = torch.empty((B, (g // 2) ** 2, cfg.fpn_dims[1]), device=dev, dtype=torch.float32)
     l2 = torch.empty((B, (g // 4) ** 2, cfg.fpn_dims[2]), device=dev, dtype=torch.float32)
     flags = torch.zeros((1,), device=dev, dtype=torch.int32)
-    _native.check(h.lib.dart_backbone(h.ptr, imgs.data_ptr(), B, l0.data_ptr(), l1.data_ptr(), l2.data_ptr(),
-                                      flags.data_ptr(), _stream_ptr(dev)))
+    _native.check(h.lib.dart_model_set_precision(h.ptr, code))
+    try:
+        _native.check(h.lib.dart_backbone(h.ptr, imgs.data_ptr(), B, l0.data_ptr(), l1.data_ptr(), l2.data_ptr(),
+                                          flags.data_ptr(), _stream_ptr(dev)))
+    finally:
+        _native.check(h.lib.dart_model_set_precision(h.ptr, 0))
     if check:
         raise_for_flags(int(flags.item()))
     return (l0, l1, l2), flags
@@ -463,7 +467,7 @@ def backbone_forward(model: DetectorModel, image: np.ndarray, mode: PrecisionMod
     if image.ndim != 3:
         raise ValueError(f"image shape {image.shape} does not match {(model.config.image_size,) * 2 + (3,)}")
     (l0, l1, l2), _ = backbone_forward_batch(model, image, mode)
-    return FpnFeatures((l0[0], l1[0], l2[0]), model.config.seed, device_mode(mode), model.plan_id)
+    return FpnFeatures((l0[0], l1[0], l2[0]), model.config.seed, device_mode(mode, backbone=True), model.plan_id)
 
 
 def _text_rows(name: str, text_tokens: int) -> list[int]:

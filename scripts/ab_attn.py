@@ -41,3 +41,16 @@ for rnd in range(5):
                 qkv.data_ptr(), o.data_ptr(), items, 16, L, hd, None, st.cuda_stream)), 10 if items < 10 else 4))
 for *_, name in shapes:
     print(name, "  ".join(f"v{v}: {np.median(res[(v, name)]):8.1f} us" for v in variants))
+# agreement with the first variant (same inputs)
+ref = {}
+for v in variants:
+    lib.dart_attention_variant(v)
+    for items, L, hd, name in shapes:
+        qkv, o = bufs[name]
+        _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, 16, L, hd, None, st.cuda_stream))
+        torch.cuda.synchronize()
+        if v == variants[0]:
+            ref[name] = o.float().clone()
+        else:
+            print(f"v{v} {name}: max |diff| vs v{variants[0]} = {(o.float() - ref[name]).abs().max().item():.3e}")
+lib.dart_attention_variant(0)
