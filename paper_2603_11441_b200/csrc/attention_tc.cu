@@ -88,8 +88,8 @@ struct FaCfg {
 // SPIN bit 0: the MMA issuer spins on its barriers; bit 1: the softmax warps spin on S-ready.
 // LEAN: every tcgen05.commit occupies the tensor pipe like a ~44-clk MMA (scripts/probes/
 // mma_rate.cu), so per key tile only S-ready is committed; K / V / Q stage releases become
-// thread arrivals by softmax warp 2 (S(g) complete => K(g) consumed, and P.V(g-2), issued
-// before S(g), complete => V(g-2) consumed), O-complete is committed once per item (and per
+// thread arrivals by softmax warp 2 (S(g) complete => K(g) consumed, and P.V(g-NS), issued
+// before S(g), complete => V(g-NS) consumed), O-complete is committed once per item (and per
 // tile only in the rare max-tracking pass, for its O rescale), and V loads get their own
 // producer thread (warp 0 lane 1) so they never hold back K loads.
 template <bool SPIN>
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           if (a.trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) a.trace[s_g] = clock64();
           if (LEAN && warp == 2 && lane == 0 && a.softmax_only != 1) {
             mbar_arrive(&k_empty[s_g % STAGES]);                    // S(g) has consumed K(g)
-            if (s_g >= 2) mbar_arrive(&v_empty[(s_g - 2) % STAGES]);  // P.V(g-2) precedes S(g)
+            if (s_g >= NS) mbar_arrive(&v_empty[(s_g - NS) % STAGES]);  // P.V(g-NS) precedes S(g)
             if (j == nkv - 1) mbar_arrive(&q_empty[s_it & 1]);      // last S of the item read Q
           }
           if (a.softmax_only == 2) {  // microbenchmark: MMA/TMA pipeline alone

@@ -1,0 +1,4 @@
+for v in 0 13 14 15 16; do for m in 0 2; do
+  echo "== variant $v DART_FA_SOFTMAX_ONLY=$m"
+  DART_FA_VARIANT=$v DART_FA_SOFTMAX_ONLY=$m python scripts/bench_attn.py 2>&1 | grep -E "N=80"
+done; done
