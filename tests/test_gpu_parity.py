@@ -238,3 +238,41 @@ def test_many_classes_class_shared_text_attention():
     assert np.abs(raw.boxes[sl] - g["boxes"]).max() < 1.02e-2
     assert np.abs(raw.score_logits[sl] - g["score_logits"]).max() < 4.0e-2
     assert np.abs(raw.presence_logits[sl] - g["presence_logits"]).max() < 4.0e-2
+
+
+def test_backbone_determinism_batch_independence_and_identity_trunk():
+    """Reference tests/test_model.py:85-126: the backbone is deterministic, images in a batch
+    never mix, and with every sub-block disabled the trunk is the identity (features =
+    FPN(patch embed)), checked against the oracle restatement with the same sub-block masks."""
+    from oracle import dart_oracle as O
+
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    imgs = [D.generate_scene(D.SceneSpec(seed=s, num_classes=3))[0] for s in (1, 2)]
+    a = D.backbone_forward(model, imgs[0])
+    b = D.backbone_forward(model, imgs[0])
+    for la, lb in zip(a.levels, b.levels):
+        np.testing.assert_array_equal(la, lb)
+    (l0, l1, l2), _ = D.model.backbone_forward_batch(model, np.stack(imgs))
+    for lvl, ref in zip((l0, l1, l2), a.levels):
+        np.testing.assert_array_equal(lvl[0].cpu().numpy(), ref)
+    c = D.backbone_forward(model, imgs[1])
+    np.testing.assert_array_equal(l0[1].cpu().numpy(), c.levels[0])
+
+    ident = model
+    for blk in range(model.config.num_blocks):
+        ident = D.set_sub_block(D.set_sub_block(ident, blk, "attn", False), blk, "mlp", False)
+    got = D.backbone_forward(ident, imgs[0]).levels
+    ocfg = O.OracleConfig()
+    P = O.build_params(ocfg)
+    off = [False] * ocfg.num_blocks
+    ref = O.backbone(P, ocfg, imgs[0], attn_on=off, mlp_on=off)
+    for g_, r_ in zip(got, ref):
+        assert cosine(g_, r_) > 0.99999
+        assert np.abs(g_ - r_).max() <= 2e-3 * np.abs(r_).max()
+    # partially disabled trunk (one attention and one MLP sub-block off) against the oracle
+    part = D.set_sub_block(D.set_sub_block(model, 1, "attn", False), 6, "mlp", False)
+    attn_on = [b != 1 for b in range(ocfg.num_blocks)]
+    mlp_on = [b != 6 for b in range(ocfg.num_blocks)]
+    got = D.backbone_forward(part, imgs[0]).levels[0]
+    ref = O.backbone(P, ocfg, imgs[0], attn_on=attn_on, mlp_on=mlp_on)[0]
+    assert cosine(got, ref) > 0.9999
