@@ -278,6 +278,51 @@ __global__ void k_roundtrip(long long* out) {
   }
 }
 
+
+// Latency of an mbarrier wait on an ALREADY COMPLETED phase issued right after NMMA async
+// MMAs (+ NCOMMIT commits to another barrier): does pending tensor work slow the wait?
+template <int NMMA, int NCOMMIT, int REPS>
+__global__ void k_wait_after_mma(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, done, sink;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&done, 1);
+    mbar_init(&sink, 1);
+    fence_barrier_init();
+    mbar_arrive(&done);  // phase 0 of `done` complete
+  }
+  fence_proxy_async();
+  if (threadIdx.x < 32) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
+    const uint32_t idesc = umma_idesc_f16(128, 32);
+    long long tot = 0;
+    for (int i = 0; i < REPS; ++i) {
+      for (int m = 0; m < NMMA; ++m) umma_f16(tmem, umma_desc_sw128(a), umma_desc_sw128(b), idesc, 1);
+      for (int c = 0; c < NCOMMIT; ++c) umma_commit(&sink);
+      const long long t0 = clock64();
+      mbar_wait(&done, 0);
+      tot += clock64() - t0;
+      umma_commit(&bar);  // drain before the next round
+      mbar_wait(&bar, i & 1);
+    }
+    out[blockIdx.x] = tot * 64 / REPS;  // run() divides by its reps argument (64)
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 template <typename K>
 void run(const char* name, K kern, int reps, int blocks = 148) {
   long long* d;
@@ -296,6 +341,11 @@ void run(const char* name, K kern, int reps, int blocks = 148) {
 }
 
 int main() {
+  run("wait(completed) after 0 MMA", k_wait_after_mma<0, 0, 64>, 64);
+  run("wait(completed) after 1 MMA", k_wait_after_mma<1, 0, 64>, 64);
+  run("wait(completed) after 6 MMA", k_wait_after_mma<6, 0, 64>, 64);
+  run("wait(completed) after 1 MMA+1 commit", k_wait_after_mma<1, 1, 64>, 64);
+  run("wait(completed) after 6 MMA+2 commits", k_wait_after_mma<6, 2, 64>, 64);
   run("SS M128 N32  K16", k_mma<32, false, 256>, 256);
   run("SS M128 N64  K16", k_mma<64, false, 256>, 256);
   run("SS M128 N96  K16", k_mma<96, false, 256>, 256);
