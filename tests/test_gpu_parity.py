@@ -276,3 +276,55 @@ def test_backbone_determinism_batch_independence_and_identity_trunk():
     got = D.backbone_forward(part, imgs[0]).levels[0]
     ref = O.backbone(P, ocfg, imgs[0], attn_on=attn_on, mlp_on=mlp_on)[0]
     assert cosine(got, ref) > 0.9999
+
+
+@pytest.mark.parametrize("kind", ["black", "white", "checker"])
+def test_edge_images_against_oracle(kind):
+    """Range-edge inputs (all 0, all 1, a 0/1 checkerboard: the [0, 1] bounds are inclusive,
+    model.py:430-433) through the whole path against the oracle restatement (toy model)."""
+    from oracle import dart_oracle as O
+
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    S = model.config.image_size
+    if kind == "black":
+        img = np.zeros((S, S, 3))
+    elif kind == "white":
+        img = np.ones((S, S, 3))
+    else:
+        img = ((np.arange(S)[:, None] + np.arange(S)[None, :]) % 2).astype(np.float64)[..., None].repeat(3, -1)
+    names = ["car", "person"]
+    ocfg = O.OracleConfig()
+    P = O.build_params(ocfg)
+    l0_ref, _, _ = O.backbone(P, ocfg, img)
+    _, boxes, pres, scores = O.encdec(P, ocfg, l0_ref, [O.text_embedding(P, ocfg, n) for n in names])
+    fpn = D.backbone_forward(model, img)
+    assert np.all(np.isfinite(fpn.levels[0]))
+    if np.abs(l0_ref).max() == 0.0:  # black image, zero biases: every feature is exactly 0
+        assert np.abs(fpn.levels[0]).max() == 0.0
+    else:
+        assert cosine(fpn.levels[0], l0_ref) > 0.9999
+    raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
+    assert np.abs(raw.boxes - boxes).max() < 1.04e-2
+    assert np.abs(raw.score_logits - scores).max() < 2.9e-2
+    assert np.abs(raw.presence_logits - pres).max() < 2.2e-2
+
+
+@pytest.mark.parametrize("n,n_max", [(1, None), (1, 1), (17, 4), (33, 8), (33, None)])
+def test_ragged_class_counts(n, n_max):
+    """N = 1 and class counts that leave ragged n_max chunks: per-class raw outputs equal the
+    class-batched single pass bitwise (classes never mix), detections equal run_batched's."""
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    image, _ = D.generate_scene(D.SceneSpec(seed=3, num_classes=3))
+    names = [f"class{i:02d}" for i in range(n)]
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0, n_max=n_max)
+    fpn = D.backbone_forward(model, image)
+    emb = D.text_encode(model, names)
+    full = D.encdec_forward(model, fpn, emb.stack(names))
+    for i in (0, n // 2, n - 1):
+        one = D.encdec_forward(model, fpn, emb.stack([names[i]]))
+        np.testing.assert_array_equal(one.boxes[0], full.boxes[i])
+        np.testing.assert_array_equal(one.score_logits[0], full.score_logits[i])
+    dets = D.run_batched(model, image, names, cfg)
+    ref = D.run_batched(model, image, names, D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0))
+    assert dets == ref
+    assert sorted({d.class_id for d in dets}) == list(range(n))  # gates open: every class keeps >= 1
