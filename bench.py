@@ -10,9 +10,12 @@ post-processing with gates open (presence 0, score 0: worst-case NMS work).  Wei
 are the deterministic random init of the full ViT-H/14 model (seed 0).
 
 value  = images/s over exactly K device-timed steps (CUDA events on the launch stream,
-         max over ranks), inputs resident in HBM.
-e2e    = the same through Detector.detect() with pinned host images: H2D of the images,
-         the whole path, D2H of the kept detections, inside the timed region.
+         max over ranks), inputs resident in HBM, through the inter-frame pipeline
+         (Detector.detect_device_pipelined: 2 backbone streams + 1 decode stream;
+         --no-pipeline: one stream, also reported as value_serial).
+e2e    = the same through the public streaming API Detector.detect_stream() with pinned host
+         images: H2D of the images, the whole path, D2H of the kept detections, inside the
+         timed region.
 value_default_thresholds = `value` with the reference's default gates (presence 0.5,
          score 0.45), same schedule.
 Multi-GPU (torchrun): image-batch data parallelism, one process per GPU, no collective
@@ -339,9 +342,8 @@ def run_ours(args):
             det.detect_device_pipelined(dev_pool[i % n_imgs])
         det.pipeline_join()
         barrier()
-        h_dec = det._pipeline(B)["h_dec"]
-        det.reset_launch_count()
-        lib.dart_reset_launch_count(h_dec.ptr)
+        det._pipeline(B)
+        det.pipeline_reset_launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         ev0.record(stream)
@@ -350,7 +352,7 @@ def run_ours(args):
         det.pipeline_join()
         ev1.record(stream)
         barrier()
-        launches_pipe = det.launch_count() + int(lib.dart_launch_count(h_dec.ptr))
+        launches_pipe = det.pipeline_launch_count()
         value_pipe_eager = imgs / (max_over_ranks(ev0.elapsed_time(ev1)) / 1000.0)
     if use_graph:
         for i in range(args.warmup):  # captures G_0 / G_1 on the first call
@@ -460,9 +462,12 @@ def run_ours(args):
             "data": "synthetic (SceneSpec seed 1000+i, random-init ViT-H/14 weights seed 0)",
             "config": {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {B} per GPU",
                        "classes": args.classes, "batch_per_gpu": B, "parallelism": f"image-dp{world}",
-                       "schedule": ("two-stream inter-frame pipeline (backbone of image t+1 overlaps enc-dec of "
-                                    "image t; every image fully processed)" + (", one CUDA graph per step" if use_graph
-                                                                               else "")) if pipelined else "one stream",
+                       "schedule": (("two-stream inter-frame pipeline (backbone of image t+1 overlaps enc-dec of "
+                                     "image t; every image fully processed), one CUDA graph per step") if use_graph else
+                                    (f"inter-frame pipeline: {det._pipeline(B)['nbb']} backbone streams taking images "
+                                     "in turn (backbones of images t+1, t+2 overlap each other) + 1 decode stream "
+                                     "(enc-dec + post-processing of image t); every image fully processed")
+                                    ) if pipelined else "one stream",
                        "thresholds": "presence 0, score 0 (gates open)",
                        "l2": "working set > L2 (1.29 GB fp16 weights streamed per step; 8-image input pool)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

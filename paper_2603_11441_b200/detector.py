@@ -139,29 +139,54 @@ class Detector:
 
     # ------------------------------------------------------------------ inter-frame pipelining
     def _pipeline(self, B: int):
-        """Two streams, two handles (the second a dart_model_fork sharing the weights) and two
-        buffer slots: the backbone of batch t+1 runs on stream 0 while the enc-dec and
-        post-processing of batch t run on stream 1 (the paper's two-stream schedule,
-        reference scheduler.py:128-187)."""
+        """Inter-frame pipeline: backbone streams (two by default, each with its own handle --
+        dart_model_fork shares the weights) take batches in turn, and one decode stream runs
+        the enc-dec and post-processing of each batch once its backbone is done; nbb + 1
+        buffer slots.  With one backbone stream this is the paper's two-stream schedule
+        (reference scheduler.py:128-187): the backbone of batch t+1 overlaps
+        the decode of batch t; with two, the backbones of t+1 and t+2 also overlap each other."""
         import torch
 
         p = getattr(self, "_pipe", None)
         if p is not None and p["B"] == B:
             return p
+        # n backbone streams (each with its own forked handle) take frames in turn, so up to n
+        # backbones are in flight beside the decode stream: the second backbone's GEMM and
+        # attention CTAs fill the first one's last waves (N=4: +3-4% over n = 1; n = 3, 4 no
+        # better).  DART_PIPE_BB overrides n (A/B measurement).
+        nbb = max(1, int(os.environ.get("DART_PIPE_BB", "2")))
+        # DART_PIPE_PRIORITY=1: the backbone stream (the pipeline's critical path) gets the
+        # higher CUDA stream priority (A/B measurement)
+        prio = -1 if os.environ.get("DART_PIPE_PRIORITY") else 0
+        s_bbs = [torch.cuda.Stream(device=self.device, priority=prio) for _ in range(nbb)]
         p = {
             "B": B,
+            "nbb": nbb,
+            "nslot": nbb + 1,
             "h_dec": self.handle.fork(),
-            # DART_PIPE_PRIORITY=1: the backbone stream (the pipeline's critical path) gets the
-            # higher CUDA stream priority (A/B measurement)
-            "s_bb": torch.cuda.Stream(device=self.device, priority=-1 if os.environ.get("DART_PIPE_PRIORITY") else 0),
+            "h_bb": [self.handle] + [self.handle.fork() for _ in range(nbb - 1)],
+            "s_bbs": s_bbs,
+            "s_bb": s_bbs[0],
             "s_dec": torch.cuda.Stream(device=self.device),
-            "slots": [self._alloc_slot(B) for _ in range(2)],
-            "ev_bb": [torch.cuda.Event() for _ in range(2)],
-            "ev_dec": [None, None],
+            "slots": [self._alloc_slot(B) for _ in range(nbb + 1)],
+            "ev_bb": [torch.cuda.Event() for _ in range(nbb + 1)],
+            "ev_dec": [None] * (nbb + 1),
             "t": 0,
         }
         self._pipe = p
         return p
+
+    def pipeline_launch_count(self) -> int:
+        """Kernel launches of every handle of the pipeline (backbone handles + decode fork)."""
+        p = getattr(self, "_pipe", None)
+        if p is None:
+            return self.launch_count()
+        return sum(int(self.lib.dart_launch_count(h.ptr)) for h in p["h_bb"] + [p["h_dec"]])
+
+    def pipeline_reset_launch_count(self) -> None:
+        p = getattr(self, "_pipe", None)
+        for h in ([self.handle] if p is None else p["h_bb"] + [p["h_dec"]]):
+            self.lib.dart_reset_launch_count(h.ptr)
 
     def detect_device_pipelined(self, images):
         """Enqueue one batch (device float32 [B, S, S, 3]) into the two-stream pipeline; returns
@@ -171,14 +196,15 @@ class Detector:
 
         B = int(images.shape[0])
         p = self._pipeline(B)
-        k = p["t"] & 1
+        t = p["t"]
+        k = t % p["nslot"]
         p["t"] += 1
         b = p["slots"][k]
-        s_bb, s_dec = p["s_bb"], p["s_dec"]
+        s_bb, s_dec = p["s_bbs"][t % p["nbb"]], p["s_dec"]
         s_bb.wait_stream(torch.cuda.current_stream(self.device))  # inputs produced on the caller's stream
         if p["ev_dec"][k] is not None:
-            s_bb.wait_event(p["ev_dec"][k])  # slot free: decode of batch t-2 done
-        self._enqueue_backbone(self.handle, images, b, s_bb.cuda_stream)
+            s_bb.wait_event(p["ev_dec"][k])  # slot free: decode of batch t-nslot done
+        self._enqueue_backbone(p["h_bb"][t % p["nbb"]], images, b, s_bb.cuda_stream)
         p["ev_bb"][k].record(s_bb)
         s_dec.wait_event(p["ev_bb"][k])
         self._enqueue_decode(p["h_dec"], b, B, s_dec.cuda_stream, b["l0"].data_ptr())
@@ -194,7 +220,8 @@ class Detector:
         p = getattr(self, "_pipe", None)
         if p is not None:
             cur = torch.cuda.current_stream(self.device)
-            cur.wait_stream(p["s_bb"])
+            for sb in p["s_bbs"]:
+                cur.wait_stream(sb)
             cur.wait_stream(p["s_dec"])
 
     # ------------------------------------------------------------------ CUDA graphs
@@ -283,7 +310,8 @@ class Detector:
                 raise ValueError(f"image shape {tuple(arr.shape)} does not match {(S, S, 3)}")
             B = int(arr.shape[0])
             p = self._pipeline(B)
-            k = p["t"] & 1
+            k = p["t"] % p["nslot"]
+            s_in = p["s_bbs"][p["t"] % p["nbb"]]  # the backbone stream this batch will run on
             hs = host_slots.get((B, k))
             if hs is None:
                 hs = host_slots[(B, k)] = {
@@ -292,7 +320,7 @@ class Detector:
                     "res": {n: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
                             for n, v in self.result_tensors(p["slots"][k]).items()},
                 }
-            if len(pending) >= 2:  # the slot's previous batch must be delivered first
+            if len(pending) >= p["nslot"]:  # the slot's previous batch must be delivered first
                 yield self._deliver(*pending.pop(0))
             if isinstance(arr, np.ndarray):
                 hs["img"].numpy()[...] = arr
@@ -300,8 +328,8 @@ class Detector:
             else:
                 src = arr
             if p["ev_dec"][k] is not None:
-                p["s_bb"].wait_event(p["ev_dec"][k])
-            with torch.cuda.stream(p["s_bb"]):
+                s_in.wait_event(p["ev_dec"][k])
+            with torch.cuda.stream(s_in):
                 hs["dimg"].copy_(src, non_blocking=True)
             b, _ = self.detect_device_pipelined(hs["dimg"])
             with torch.cuda.stream(p["s_dec"]):

@@ -21,12 +21,22 @@ def _setup(n_img=5):
     return model, names, cfg, imgs
 
 
-def test_detect_stream_matches_detect():
-    model, names, cfg, imgs = _setup()
+@pytest.mark.parametrize("nbb", ["1", "2", "3"])
+def test_detect_stream_matches_detect(nbb, monkeypatch):
+    """1, 2 or 3 backbone streams (DART_PIPE_BB) taking images in turn: same detections."""
+    monkeypatch.setenv("DART_PIPE_BB", nbb)
+    model, names, cfg, imgs = _setup(7)
     det = Detector(model, names, cfg)
     serial = [det.detect(im) for im in imgs]
     streamed = [r[0] for r in det.detect_stream(imgs)]
     assert streamed == serial
+    # device-resident pipelined path: image t's slot holds image t's results once its event fired
+    outs = []
+    for im in imgs:
+        b, ev = det.detect_device_pipelined(torch.from_numpy(im[None]).cuda())
+        ev.synchronize()
+        outs.append(det.unpack({k: v.cpu() for k, v in det.result_tensors(b).items()}, 1)[0])
+    assert outs == serial
 
 
 def test_detect_stream_batched_and_device_inputs():
