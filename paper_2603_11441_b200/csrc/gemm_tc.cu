@@ -146,9 +146,9 @@ __device__ __forceinline__ float sat_f16(float x) { return fminf(fmaxf(x, -65504
 __device__ __forceinline__ float round_f16(float x) { return __half2float(__float2half_rn(sat_f16(x))); }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_bias_act(float* v, int col, const GemmEpi& e) {
-  if (e.bias != nullptr) {
-    const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
+__device__ __forceinline__ void epilogue_bias_act(float* v, int col, const float* bias) {
+  if (bias != nullptr) {
+    const float4* b4 = reinterpret_cast<const float4*>(bias + col);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       float4 b = __ldg(b4 + q);
@@ -307,6 +307,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // kernel parameters read inside the loops are hoisted: after every asm "memory" clobber
+      // (barrier waits, TMA) a parameter is otherwise re-loaded from the constant bank
+      const bool noload = epi.dbg_noload != 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = cl; unit < num_units; unit += ncl) {
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
-          if (epi.dbg_noload && (unit != cl || kb >= STAGES)) {
+          if (noload && (unit != cl || kb >= STAGES)) {
             if (rank == 0) mbar_arrive(&full[stage]);
           } else if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], bytes);
@@ -391,6 +394,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       named_bar_sync(1, GEMM_THREADS - 128);
     }
     const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const float* const bias = epi.bias;  // hoisted kernel parameters (see the producer)
+    const int rope_cols = epi.rope_cols, rope_hd = epi.rope_hd;
     constexpr int NBUF = L::NBUF;
     constexpr int BUF_F = L::BUF_BYTES / 4;  // staging buffer size in floats
     float* bufs = reinterpret_cast<float*>(smem + L::EPI_OFF) + (warp - 4) * NBUF * BUF_F;
@@ -475,8 +480,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
-        if (kh == 0) epilogue_bias_act<EPI>(v, n0 + c, epi);  // split-K: bias once (half 0)
-        if (EPI == EPI_QKV_ROPE && n0 + c < epi.rope_cols) rope_chunk(v, n0 + c, epi.rope_hd, rt, ct);
+        if (kh == 0) epilogue_bias_act<EPI>(v, n0 + c, bias);  // split-K: bias once (half 0)
+        if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) rope_chunk(v, n0 + c, rope_hd, rt, ct);
         if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = (EPI == EPI_F32 || EPI == EPI_F32_F16) ? round_f16(v[j]) : sat_f16(v[j]);

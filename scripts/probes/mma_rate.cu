@@ -323,13 +323,77 @@ __global__ void k_wait_after_mma(long long* out) {
   }
 }
 
+
+// The attention MMA-alone protocol in isolation (no TMA, no softmax math): warp 0 issues
+// S(g) = 1 MMA (N=96) and P.V(g) = 6 TS MMAs (N=32) per tile with NS S buffers; NSOFT
+// "softmax" warps wait S-ready, fence and arrive P-ready.  EXTRA extra commits per tile
+// (the kernel's non-LEAN stage releases).  Reports clk per tile.
+template <int NS, int NSOFT, int EXTRA, int TILES>
+__global__ void k_pingpong(long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t s_full[NS], p_full[NS], sink;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], NSOFT);
+    }
+    mbar_init(&sink, 1);
+    fence_barrier_init();
+  }
+  fence_proxy_async();
+  if (threadIdx.x < 32) tmem_alloc<256>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 16384);
+    const uint32_t id_pv = umma_idesc_f16(128, 32) | (1u << 16), id_s = umma_idesc_f16(128, 96);
+    const long long t0 = clock64();
+    for (int g = 0; g < NS; ++g) {
+      umma_f16_w(tmem + g * 96, desc_sw32(a, 16, 256), desc_sw32(b, 16, 256), id_s, 0);
+      umma_commit_w(&s_full[g]);
+    }
+    for (int g = 0; g < TILES; ++g) {
+      mbar_wait(&p_full[g % NS], (g / NS) & 1);
+      tc_fence_after();
+      for (int k = 0; k < 6; ++k)
+        umma_f16_ts_w(tmem + NS * 96, tmem + (g % NS) * 96 + k * 8, desc_sw32(b, 96 * 32, 256), id_pv, 1);
+      for (int c = 0; c < EXTRA; ++c) umma_commit_w(&sink);
+      if (g + NS < TILES) {
+        umma_f16_w(tmem + (g % NS) * 96, desc_sw32(a, 16, 256), desc_sw32(b, 16, 256), id_s, 0);
+        umma_commit_w(&s_full[g % NS]);
+      }
+    }
+    umma_commit_w(&sink);
+    if (lane == 0) out[blockIdx.x] = (clock64() - t0) * 64 / TILES;  // run() divides by 64
+  } else if (warp <= NSOFT) {
+    for (int g = 0; g < TILES; ++g) {
+      mbar_wait(&s_full[g % NS], (g / NS) & 1);
+      tc_fence_after();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[g % NS]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 template <typename K>
-void run(const char* name, K kern, int reps, int blocks = 148) {
+void run(const char* name, K kern, int reps, int blocks = 148, int threads = 128) {
   long long* d;
   cudaMalloc(&d, 296 * sizeof(long long));
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  kern<<<blocks, 128, 64 * 1024>>>(d);
-  kern<<<blocks, 128, 64 * 1024>>>(d);
+  kern<<<blocks, threads, 64 * 1024>>>(d);
+  kern<<<blocks, threads, 64 * 1024>>>(d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -341,6 +405,11 @@ void run(const char* name, K kern, int reps, int blocks = 148) {
 }
 
 int main() {
+  run("pingpong NS2 soft1 extra0 1CTA", k_pingpong<2, 1, 0, 256>, 64, 148, 64);
+  run("pingpong NS2 soft4 extra0 1CTA", k_pingpong<2, 4, 0, 256>, 64, 148, 160);
+  run("pingpong NS2 soft4 extra3 1CTA", k_pingpong<2, 4, 3, 256>, 64, 148, 160);
+  run("pingpong NS2 soft4 extra3 2CTA", k_pingpong<2, 4, 3, 256>, 64, 296, 160);
+  run("pingpong NS3 soft4 extra3 1CTA", k_pingpong<3, 4, 3, 256>, 64, 148, 160);
   run("wait(completed) after 0 MMA", k_wait_after_mma<0, 0, 64>, 64);
   run("wait(completed) after 1 MMA", k_wait_after_mma<1, 0, 64>, 64);
   run("wait(completed) after 6 MMA", k_wait_after_mma<6, 0, 64>, 64);
