@@ -306,6 +306,28 @@ def test_attention_tcgen05_forced_safe_pass(lib, items, L, hd):
     assert float((o2.float() - ref).abs().max()) < 1e-2
 
 
+@pytest.mark.parametrize("items,L,hd", [(1, 5184, 80), (9, 576, 80), (3, 5184, 16)])
+def test_attention_tcgen05_production_equals_hooked(lib, items, L, hd):
+    """The default launch runs the hook-free production instantiation; with a trace buffer set
+    it runs the hooked twin.  Same arithmetic: outputs bitwise equal."""
+    H = 16
+    E = H * hd
+    g = torch.Generator(device="cuda").manual_seed(7 * L + items)
+    qkv = torch.randn(items * L, 3 * E, device="cuda", generator=g).half()
+    o1 = torch.empty(items * L, E, device="cuda", dtype=torch.float16)
+    o2 = torch.empty_like(o1)
+    tr = torch.zeros(11 * 256, dtype=torch.int64, device="cuda")
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o1.data_ptr(), items, H, L, hd, None, stream()))
+    lib.dart_attention_trace(tr.data_ptr())
+    try:
+        _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o2.data_ptr(), items, H, L, hd, None, stream()))
+        torch.cuda.synchronize()
+    finally:
+        lib.dart_attention_trace(None)
+    assert torch.equal(o1, o2)
+    assert int(tr.count_nonzero()) > 0  # the hooked twin really ran (it wrote its stamps)
+
+
 @pytest.mark.parametrize("rows,dim,f16", [(5184, 1280, 1), (20736, 256, 1), (777, 256, 0), (1001, 1280, 1), (33, 64, 1)])
 def test_layernorm(lib, rows, dim, f16):
     """LayerNorm (population variance, eps 1e-6; reference tensors.py:215-227) vs fp32 torch."""
