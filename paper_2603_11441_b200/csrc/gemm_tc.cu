@@ -732,6 +732,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     float* bufs = reinterpret_cast<float*>(smem + OFF_EPI) + (warp - 4) * 2048;
     uint64_t* rbar = rfull + (warp - 4) * 2;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float* const bias1 = b1;  // hoisted kernel parameters (no reloads after asm clobbers)
+    const float* const bias2 = b2;
     int it = 0, g = 0;  // g: residual chunks processed by this warp
     for (int unit = cl; unit < num_units; unit += ncl, ++it) {
       const int row0 = unit * BM * CG + rank * BM + quarter * 32;
@@ -756,7 +758,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float v[32];
           tmem_ld32(rb + col, v);
           tmem_ld_wait();
-          const float4* bb = reinterpret_cast<const float4*>(b1 + e * SL + col);
+          const float4* bb = reinterpret_cast<const float4*>(bias1 + e * SL + col);
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -791,7 +793,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(o_empty);
         }
-        const float4* bb = reinterpret_cast<const float4*>(b2 + col);
+        const float4* bb = reinterpret_cast<const float4*>(bias2 + col);
         mbar_wait(&rbar[g & 1], (g >> 1) & 1);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
