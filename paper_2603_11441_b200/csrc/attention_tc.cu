@@ -31,6 +31,8 @@
 //              Pass 1 (flagged items only, or all with force_safe): max-tracking softmax that
 //              rescales O whenever the running max grows by more than 2^8 (P <= 256), MUFU
 //              exponentials only.  Both passes give softmax(x) exactly up to fp16 rounding of P.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -301,162 +303,171 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       }
       __syncwarp();
     } else {
-      // softmax warp: TMEM lane quarter (warp & 3), column slice `part` of every S tile
-      const int quarter = warp & 3, part = (warp - 2) >> 2;
-      const int r = quarter * 32 + lane;
-      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-      float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
-      const float c = a.scale_log2;
-      // row max of the loaded S slice, combined over the SPLIT slices of this row
-      auto row_max = [&](const float* v, int gg) {
-        float pm[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pm[k] = v[k];
-#pragma unroll
-        for (int i = 8; i < L::COLS; i += 16)
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            pm[k] = i + 8 + k < L::COLS ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
-        float mx = fmaxf(fmax3f(pm[0], pm[1], pm[2]), fmax3f(fmax3f(pm[3], pm[4], pm[5]), pm[6], pm[7]));
-        if constexpr (SPLIT > 1) {
-          float* rb = red + (gg & 1) * SPLIT * BQ;
-          rb[part * BQ + r] = mx;
-          named_bar_sync(1 + quarter, 32 * SPLIT);
-#pragma unroll
-          for (int q = 0; q < SPLIT; ++q) mx = fmaxf(mx, rb[q * BQ + r]);
-        }
-        return mx;
-      };
-      int local = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-        if (!todo(local)) continue;
-        const int qt = item % q_tiles;
-        const int h = (item / q_tiles) % a.heads;
-        const int z = item / (q_tiles * a.heads) + a.z_base;
-        float m_ref = -INFINITY;
-        float nb = 0.f, cr = 0.f, br = 0.f;
-        for (int j = 0; j < nkv; ++j, ++s_g) {
-          const int sb = s_g % NS;
-          if (sm_only != 1) wait_sel<(SPIN >> 1) & 1>(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, dbg);
-          if (trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) trace[s_g] = clock64();
-          if (LEAN && warp == 2 && lane == 0 && sm_only != 1) {
-            mbar_arrive(&k_empty[s_g % STAGES]);                    // S(g) has consumed K(g)
-            if (s_g >= NS) mbar_arrive(&v_empty[(s_g - NS) % STAGES]);  // P.V(g-NS) precedes S(g)
-            if (j == nkv - 1) mbar_arrive(&q_empty[s_it & 1]);      // last S of the item read Q
+      // the two softmax passes are separate instantiations: the fast pass carries none of the
+      // max-tracking pass's code (register allocation, branches) and vice versa
+      auto softmax_pass = [&](auto pass_c) {
+        constexpr int PASS = decltype(pass_c)::value;
+        // softmax warp: TMEM lane quarter (warp & 3), column slice `part` of every S tile
+        const int quarter = warp & 3, part = (warp - 2) >> 2;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
+        const float c = a.scale_log2;
+        // row max of the loaded S slice, combined over the SPLIT slices of this row
+        auto row_max = [&](const float* v, int gg) {
+          float pm[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) pm[k] = v[k];
+  #pragma unroll
+          for (int i = 8; i < L::COLS; i += 16)
+  #pragma unroll
+            for (int k = 0; k < 8; ++k)
+              pm[k] = i + 8 + k < L::COLS ? fmax3f(pm[k], v[i + k], v[i + 8 + k]) : fmaxf(pm[k], v[i + k]);
+          float mx = fmaxf(fmax3f(pm[0], pm[1], pm[2]), fmax3f(fmax3f(pm[3], pm[4], pm[5]), pm[6], pm[7]));
+          if constexpr (SPLIT > 1) {
+            float* rb = red + (gg & 1) * SPLIT * BQ;
+            rb[part * BQ + r] = mx;
+            named_bar_sync(1 + quarter, 32 * SPLIT);
+  #pragma unroll
+            for (int q = 0; q < SPLIT; ++q) mx = fmaxf(mx, rb[q * BQ + r]);
           }
-          if (sm_only == 2) {  // microbenchmark: MMA/TMA pipeline alone
+          return mx;
+        };
+        int local = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+          if (!todo(local)) continue;
+          const int qt = item % q_tiles;
+          const int h = (item / q_tiles) % a.heads;
+          const int z = item / (q_tiles * a.heads) + a.z_base;
+          float m_ref = -INFINITY;
+          float nb = 0.f, cr = 0.f, br = 0.f;
+          for (int j = 0; j < nkv; ++j, ++s_g) {
+            const int sb = s_g % NS;
+            if (sm_only != 1) wait_sel<(SPIN >> 1) & 1>(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, dbg);
+            if (trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) trace[s_g] = clock64();
+            if (LEAN && warp == 2 && lane == 0 && sm_only != 1) {
+              mbar_arrive(&k_empty[s_g % STAGES]);                    // S(g) has consumed K(g)
+              if (s_g >= NS) mbar_arrive(&v_empty[(s_g - NS) % STAGES]);  // P.V(g-NS) precedes S(g)
+              if (j == nkv - 1) mbar_arrive(&q_empty[s_it & 1]);      // last S of the item read Q
+            }
+            if (sm_only == 2) {  // microbenchmark: MMA/TMA pipeline alone
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&p_full[sb]);
+              continue;
+            }
+            tc_fence_after();
+            const uint32_t sbase = lane_base + sb * BKV + part * L::COLS;
+            float v[L::COLS];
+            tmem_ld_cols<L::COLS>(sbase, v);
+            tmem_ld_wait();
+            uint32_t p[L::COLS / 2];
+            if (PASS == 0) {
+              if (j == 0) {
+                m_ref = row_max(v, s_g);
+                nb = -m_ref * c;
+                cr = c * (1.0f / EXP_R);
+                br = (nb - EXP_XMIN) * (1.0f / EXP_R);
+              }
+              const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
+  #pragma unroll
+              for (int i = 0; i < L::COLS / 2; ++i) {
+                float x0, x1;
+                if ((i & 7) < NPOLY / 2) {  // NPOLY of every 16 exponentials on the FMA pipe
+                  exp2_poly2_sat(v[2 * i], v[2 * i + 1], cr, br, x0, x1);
+                } else {
+                  f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
+                  x0 = fast_exp2(x0);
+                  x1 = fast_exp2(x1);
+                }
+                p[i] = pack_half2(x0, x1);
+              }
+            } else {
+              const float mx = row_max(v, s_g);
+              // warp-uniform decision (identical in every slice of this row quarter): tcgen05.ld/st
+              // are warp-collective (.sync.aligned)
+              if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
+                const float m_new = fmaxf(m_ref, mx);
+                if (j > 0 && part == 0) {
+                  const int gp = LEAN ? s_g1 - 1 : s_g - 1;  // previous P.V complete before O is rescaled
+                  mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, dbg);
+                  tc_fence_after();
+                  const float f = fast_exp2((m_ref - m_new) * c);
+  #pragma unroll 1
+                  for (int ch = 0; ch < L::ON / 16; ++ch) {
+                    float o[16];
+                    tmem_ld16(lane_base + L::OCOL + ch * 16, o);
+                    tmem_ld_wait();
+                    uint32_t u[16];
+  #pragma unroll
+                    for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * f);
+                    tmem_st16(lane_base + L::OCOL + ch * 16, u);
+                  }
+                }
+                m_ref = m_new;
+              }
+              nb = -m_ref * c;
+              const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
+  #pragma unroll
+              for (int i = 0; i < L::COLS / 2; ++i) {
+                float x0, x1;
+                f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
+                p[i] = pack_half2(fast_exp2(x0), fast_exp2(x1));
+              }
+            }
+            // P (fp16 pairs) over this slice's own, already loaded S columns (no cross-slice hazard)
+            tmem_st_cols<L::COLS / 2>(lane_base + sb * BKV + part * L::COLS, p);
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[sb]);
-            continue;
+            if (lane == 0 && sm_only != 1) mbar_arrive(&p_full[sb]);
+            if (PASS == 1) ++s_g1;
+            if (trace && blockIdx.x == 0 && lane == 0 && s_g < 256) {
+              if (warp == 2) trace[256 + s_g] = clock64();
+              trace[1792 + (warp - 2) * 256 + s_g] = clock64();  // P done, per softmax warp
+            }
           }
+          // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
+          // part, part + SPLIT, ...
+          const int gl = s_g - 1;
+          if (sm_only != 1) {
+            if constexpr (LEAN)
+              mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, dbg);
+            else
+              mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, dbg);
+          }
+          ++s_it;
           tc_fence_after();
-          const uint32_t sbase = lane_base + sb * BKV + part * L::COLS;
-          float v[L::COLS];
-          tmem_ld_cols<L::COLS>(sbase, v);
+          float lsum[8];
+          tmem_ld8(lane_base + L::OCOL + HD, lsum);
           tmem_ld_wait();
-          uint32_t p[L::COLS / 2];
-          if (pass == 0) {
-            if (j == 0) {
-              m_ref = row_max(v, s_g);
-              nb = -m_ref * c;
-              cr = c * (1.0f / EXP_R);
-              br = (nb - EXP_XMIN) * (1.0f / EXP_R);
-            }
-            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
-#pragma unroll
-            for (int i = 0; i < L::COLS / 2; ++i) {
-              float x0, x1;
-              if ((i & 7) < NPOLY / 2) {  // NPOLY of every 16 exponentials on the FMA pipe
-                exp2_poly2_sat(v[2 * i], v[2 * i + 1], cr, br, x0, x1);
-              } else {
-                f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
-                x0 = fast_exp2(x0);
-                x1 = fast_exp2(x1);
-              }
-              p[i] = pack_half2(x0, x1);
-            }
-          } else {
-            const float mx = row_max(v, s_g);
-            // warp-uniform decision (identical in every slice of this row quarter): tcgen05.ld/st
-            // are warp-collective (.sync.aligned)
-            if (__any_sync(0xffffffffu, (mx - m_ref) * c > RESCALE_LOG2)) {  // always on the first tile
-              const float m_new = fmaxf(m_ref, mx);
-              if (j > 0 && part == 0) {
-                const int gp = LEAN ? s_g1 - 1 : s_g - 1;  // previous P.V complete before O is rescaled
-                mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, dbg);
-                tc_fence_after();
-                const float f = fast_exp2((m_ref - m_new) * c);
-#pragma unroll 1
-                for (int ch = 0; ch < L::ON / 16; ++ch) {
-                  float o[16];
-                  tmem_ld16(lane_base + L::OCOL + ch * 16, o);
-                  tmem_ld_wait();
-                  uint32_t u[16];
-#pragma unroll
-                  for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * f);
-                  tmem_st16(lane_base + L::OCOL + ch * 16, u);
-                }
-              }
-              m_ref = m_new;
-            }
-            nb = -m_ref * c;
-            const uint64_t c2 = f2_pack(c, c), nb2 = f2_pack(nb, nb);
-#pragma unroll
-            for (int i = 0; i < L::COLS / 2; ++i) {
-              float x0, x1;
-              f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
-              p[i] = pack_half2(fast_exp2(x0), fast_exp2(x1));
+          const int qrow = qt * BQ + r;
+          if (PASS == 0) {
+            const bool bad = qrow < a.Lq && !(fabsf(lsum[0]) < INFINITY);
+            if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&ovf[local >> 5], 1u << (local & 31));
+          }
+          const float inv = 1.f / lsum[0];
+          __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
+  #pragma unroll 1
+          for (int ch = part; ch < HD / 8; ch += SPLIT) {
+            float o[8];
+            tmem_ld8(lane_base + L::OCOL + ch * 8, o);
+            tmem_ld_wait();
+            if (qrow < a.Lq) {
+              uint4 w;
+              w.x = pack_half2(o[0] * inv, o[1] * inv);
+              w.y = pack_half2(o[2] * inv, o[3] * inv);
+              w.z = pack_half2(o[4] * inv, o[5] * inv);
+              w.w = pack_half2(o[6] * inv, o[7] * inv);
+              reinterpret_cast<uint4*>(dst + ch * 8)[0] = w;
             }
           }
-          // P (fp16 pairs) over this slice's own, already loaded S columns (no cross-slice hazard)
-          tmem_st_cols<L::COLS / 2>(lane_base + sb * BKV + part * L::COLS, p);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0 && sm_only != 1) mbar_arrive(&p_full[sb]);
-          if (pass == 1) ++s_g1;
-          if (trace && blockIdx.x == 0 && lane == 0 && s_g < 256) {
-            if (warp == 2) trace[256 + s_g] = clock64();
-            trace[1792 + (warp - 2) * 256 + s_g] = clock64();  // P done, per softmax warp
-          }
         }
-        // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
-        // part, part + SPLIT, ...
-        const int gl = s_g - 1;
-        if (sm_only != 1) {
-          if constexpr (LEAN)
-            mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, dbg);
-          else
-            mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, dbg);
-        }
-        ++s_it;
-        tc_fence_after();
-        float lsum[8];
-        tmem_ld8(lane_base + L::OCOL + HD, lsum);
-        tmem_ld_wait();
-        const int qrow = qt * BQ + r;
-        if (pass == 0) {
-          const bool bad = qrow < a.Lq && !(fabsf(lsum[0]) < INFINITY);
-          if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&ovf[local >> 5], 1u << (local & 31));
-        }
-        const float inv = 1.f / lsum[0];
-        __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
-#pragma unroll 1
-        for (int ch = part; ch < HD / 8; ch += SPLIT) {
-          float o[8];
-          tmem_ld8(lane_base + L::OCOL + ch * 8, o);
-          tmem_ld_wait();
-          if (qrow < a.Lq) {
-            uint4 w;
-            w.x = pack_half2(o[0] * inv, o[1] * inv);
-            w.y = pack_half2(o[2] * inv, o[3] * inv);
-            w.z = pack_half2(o[4] * inv, o[5] * inv);
-            w.w = pack_half2(o[6] * inv, o[7] * inv);
-            reinterpret_cast<uint4*>(dst + ch * 8)[0] = w;
-          }
-        }
-      }
+      };
+      if (pass == 0)
+        softmax_pass(std::integral_constant<int, 0>{});
+      else
+        softmax_pass(std::integral_constant<int, 1>{});
     }
   }
   tc_fence_before();
