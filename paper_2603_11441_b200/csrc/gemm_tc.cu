@@ -237,8 +237,9 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 constexpr int GEMM_THREADS = 384;
 
 // PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
-// path's instantiations (PREC = false) carry none of that code.
-template <int BN, int STAGES, int EPI, int CG, bool PREC>
+// path's instantiations (PREC = false) carry none of that code.  SPLITK: the opt-in split-K
+// residual variant (GemmEpi::splitk); without it the split-K paths compile out.
+template <int BN, int STAGES, int EPI, int CG, bool PREC, bool SPLITK>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
-  const int SK = RESID ? epi.splitk : 1;  // K slices per tile (work unit = tile x slice)
+  const int SK = (RESID && SPLITK) ? epi.splitk : 1;  // K slices per tile (work unit = tile x slice)
   const int TF = epi.tail_full;           // tail halves: units >= TF are BN/2-wide halves of a tile
   const int num_units = TF > 0 ? TF + 2 * (num_tiles - TF) : num_tiles * SK;
   const int nk = K / BK / SK;             // k-blocks per unit
@@ -825,18 +826,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BN, int STAGES, int EPI, int CG, bool PREC>
+template <int BN, int STAGES, int EPI, int CG, bool PREC, bool SPLITK>
 int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES, EPI, CG>;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG, PREC>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG, PREC, SPLITK>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return (int)e;
     configured = true;
   }
-  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID ? epi.splitk : 1);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID && SPLITK ? epi.splitk : 1);
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   if constexpr (CG == 1) {
@@ -873,9 +874,12 @@ constexpr int stages_for() {
 template <int BN, int EPI, int CG>
 int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tB2, const CUtensorMap& tC,
                    const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  constexpr int ST = stages_for<BN, EPI, CG>();
   if (epi.acc_f16 || epi.round_f16)
-    return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG, true>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
-  return launch_gemm<BN, stages_for<BN, EPI, CG>(), EPI, CG, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    return launch_gemm<BN, ST, EPI, CG, true, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+  if constexpr (EPI == EPI_F32_RESID)
+    if (epi.splitk > 1) return launch_gemm<BN, ST, EPI, CG, false, true>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+  return launch_gemm<BN, ST, EPI, CG, false, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
 }
 
 template <int BN, int CG>
