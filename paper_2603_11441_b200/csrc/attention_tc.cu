@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         const int quarter = warp & 3, part = (warp - 2) >> 2;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
+        [[maybe_unused]] float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
         const float c = a.scale_log2;
         // row max of the loaded S slice, combined over the SPLIT slices of this row
         auto row_max = [&](const float* v, int gg) {
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           }
           // epilogue: O / rowsum -> fp16 rows of the output; slice `part` writes 8-column chunks
           // part, part + SPLIT, ...
-          const int gl = s_g - 1;
+          [[maybe_unused]] const int gl = s_g - 1;
           if (sm_only != 1) {
             if constexpr (LEAN)
               mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, dbg);
