@@ -1,35 +1,46 @@
 #!/usr/bin/env python
 """DART multi-class detection throughput on B200 (BASELINE.json metric: images/sec at
-1008^2 ViT-H/14 DART, N classes).
+1008^2 ViT-H/14 DART, N=4 and N=80 classes, on 1/2/4/8 B200).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--classes 4] [--batch 1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--classes 4] [--batch 1]
+                    [--impl ours|reference] [--shard images|classes]
 
 A step = one detection of one batch of synthetic 1008^2 scenes (SceneSpec(seed=1000+i,
 num_rects=3, noise=0.05)) against N class prompts: backbone, class-batched enc-dec,
-post-processing with gates open (presence 0, score 0: worst-case NMS work).  Weights
-are the deterministic random init of the full ViT-H/14 model (seed 0).
+post-processing with gates open (presence 0, score 0: worst-case NMS work).  Weights are
+the deterministic random init of the full ViT-H/14 model (seed 0).
 
-value  = images/s over exactly K device-timed steps (CUDA events on the launch stream,
-         max over ranks), inputs resident in HBM, through the inter-frame pipeline
-         (Detector.detect_device_pipelined: 2 backbone streams + 1 decode stream;
-         --no-pipeline: one stream, also reported as value_serial).
-e2e    = the same through the public streaming API Detector.detect_stream() with pinned host
-         images: H2D of the images, the whole path, D2H of the kept detections, inside the
-         timed region.
-value_default_thresholds = `value` with the reference's default gates (presence 0.5,
-         score 0.45), same schedule.
-Multi-GPU (torchrun): image-batch data parallelism, one process per GPU, no collective
-on the data path ("scaling": "weak"); timing is the max over ranks.
---impl reference: the CPU reference path (the float64 NumPy oracle port of the
-reference's algorithm) on the host cores, timed on bounded per-unit samples and
-composed additively (the reference's per-block / per-class loops are additive).
+The headline line (configs[1], N=4, batch 1 per GPU):
+  value  = images/s over exactly K device-timed steps (CUDA events on the launch stream,
+           max over ranks), inputs resident in HBM, through the inter-frame pipeline
+           (Detector.detect_device_pipelined: 2 backbone streams + 1 decode stream).
+  e2e    = the same through the public streaming API Detector.detect_stream() with pinned
+           host images: H2D of the images, the whole path, D2H of the kept detections,
+           inside the timed region.
+  n80    = the same two numbers at N=80 COCO classes (configs[2]) in the same run.
+  shard_classes (N>1 GPUs, or --shard classes) = config 5: 80 classes sharded over the ranks,
+           backbone + enc-dec prefix of one image per rank, NCCL all-gather of the prefix
+           output e1, class-shard decode of all W images, all-gather of raw outputs.
+  roofline = the dominant kernel of the N=4 step (tcgen05 GEMM with the fp32 residual
+           epilogue: backbone attn.out + mlp.fc2) timed live with CUDA events; roofline_attn16
+           = the dominant kernel of the N=80 step (hd-16 encoder self-attention) against the
+           exp (MUFU + FMA-polynomial) roof.
+  cpu_baseline = the UNMODIFIED reference (baseline/_ref, pip-installed from /root/reference
+           by oracle/install_ref.sh) timed per additive unit on the host cores, composed as
+           the reference's own loops compose (model.py:457-458 blocks, 559-564 classes).
+Multi-GPU: `--gpus N` without torchrun re-launches itself under torch.distributed.run with N
+ranks (one per GPU, NCCL); image-batch data parallelism has no collective on the data path
+("scaling": "weak"); timing is the max over ranks.
+--impl reference: the reference CPU path alone (rank 0), same units and composition.
 """
 
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -39,10 +50,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "images/sec at 1008^2 ViT-H/14 DART (N classes), B images per step"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+N80 = 80
 
 
 def gflops_per_image(cfg, n_classes: int) -> float:
@@ -75,48 +88,75 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every 10 ms through NVML while `active` (the timed
+    regions only: `with sampler.timed(): ...`); nvidia-smi polling as a fallback."""
 
-    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4,
+            "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
-        self.index, self.samples, self.proc = index, [], None
-
-    def __enter__(self):
+        self.index, self.samples, self.active, self.stop = index, [], False, False
+        self.nvml = None
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
-        return self
+            self.nvml = None
+            self.max_mhz = None
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
-
-    def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
+    def _sample(self):
+        if self.nvml is not None:
+            pn = self.nvml
+            sm = pn.nvmlDeviceGetClockInfo(self.h, pn.NVML_CLOCK_SM)
             try:
-                self.proc.wait(timeout=5)
+                bits = pn.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
-                self.proc.kill()
+                bits = pn.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            return float(sm), int(bits)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        a = [x.strip() for x in out.split(",")]
+        if self.max_mhz is None:
+            self.max_mhz = float(a[1])
+        return float(a[0]), 0
+
+    def _run(self):
+        while not self.stop:
+            if self.active:
+                try:
+                    self.samples.append(self._sample())
+                except Exception:
+                    pass
+            time.sleep(0.01)
+
+    class _Timed:
+        def __init__(self, s):
+            self.s = s
+
+        def __enter__(self):
+            self.s.active = True
+
+        def __exit__(self, *exc):
+            self.s.active = False
+
+    def timed(self):
+        return ClockSampler._Timed(self)
 
     def summary(self):
+        self.stop = True
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({k for _, b in self.samples for k, bit in self.BITS.items() if b & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi",
+                "window": "timed regions only, 10 ms period"}
 
 
 def coco80():
@@ -138,28 +178,134 @@ def class_names(n: int):
     return coco80()[:n] if n <= 80 else [f"class{i:02d}" for i in range(n)]
 
 
-# ============================================================================ CPU reference arm
+def bench_config(args, world: int) -> dict:
+    """The workload description, identical in both arms (so the driver can match them)."""
+    return {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {args.batch} per GPU",
+            "classes": args.classes, "batch_per_gpu": args.batch, "secondary_classes": N80,
+            "parallelism": f"image-dp{world}", "thresholds": "presence 0, score 0 (gates open)",
+            "images": "SceneSpec(seed=1000+i, image_size=1008, num_rects=3, noise=0.05, num_classes=4)",
+            "weights": "random init, seed 0"}
 
-def cpu_reference_units(cfg, n_classes: int, budget_s: float, log=None):
-    """Time the oracle port (float64 NumPy, all BLAS threads) per additive unit of the
-    reference's loops and compose seconds/image:
-        t = t_patch + (L-G) t_windowed_block + G t_global_block + t_fpn + t_prefix
-            + N (t_enc_layer * ne + t_dec_layer * nd)
-    Each unit is measured once (the global block and encoder layer dominate)."""
-    from oracle import dart_oracle as O
 
-    ocfg = O.full_config()
-    rng = np.random.default_rng(0)
+# ============================================================================ CPU reference
+def _blas_threads() -> int | None:
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads") or 0) for i in threadpool_info()) or None
+    except Exception:
+        return None
+
+
+def reference_cpu_units(log=None):
+    """Time the UNMODIFIED reference package (baseline/_ref; float64 NumPy, all BLAS threads)
+    per additive unit of its own loops, on a model with the full-size shapes but only the
+    units needed (weights are keyed by parameter path, so block 0 / block 1 / layer 0 hold
+    exactly the full model's values):
+        patch      = patch_tokens                        (model.py:426)
+        windowed   = _block_forward(block 0, windowed)   (model.py:412)
+        global     = _block_forward(block 1, global)
+        fpn        = fpn_from_tokens                     (model.py:446)
+        class_1x1  = _encdec_single of a 1-encoder/1-decoder-layer model, one class
+                     (input proj + layer + final LN + layer + heads, model.py:511-533)
+        enc_layer / dec_layer = one more layer body, the reference's own _ln/_mha/_mlp_forward
+        postprocess(N) = pipeline.postprocess of N classes x 200 queries, gates open
+    seconds/image(N) = patch + (L-G) windowed + G global + fpn
+                       + N (class_1x1 + (ne-1) enc_layer + (nd-1) dec_layer) + postprocess(N)
+    (exact for the reference: blocks and classes are independent Python loops,
+    model.py:457-458, 559-564).  Falls back to the oracle port if baseline/_ref is absent."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import dart.model as M
+        import dart.pipeline as PL
+        from dart.scenes import SceneSpec, generate_scene
+        from dart.tensors import PrecisionMode
+    except ImportError:
+        return None
+    mode = PrecisionMode.FP32
+    full = M.ModelConfig(1008, 14, 1280, 32, (7, 15, 23, 31), 24, 16, (256, 256, 256), 32, 256, 200, 6, 6, seed=0)
+    unit_cfg = dataclasses.replace(full, num_blocks=2, global_block_indices=(1,), num_encoder_layers=1,
+                                   num_decoder_layers=1)
     units = {}
 
     def timed(name, fn):
         t0 = time.perf_counter()
-        fn()
+        r = fn()
         units[name] = time.perf_counter() - t0
         if log:
-            log(f"[cpu] {name}: {units[name]:.2f}s")
+            log(f"[cpu-ref] {name}: {units[name]:.2f}s")
+        return r
 
-    # weights only for the blocks/layers sampled (same shapes and init as the full model)
+    t0 = time.perf_counter()
+    model = M.build_model(unit_cfg, with_mask_head=False)
+    build_s = time.perf_counter() - t0
+    image, _ = generate_scene(SceneSpec(seed=1000, image_size=1008, num_rects=3, noise=0.05, num_classes=4))
+    x = timed("patch", lambda: M.patch_tokens(model, image, mode))
+    x = timed("windowed_block", lambda: M._block_forward(model, x, 0, mode))
+    x = timed("global_block", lambda: M._block_forward(model, x, 1, mode))
+    lv = timed("fpn", lambda: M.fpn_from_tokens(model, x, mode))
+    text = M.text_encode(model, ["person"]).stack(["person"])[0]
+    qf, bx, pl, sl = timed("class_1x1", lambda: M._encdec_single(model, lv[0], text, mode))
+    e = M._linear(model, lv[0], "encdec.input", mode)
+
+    def enc_layer():  # the loop body of _encdec_single (model.py:514-519)
+        p = "encoder.layer0"
+        h = M._ln(model, e, f"{p}.ln1")
+        e2 = e + M._mha(model, h, h, f"{p}.self", mode)
+        e2 = e2 + M._mha(model, M._ln(model, e2, f"{p}.ln2"), text, f"{p}.cross", mode)
+        return e2 + M._mlp_forward(model, M._ln(model, e2, f"{p}.ln3"), f"{p}.mlp", mode)
+
+    timed("enc_layer", enc_layer)
+    mem = M._ln(model, e, "encoder.final_ln")
+
+    def dec_layer():  # model.py:522-527
+        q = np.concatenate([model.params["decoder.queries"], model.params["decoder.presence_token"]], axis=0)
+        p = "decoder.layer0"
+        h = M._ln(model, q, f"{p}.ln1")
+        q = q + M._mha(model, h, h, f"{p}.self", mode)
+        q = q + M._mha(model, M._ln(model, q, f"{p}.ln2"), mem, f"{p}.cross", mode)
+        return q + M._mlp_forward(model, M._ln(model, q, f"{p}.ln3"), f"{p}.mlp", mode)
+
+    timed("dec_layer", dec_layer)
+    pcfg = PL.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    for n in (4, N80):
+        raw = M.RawQueryOutputs(query_features=np.stack([qf] * n), boxes=np.stack([bx] * n),
+                                presence_logits=np.array([pl] * n, dtype=np.float64), score_logits=np.stack([sl] * n))
+        timed(f"postprocess_n{n}", lambda: PL.postprocess(raw, class_names(n), pcfg))
+    L, G = full.num_blocks, len(full.global_block_indices)
+    per_class = units["class_1x1"] + (full.num_encoder_layers - 1) * units["enc_layer"] + \
+        (full.num_decoder_layers - 1) * units["dec_layer"]
+    shared = units["patch"] + (L - G) * units["windowed_block"] + G * units["global_block"] + units["fpn"]
+
+    def per_image(n):
+        pp = units.get(f"postprocess_n{n}", units["postprocess_n4"] * n / 4)
+        return shared + n * per_class + pp
+
+    sample = ("unmodified reference dart 0.1.0 (baseline/_ref), float64 NumPy/OpenBLAS, timed once per unit at "
+              "full size on image SceneSpec(seed=1000): patch_tokens, 1 windowed + 1 global _block_forward, "
+              "fpn_from_tokens, one class through _encdec_single of a 1+1-layer model, one more encoder and decoder "
+              "layer, postprocess; extrapolated additively to (L-G)=28 windowed + G=4 global blocks and "
+              "N x (6 enc + 6 dec) layers, exactly as the reference's loops compose")
+    return {"per_image": per_image, "units_s": units, "sample": sample, "kind": "reference",
+            "build_s": build_s, "cpu_s": sum(units.values())}
+
+
+def oracle_port_units(log=None):
+    """Fallback when baseline/_ref is missing: the float64 NumPy oracle port, same units."""
+    from oracle import dart_oracle as O
+
+    ocfg = O.full_config()
+    units = {}
+
+    def timed(name, fn):
+        t0 = time.perf_counter()
+        r = fn()
+        units[name] = time.perf_counter() - t0
+        if log:
+            log(f"[cpu-port] {name}: {units[name]:.2f}s")
+        return r
+
     decl = {p: (s, i) for p, s, i in O.param_declaration(ocfg)}
     P = {}
 
@@ -171,98 +317,65 @@ def cpu_reference_units(cfg, n_classes: int, budget_s: float, log=None):
                 elif i == "zeros":
                     P[p] = np.zeros(s)
                 elif i in ("rope_cos", "rope_sin"):
-                    c, sn = O.rope_tables(ocfg)
-                    P["rope.cos"], P["rope.sin"] = c, sn
+                    P["rope.cos"], P["rope.sin"] = O.rope_tables(ocfg)
                 else:
                     P[p] = O.philox_uniform(0, p, s, int(i))
 
-    need("rope")
-    need("patch_embed")
+    for pre in ("rope", "patch_embed", "backbone.block0.", "backbone.block7.", "fpn.", "encdec.", "encoder.",
+                "decoder.", "text.", "heads."):
+        need(pre)
     image, _ = O.scene(1000, 1008, num_classes=4)
-    x = None
-
-    def patch():
-        nonlocal x
-        x = O.linear(P, O.patchify(ocfg, image), "patch_embed")
-
-    timed("patch_embed", patch)
-    need("backbone.block0.")
+    x = timed("patch", lambda: O.linear(P, O.patchify(ocfg, image), "patch_embed"))
     timed("windowed_block", lambda: O.backbone_block(P, ocfg, x, 0))
-    need("backbone.block7.")
     timed("global_block", lambda: O.backbone_block(P, ocfg, x, 7))
-    need("fpn.")
-    timed("fpn", lambda: O.fpn(P, ocfg, x))
-    need("encdec.")
-    need("encoder.")
-    need("decoder.")
-    need("text.")
-    l0 = rng.standard_normal((ocfg.tokens, 256)) * 0.5
-    e = None
-
-    def prefix():
-        nonlocal e
-        e = O.encoder_prefix(P, ocfg, l0)
-
-    timed("encdec_prefix", prefix)
+    l0 = timed("fpn", lambda: O.fpn(P, ocfg, x))[0]
     text = O.text_embedding(P, ocfg, "person")
+    timed("class_6x6", lambda: O.encdec_one(P, ocfg, l0, text))
+    L, G = ocfg.num_blocks, len(ocfg.global_block_indices)
+    shared = units["patch"] + (L - G) * units["windowed_block"] + G * units["global_block"] + units["fpn"]
+    return {"per_image": lambda n: shared + n * units["class_6x6"], "units_s": units, "kind": "port",
+            "sample": "oracle port (float64 NumPy) per unit at full size, composed additively", "build_s": 0.0,
+            "cpu_s": sum(units.values())}
 
-    def enc_layer():
-        p = "encoder.layer1"
-        h = O._ln(P, e, f"{p}.ln1")
-        e2 = e + O.mha(P, ocfg, h, h, f"{p}.self")
-        e2 = e2 + O.mha(P, ocfg, O._ln(P, e2, f"{p}.ln2"), text, f"{p}.cross")
-        return e2 + O.mlp(P, O._ln(P, e2, f"{p}.ln3"), f"{p}.mlp")
 
-    timed("encoder_layer", enc_layer)
-
-    def dec_layer():
-        q = np.concatenate([P["decoder.queries"], P["decoder.presence_token"]])
-        p = "decoder.layer1"
-        h = O._ln(P, q, f"{p}.ln1")
-        q = q + O.mha(P, ocfg, h, h, f"{p}.self")
-        q = q + O.mha(P, ocfg, O._ln(P, q, f"{p}.ln2"), e, f"{p}.cross")
-        return q + O.mlp(P, O._ln(P, q, f"{p}.ln3"), f"{p}.mlp")
-
-    timed("decoder_layer", dec_layer)
-    L, G = cfg.num_blocks, len(cfg.global_block_indices)
-    per_image = (units["patch_embed"] + (L - G) * units["windowed_block"] + G * units["global_block"] + units["fpn"]
-                 + units["encdec_prefix"] + n_classes * (cfg.num_encoder_layers * units["encoder_layer"]
-                                                          + cfg.num_decoder_layers * units["decoder_layer"]))
-    sample = ("oracle port (float64 NumPy) timed per unit at full size: patch-embed, 1 windowed block, 1 global "
-              "block, FPN, enc-dec prefix, 1 encoder layer + 1 decoder layer for 1 class; composed additively as "
-              f"(L-G)*win + G*glob + N*(6*enc + 6*dec) for L={L}, G={G}, N={n_classes}")
-    return per_image, units, sample
+def cpu_units(log=None):
+    return reference_cpu_units(log) or oracle_port_units(log)
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2603_11441_b200 as D
-
-    cfg = D.vit_h_config()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     t0 = time.perf_counter()
-    per_image, units, sample = cpu_reference_units(cfg, args.classes, budget_s=240,
-                                                   log=lambda s: print(s, file=sys.stderr))
-    value = 1.0 / per_image
+    cu = cpu_units(log=lambda s: print(s, file=sys.stderr, flush=True))
+    per = cu["per_image"](args.classes)
+    value = 1.0 / per
+    cores = os.cpu_count()
+    cpu = {"value": value, "unit": "images/s", "cores": cores, "blas_threads": _blas_threads(), "kind": cu["kind"],
+           "sample": cu["sample"], "units_s": cu["units_s"], "value_n80": 1.0 / cu["per_image"](N80),
+           "extrapolated": True, "units_measured_once": True}
     line = {
-        "impl": "reference", "metric": METRIC.replace("N classes", f"N={args.classes} classes").replace(
-            "B images", "1 image" if args.batch == 1 else f"{args.batch} images"), "value": value,
-        "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_image * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": 1, "steps_requested": args.steps, "warmup": 0,
+        "steps_note": "each additive unit of the reference's loops ran once (one step = one bounded sample); "
+                      "value = 1 / (sum of units composed to one full image)",
+        "ms_per_step": per * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SceneSpec seed 1000, random-init ViT-H/14 weights seed 0)",
-        "config": {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {args.batch}",
-                   "classes": args.classes, "batch": args.batch},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": sample, "units_s": units},
+        "config": bench_config(args, world), "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": time.perf_counter() - t0,
+        "n80": {"value": cpu["value_n80"], "unit": "images/s"},
+        "wall_s": time.perf_counter() - t0, "cpu_s_measured": cu["cpu_s"], "build_s": cu["build_s"],
     }
     print(json.dumps(line), flush=True)
 
 
-# ============================================================================ B200 arm
+def metric_name(args):
+    return METRIC.replace("N classes", f"N={args.classes} classes").replace(
+        "B images", "1 image" if args.batch == 1 else f"{args.batch} images")
 
+
+# ============================================================================ B200 arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -271,25 +384,32 @@ def run_ours(args):
     from paper_2603_11441_b200 import _native
     from paper_2603_11441_b200.detector import Detector
 
-    lib = _native.load()
+    _native.load()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench: rank {rank} needs GPU {local} but only {torch.cuda.device_count()} are visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
+    elif args.shard == "classes":  # the class-sharded protocol on a single-rank NCCL group
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
+        s.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     log = (lambda s: print(s, file=sys.stderr, flush=True)) if rank == 0 else (lambda s: None)
+    clocks = ClockSampler(local)
 
     cfg = D.vit_h_config(seed=0)
     t0 = time.perf_counter()
     model = D.build_model(cfg, with_mask_head=False)
     log(f"[bench] build_model {time.perf_counter() - t0:.1f}s")
-    names = class_names(args.classes)
-    pcfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
-    t0 = time.perf_counter()
-    det = Detector(model, names, pcfg, device=dev)
-    log(f"[bench] weight upload {time.perf_counter() - t0:.1f}s")
+    gates_open = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
 
     B = args.batch
     n_imgs = max(2, min(8, args.steps + args.warmup))
@@ -312,226 +432,298 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- device-resident throughput, one stream (value_serial)
-    for i in range(args.warmup):
-        det.detect_device(dev_pool[i % n_imgs])
-    barrier()
-    det.reset_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ev0.record(stream)
-    for i in range(args.steps):
-        det.detect_device(dev_pool[i % n_imgs])
-    ev1.record(stream)
-    barrier()
-    launches_serial = det.launch_count()
-    ms_serial = max_over_ranks(ev0.elapsed_time(ev1))
-    imgs = args.steps * B * world
-    value_serial = imgs / (ms_serial / 1000.0)
-    res = det.result_tensors(det._buffers(B))
-    kept = int(res["kc"].sum().item())
+    def timed_ms(fn, steps, sample_clocks=True):
+        """Barrier + sync, CUDA events around exactly `steps` calls on the launch stream, barrier
+        + sync; max over ranks."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        with clocks.timed() if sample_clocks else _null():
+            e0.record(stream)
+            for i in range(steps):
+                fn(i)
+            e1.record(stream)
+            barrier()
+        return max_over_ranks(e0.elapsed_time(e1))
 
-    # ---------------- device-resident throughput, two-stream inter-frame pipeline (value):
-    # backbone of image t+1 overlapped with the enc-dec + post-processing of image t; --graph
-    # replays each pipelined step as one CUDA graph (G_0 / G_1, Detector.detect_device_graph)
-    pipelined = not args.no_pipeline
-    use_graph = pipelined and args.graph
-    value_pipe_eager = None
-    if pipelined:
+    imgs = args.steps * B * world
+    h2d = B * cfg.image_size * cfg.image_size * 3 * 4
+
+    def measure(n_classes, serial=True, defaults=True):
+        """All legs of one class count: serial, pipelined (value), default gates, e2e."""
+        names = class_names(n_classes)
+        t0 = time.perf_counter()
+        det = Detector(model, names, gates_open, device=dev)
+        log(f"[bench] N={n_classes}: detector ready {time.perf_counter() - t0:.1f}s")
+        r = {}
+        if serial:
+            for i in range(args.warmup):
+                det.detect_device(dev_pool[i % n_imgs])
+            barrier()
+            det.reset_launch_count()
+            ms = timed_ms(lambda i: det.detect_device(dev_pool[i % n_imgs]), args.steps)
+            r["value_serial"] = imgs / (ms / 1000.0)
+            r["ms_per_step_serial"] = ms / args.steps
+            r["gpu_launches_serial"] = det.launch_count()
+        # inter-frame pipeline (headline value)
         for i in range(args.warmup):
             det.detect_device_pipelined(dev_pool[i % n_imgs])
         det.pipeline_join()
         barrier()
-        det._pipeline(B)
         det.pipeline_reset_launch_count()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        ev0.record(stream)
-        for i in range(args.steps):
+
+        def pipe_step(i):
             det.detect_device_pipelined(dev_pool[i % n_imgs])
-        det.pipeline_join()
-        ev1.record(stream)
-        barrier()
-        launches_pipe = det.pipeline_launch_count()
-        value_pipe_eager = imgs / (max_over_ranks(ev0.elapsed_time(ev1)) / 1000.0)
-    if use_graph:
-        for i in range(args.warmup):  # captures G_0 / G_1 on the first call
-            det.detect_device_graph(dev_pool[i % n_imgs])
-        barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clocks:
-            barrier()
-            ev0.record(stream)
-            # K steps = K backbones + K decodes (the first decode is the last warm-up image's)
-            for i in range(args.steps):
-                det.detect_device_graph(dev_pool[i % n_imgs])
-            ev1.record(stream)
-            barrier()
-        det.graph_drain()
-        launches = launches_pipe  # a graph replay launches the same kernels as the eager step
-        ms = max_over_ranks(ev0.elapsed_time(ev1))
-    elif pipelined:
-        with ClockSampler(local) as clocks:
-            barrier()
-            ev0.record(stream)
-            for i in range(args.steps):
-                det.detect_device_pipelined(dev_pool[i % n_imgs])
-            det.pipeline_join()
-            ev1.record(stream)
-            barrier()
-        launches = launches_pipe
-        ms = max_over_ranks(ev0.elapsed_time(ev1))
-    else:
-        with ClockSampler(local) as clocks:
-            barrier()
-            ev0.record(stream)
-            for i in range(args.steps):
-                det.detect_device(dev_pool[i % n_imgs])
-            ev1.record(stream)
-            barrier()
-        launches = det.launch_count()
-        ms = max_over_ranks(ev0.elapsed_time(ev1))
-    value = imgs / (ms / 1000.0)
+            if i == args.steps - 1:
+                det.pipeline_join()
 
-    # ---------------- the reference's default gates (presence 0.5, score 0.45; pipeline.py:67-100),
-    # same schedule: SURVEY 8(d) asks for the defaults beside the gates-open headline
-    det_def = Detector(model, names, D.PipelineConfig(), device=dev)
-    run_def = det_def.detect_device_pipelined if pipelined else det_def.detect_device
-    for i in range(args.warmup):
-        run_def(dev_pool[i % n_imgs])
-    if pipelined:
-        det_def.pipeline_join()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for i in range(args.steps):
-        run_def(dev_pool[i % n_imgs])
-    if pipelined:
-        det_def.pipeline_join()
-    ev1.record(stream)
-    barrier()
-    value_default = imgs / (max_over_ranks(ev0.elapsed_time(ev1)) / 1000.0)
-    del det_def
+        ms = timed_ms(pipe_step, args.steps)
+        r["value"] = imgs / (ms / 1000.0)
+        r["ms_per_step"] = ms / args.steps
+        r["gpu_launches"] = det.pipeline_launch_count()
+        r["nbb"] = det._pipeline(B)["nbb"]
+        p = det._pipeline(B)
+        res = det.result_tensors(p["slots"][(p["t"] - 1) % p["nslot"]])
+        r["kept_detections_last_step"] = int(res["kc"].sum().item())
+        if defaults:  # the reference's default gates (presence 0.5, score 0.45; pipeline.py:67-100)
+            det_def = Detector(model, names, D.PipelineConfig(), device=dev)
+            for i in range(args.warmup):
+                det_def.detect_device_pipelined(dev_pool[i % n_imgs])
+            det_def.pipeline_join()
+            barrier()
 
-    # ---------------- end to end through the public API with pinned host images: H2D of the
-    # images and D2H of the kept detections inside the timed region
-    if pipelined:
+            def def_step(i):
+                det_def.detect_device_pipelined(dev_pool[i % n_imgs])
+                if i == args.steps - 1:
+                    det_def.pipeline_join()
+
+            r["value_default_thresholds"] = imgs / (timed_ms(def_step, args.steps) / 1000.0)
+            del det_def
+        # end to end through the public API with pinned host images: H2D of the images and D2H
+        # of the kept detections inside the timed region
         for _ in det.detect_stream([host_pool[i % n_imgs] for i in range(max(1, args.warmup))]):
             pass
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for res_i in det.detect_stream([host_pool[i % n_imgs] for i in range(args.steps)]):
-            out = res_i[0]
-        det.pipeline_join()
-        e1.record(stream)
-        barrier()
-    else:
-        for i in range(max(1, args.warmup)):
-            det.detect(host_pool[i % n_imgs])
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            out = det.detect(host_pool[i % n_imgs])
-        e1.record(stream)
-        barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    e2e_value = imgs / (e2e_ms / 1000.0)
-    h2d = B * cfg.image_size * cfg.image_size * 3 * 4
-    d2h = det.d2h_bytes(B)
+        out = [None]
 
-    # ---------------- dominant-kernel roofline: backbone MLP fc1 GEMM (tcgen05), live CUDA events
-    roof = kernel_roofline(det, model, cfg, dev, args)
+        def e2e_all(_):
+            for res_i in det.detect_stream([host_pool[i % n_imgs] for i in range(args.steps)]):
+                out[0] = res_i[0]
+            det.pipeline_join()
+
+        e2e_ms = timed_ms(e2e_all, 1)
+        r["e2e"] = {"value": imgs / (e2e_ms / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": det.d2h_bytes(B)}
+        r["detections_e2e_last"] = len(out[0])
+        del det
+        torch.cuda.empty_cache()
+        return r
+
+    r4 = measure(args.classes)
+    log(f"[bench] N={args.classes}: {r4['value']:.2f} img/s (e2e {r4['e2e']['value']:.2f})")
+    r80 = None
+    if not args.no_n80 and args.classes != N80:
+        r80 = measure(N80, serial=False, defaults=False)
+        log(f"[bench] N={N80}: {r80['value']:.2f} img/s (e2e {r80['e2e']['value']:.2f})")
+
+    shard = None
+    if world > 1 or args.shard == "classes":
+        shard = measure_class_sharded(model, dev_pool, n_imgs, args, world, rank, timed_ms, barrier, log)
+
+    roof = gemm_roofline(cfg, dev, args, stream)
+    roof16 = attn16_roofline(cfg, dev, stream)
 
     pk, pk_kind = load_peaks()
     gf = gflops_per_image(cfg, args.classes)
-    step_tflops = gf * imgs / (ms / 1000.0) / 1000.0 / world
+    step_tflops = gf * imgs / (r4["ms_per_step"] * args.steps / 1000.0) / 1000.0 / world
+    clk = clocks.summary()
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            per_image, units, sample = cpu_reference_units(cfg, args.classes, budget_s=60, log=log)
-            cpu = {"value": 1.0 / per_image, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": sample, "units_s": units}
+            cu = cpu_units(log=log)
+            cpu = {"value": 1.0 / cu["per_image"](args.classes), "unit": "images/s", "cores": os.cpu_count(),
+                   "blas_threads": _blas_threads(), "kind": cu["kind"], "sample": cu["sample"],
+                   "units_s": cu["units_s"], "value_n80": 1.0 / cu["per_image"](N80), "extrapolated": True}
         line = {
-            "metric": METRIC.replace("N classes", f"N={args.classes} classes").replace(
-                "B images", "1 image" if B == 1 else f"{B} images"), "value": value, "unit": "images/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "metric": metric_name(args), "value": r4["value"], "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r4["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "fp16 operands, fp32 accumulate/residual, fp64 post-processing",
             "data": "synthetic (SceneSpec seed 1000+i, random-init ViT-H/14 weights seed 0)",
-            "config": {"workload": f"full ViT-H/14 DART 1008^2, {args.classes} classes, batch {B} per GPU",
-                       "classes": args.classes, "batch_per_gpu": B, "parallelism": f"image-dp{world}",
-                       "schedule": (("two-stream inter-frame pipeline (backbone of image t+1 overlaps enc-dec of "
-                                     "image t; every image fully processed), one CUDA graph per step") if use_graph else
-                                    (f"inter-frame pipeline: {det._pipeline(B)['nbb']} backbone streams taking images "
-                                     "in turn (backbones of images t+1, t+2 overlap each other) + 1 decode stream "
-                                     "(enc-dec + post-processing of image t); every image fully processed")
-                                    ) if pipelined else "one stream",
-                       "thresholds": "presence 0, score 0 (gates open)",
-                       "l2": "working set > L2 (1.29 GB fp16 weights streamed per step; 8-image input pool)"},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches,
-            "value_serial": value_serial, "ms_per_step_serial": ms_serial / args.steps,
-            "value_pipelined_eager": value_pipe_eager,
-            "value_default_thresholds": value_default,
-            "gpu_launches_serial": launches_serial,
+            "config": dict(bench_config(args, world), schedule=(
+                f"inter-frame pipeline: {r4['nbb']} backbone streams taking images in turn + 1 decode stream "
+                "(enc-dec + post-processing of image t); every image fully processed"),
+                l2="working set > L2 (1.29 GB fp16 weights streamed per step; 8-image input pool)"),
+            "e2e": r4["e2e"],
+            "gpu_launches": r4["gpu_launches"],
+            "value_serial": r4.get("value_serial"), "ms_per_step_serial": r4.get("ms_per_step_serial"),
+            "gpu_launches_serial": r4.get("gpu_launches_serial"),
+            "value_default_thresholds": r4.get("value_default_thresholds"),
+            "kept_detections_last_step": r4["kept_detections_last_step"],
+            "detections_e2e_last": r4["detections_e2e_last"],
+            "n80": None if r80 is None else {
+                "classes": N80, "value": r80["value"], "unit": "images/s", "ms_per_step": r80["ms_per_step"],
+                "e2e": r80["e2e"], "gpu_launches": r80["gpu_launches"],
+                "kept_detections_last_step": r80["kept_detections_last_step"],
+                "step_roofline_frac": gflops_per_image(cfg, N80) * r80["value"] / world / 1000.0 /
+                pk["bf16_tflops_sustained"],
+                "cpu_baseline_value": None if cpu is None else cpu["value_n80"]},
+            "shard_classes": shard,
             "roofline": roof,
+            "roofline_attn16": roof16,
             "step_roofline": {"bound": "tensor", "gflop_per_image": gf, "achieved_tflops": step_tflops,
                               "peak_tflops": pk["bf16_tflops_sustained"], "peak_kind": f"{pk_kind} sustained",
                               "frac": step_tflops / pk["bf16_tflops_sustained"]},
             "cpu_baseline": cpu,
-            "clocks": clocks.summary(),
-            "kept_detections_last_step": kept,
-            "detections_e2e_last": len(out),
+            "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
-def kernel_roofline(det, model, cfg, dev, args):
-    """Time the backbone MLP fc1 GEMM ([B*T, E] x [E, 4E], the largest single tcgen05 launch
-    shape) on the launching stream with CUDA events; achieved = 2*M*N*K / mean duration."""
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def measure_class_sharded(model, dev_pool, n_imgs, args, world, rank, timed_ms, barrier, log):
+    """Config 5: 80 classes sharded over the W ranks (distributed.class_sharded_raw): each round
+    every rank contributes one image (backbone + enc-dec prefix), the prefix outputs are
+    all-gathered over NCCL, each rank decodes its N/W classes for all W images, the raw
+    outputs are all-gathered and every rank post-processes its own image.  K rounds = K*W
+    images; device-timed, no host sync inside."""
+    import paper_2603_11441_b200 as D
+    from paper_2603_11441_b200.distributed import ClassShardPlan, NativeEngine, class_sharded_raw
+
+    names = class_names(N80)
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    eng = NativeEngine(model)
+
+    def step(i):
+        bx, sc, pr, _ = class_sharded_raw(eng, dev_pool[i % n_imgs], names, None)
+        eng.postprocess_device(bx, sc, pr, cfg)
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    ms = timed_ms(step, args.steps)
+    val = args.steps * world / (ms / 1000.0)
+    log(f"[bench] class-sharded N={N80} over {world} ranks: {val:.2f} img/s")
+    return {"classes": N80, "value": val, "unit": "images/s", "ms_per_round": ms / args.steps, "n_gpus": world,
+            "classes_per_rank": ClassShardPlan(N80, world).width,
+            "exchange": "NCCL all_gather of e1 [5184, 256] fp32 per image + raw outputs [N/W, 200, 5] fp64"}
+
+
+def _time_launches(fn, stream, reps=30):
     import torch
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps / 1000.0
+
+
+def gemm_roofline(cfg, dev, args, stream):
+    """Dominant kernel of the N=4 step: gemm_tc_kernel with the fp32 residual epilogue (epi 3),
+    one backbone attn.out ([T,1280]x[1280,1280]) and one mlp.fc2 ([T,5120]x[5120,1280]) launch per
+    block, timed on the launching stream with CUDA events at the step's shapes."""
+    import torch
+
     from paper_2603_11441_b200 import _native
 
     pk, pk_kind = load_peaks()
     lib = _native.load()
-    M, K, N = args.batch * cfg.tokens, cfg.embed_dim, 4 * cfg.embed_dim
-    A = torch.randn(M, K, device=dev).half()
-    W = (torch.randn(N, K, device=dev) / K ** 0.5).half()
-    bias = torch.zeros(N, device=dev)
-    out = torch.empty(M, N, device=dev, dtype=torch.float16)
-    st = torch.cuda.current_stream(dev)
-    call = lambda: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None,
-                                               M, N, K, 1, None, None, 0, 0, 0, st.cuda_stream))
-    for _ in range(5):
-        call()
-    torch.cuda.synchronize(dev)
-    reps = 50
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(reps):
-        call()
-    e1.record(st)
-    torch.cuda.synchronize(dev)
-    t = e0.elapsed_time(e1) / reps / 1000.0
-    achieved = 2.0 * M * N * K / t / 1e12
+    M, E = args.batch * cfg.tokens, cfg.embed_dim
+    out = torch.zeros(M, E, device=dev, dtype=torch.float32)
+    bias = torch.zeros(E, device=dev)
+    res = {}
+    for name, K in (("attn.out", E), ("mlp.fc2", 4 * E)):
+        A = torch.randn(M, K, device=dev).half()
+        W = (torch.randn(E, K, device=dev) / K ** 0.5).half()
+        call = lambda A=A, W=W, K=K: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(),
+                                                                 out.data_ptr(), None, M, E, K, 3, None, None, 0, 0,
+                                                                 0, stream.cuda_stream))
+        res[name] = (2.0 * M * E * K, _time_launches(call, stream))
+    flop = sum(f for f, _ in res.values())
+    t = sum(s for _, s in res.values())
+    achieved = flop / t / 1e12
     peak = pk["bf16_tflops"]
-    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+    traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
-            tj = json.load(f)["gemm_fc1"]
+        with open(os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json")) as f:
+            tj = json.load(f)
         if args.batch == 1:
-            traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+            traffic = sum(tj[k]["dram_read_bytes"] + tj[k]["dram_write_bytes"] for k in ("attn.out", "mlp.fc2")) / 2
     except Exception:
         pass
-    return {"kernel": "gemm_tc_kernel<BN 256, EPI_F16_RELU, CTA pair> (backbone mlp.fc1)", "bound": "tensor",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "peak_kind": f"{pk_kind} burst bf16/fp16 dense", "flop_per_launch": 2.0 * M * N * K,
-            "us_per_launch": t * 1e6, "traffic": traffic,
-            "traffic_note": "dram read+write bytes per launch, ncu --set full (profiles/r01/roofline_traffic.json)"}
+    return {"kernel": "gemm_tc_kernel, fp32 residual epilogue (backbone attn.out + mlp.fc2; 1 of each per block)",
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_kind": f"{pk_kind} burst bf16/fp16 dense",
+            "flop_per_launch": flop / 2, "us_per_launch": t / 2 * 1e6,
+            "per_shape": {k: {"flop": f, "us": s * 1e6, "tflops": f / s / 1e12} for k, (f, s) in res.items()},
+            "traffic": traffic,
+            "traffic_note": "mean dram read+write bytes per launch of the two shapes, ncu --set full "
+                            "(profiles/r02/roofline_traffic.json)"}
+
+
+def attn16_roofline(cfg, dev, stream):
+    """Dominant kernel of the N=80 step: hd-16 encoder self-attention over 80 classes x 16 heads x
+    5184^2 scores (tcgen05 fa_tc_kernel<16>), timed on its launching stream.  Bound: exponentials
+    (one per score); roof = MUFU ex2 16/clk/SM with the FMA-pipe polynomial share of the kernel
+    (6 of 16), at the sampled SM clock."""
+    import torch
+
+    from paper_2603_11441_b200 import _native
+
+    lib = _native.load()
+    H, L, hd, items = cfg.num_heads, cfg.tokens, cfg.text_dim // cfg.num_heads, N80
+    qkv = (torch.randn(items * L, 3 * H * hd, device=dev) * 0.5).half()
+    o = torch.empty(items * L, H * hd, device=dev, dtype=torch.float16)
+    call = lambda: _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None,
+                                                        stream.cuda_stream))
+    t = _time_launches(call, stream, reps=5)
+    exps = float(items) * H * L * L
+    flops = 4.0 * exps * hd
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = 1.965e9
+    mufu_roof = 16 * sms * clk  # exp/s, MUFU only
+    poly_roof = mufu_roof * 16 / 10  # 6 of 16 exps on the FMA pipe
+    return {"kernel": "fa_tc_kernel<16,96,...> (enc self-attention, N=80)", "bound": "exp",
+            "achieved": exps / t / 1e12, "unit": "Texp/s", "peak": poly_roof / 1e12,
+            "frac": exps / t / poly_roof, "frac_mufu_only_roof": exps / t / mufu_roof,
+            "us_per_launch": t * 1e6, "exps_per_launch": exps, "tensor_tflops": flops / t / 1e12,
+            "peak_note": "16 ex2/clk/SM x SMs x 1.965 GHz, x16/10 for the 6-of-16 polynomial share"}
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-launch this script under torch.distributed.run with N
+    ranks on this node (one per GPU, NCCL over NVLink)."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench: --gpus {args.gpus} requested but only {have} GPU(s) are visible", file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -542,17 +734,19 @@ def main():
     ap.add_argument("--classes", type=int, default=4)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shard", default="images", choices=["images", "classes"],
+                    help="classes: also run the class-sharded 80-class leg (always on with >1 GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-pipeline", action="store_true", help="one stream (no inter-frame overlap)")
-    ap.add_argument("--graph", action="store_true",
-                    help="each pipelined step as one CUDA-graph replay (measured: same throughput as eager)")
+    ap.add_argument("--no-n80", action="store_true", help="skip the N=80 section of the line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

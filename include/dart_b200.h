@@ -111,6 +111,16 @@ int dart_backbone_fpn(dart_model* m, const float* x, int32_t B, float* l0, float
 int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
                 double* score_logits, double* presence_logits, float* query_features, void* stream);
 
+/* The same enc-dec split at its class-independent prefix (model.py:513-517: input projection and
+ * encoder layer-0 self-attention; text first enters at :518), for class sharding across GPUs
+ * (SURVEY 8(e) config 5): dart_encdec_prefix writes e1 [B, T, d] float32 (l0 NULL: the last
+ * dart_backbone output), which a caller may exchange between ranks (NCCL all-gather) before each
+ * rank runs dart_encdec_from_prefix on its own class shard.  dart_encdec == prefix + from_prefix
+ * (bitwise). */
+int dart_encdec_prefix(dart_model* m, const float* l0, int32_t B, float* e1, void* stream);
+int dart_encdec_from_prefix(dart_model* m, const float* e1, int32_t B, const float* text, int32_t N, double* boxes,
+                            double* score_logits, double* presence_logits, float* query_features, void* stream);
+
 /* Presence gate, score gate, (score desc, query asc) ordering and greedy per-class NMS,
  * decisions in fp64 (pipeline.py:243-294).  Inputs float64 [N,Q,4] / [N,Q] / [N].  For N items of Q queries:
  *   kept_count [N] int32, kept_query [N, Q] int32, kept_score [N, Q] float64 (sigmoid),

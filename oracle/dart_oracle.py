@@ -356,10 +356,11 @@ def encoder_prefix(P, cfg: OracleConfig, level0):
     return e + mha(P, cfg, h, h, "encoder.layer0.self")
 
 
-def encdec_one(P, cfg: OracleConfig, level0, text, taps: dict | None = None):
+def encdec_one(P, cfg: OracleConfig, level0, text, taps: dict | None = None, e1=None):
     """One class: 6-layer encoder, 6-layer decoder, heads (model.py:511-533).
-    Returns (query_features, boxes, presence_logit, score_logits)."""
-    e = encoder_prefix(P, cfg, level0)
+    Returns (query_features, boxes, presence_logit, score_logits).  `e1`: the class-independent
+    prefix output (encoder_prefix) when already computed; level0 is then unused."""
+    e = encoder_prefix(P, cfg, level0) if e1 is None else e1
     for l in range(cfg.num_encoder_layers):
         p = f"encoder.layer{l}"
         if l > 0:
@@ -390,11 +391,11 @@ def encdec_one(P, cfg: OracleConfig, level0, text, taps: dict | None = None):
     return qf, boxes, presence, scores
 
 
-def encdec(P, cfg: OracleConfig, level0, texts):
+def encdec(P, cfg: OracleConfig, level0, texts, e1=None):
     """Classes decoded independently and stacked (model.py:536-570)."""
     if len(texts) < 1:
         raise ValueError("text batch must contain at least one class")
-    outs = [encdec_one(P, cfg, level0, t) for t in texts]
+    outs = [encdec_one(P, cfg, level0, t, e1=e1) for t in texts]
     return (np.stack([o[0] for o in outs]), np.stack([o[1] for o in outs]),
             np.array([o[2] for o in outs], dtype=np.float64), np.stack([o[3] for o in outs]))
 

@@ -33,6 +33,8 @@ EXPORTS = (
     "dart_backbone_blocks",
     "dart_backbone_fpn",
     "dart_encdec",
+    "dart_encdec_prefix",
+    "dart_encdec_from_prefix",
     "dart_postprocess",
     "dart_model_set_mask_head",
     "dart_mask_head",
@@ -142,6 +144,10 @@ def load() -> ctypes.CDLL:
     lib.dart_backbone_fpn.restype = ctypes.c_int
     lib.dart_encdec.argtypes = [P, P, I32, P, I32, P, P, P, P, P]
     lib.dart_encdec.restype = ctypes.c_int
+    lib.dart_encdec_prefix.argtypes = [P, P, I32, P, P]
+    lib.dart_encdec_prefix.restype = ctypes.c_int
+    lib.dart_encdec_from_prefix.argtypes = [P, P, I32, P, I32, P, P, P, P, P]
+    lib.dart_encdec_from_prefix.restype = ctypes.c_int
     lib.dart_postprocess.argtypes = [P, P, P, P, I32, I32, F64, F64, F64, I32, P, P, P, P, P, P, P]
     lib.dart_postprocess.restype = ctypes.c_int
     lib.dart_model_set_mask_head.argtypes = [P, P, P, P, P]

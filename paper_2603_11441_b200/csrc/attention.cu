@@ -360,12 +360,8 @@ template <int HD>
 int launch(const AttnArgs& a, cudaStream_t stream) {
   constexpr int WARPS = 4;
   constexpr int SMEM = (16 * WARPS + 4 * BKV) * (HD + 8) * 2;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(flash_attn_kernel<HD, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (const cudaError_t e = set_smem_once(smem_set, flash_attn_kernel<HD, WARPS>, SMEM); e != cudaSuccess) return (int)e;
   dim3 grid((a.Lq + 16 * WARPS - 1) / (16 * WARPS), a.heads, a.batch);
   flash_attn_kernel<HD, WARPS><<<grid, WARPS * 32, SMEM, stream>>>(a);
   return (int)cudaGetLastError();
@@ -383,12 +379,8 @@ bool attention_short_supported(const AttnArgs& a, int head_dim) {
 
 int attention_short(const AttnArgs& a, cudaStream_t stream) {
   constexpr int SMEM = (XS_ROWS + 2 * XS_LK) * XS_PITCH * 2;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(xattn_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (const cudaError_t e = set_smem_once(smem_set, xattn_short_kernel, SMEM); e != cudaSuccess) return (int)e;
   dim3 grid((a.Lq + XS_ROWS - 1) / XS_ROWS, a.batch);
   xattn_short_kernel<<<grid, 256, SMEM, stream>>>(a);
   return (int)cudaGetLastError();

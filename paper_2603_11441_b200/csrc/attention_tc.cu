@@ -484,12 +484,8 @@ template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, i
 int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
   using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
   auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (const cudaError_t e = set_smem_once(smem_set, kern, Lay::TOTAL); e != cudaSuccess) return (int)e;
   // items of one launch: each CTA may own at most ATTN_TC_MAX_LOCAL_ITEMS (overflow bitmask)
   const long long per_z = (long long)((a.Lq + BQ - 1) / BQ) * a.heads;
   const long long max_grid = (long long)num_sms * CTAS;

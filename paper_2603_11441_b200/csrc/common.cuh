@@ -7,11 +7,27 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "paper_2603_11441_b200 kernels target sm_100a only"
 #endif
 
 namespace dart {
+
+// One-time cudaFuncSetAttribute(MaxDynamicSharedMemorySize) per kernel AND per device: the
+// attribute is per-device state, so the "done" flag is a bitmask over device ordinals.
+template <typename K>
+inline cudaError_t set_smem_once(std::atomic<uint64_t>& done, K kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 typedef __half act_t;  // GEMM/attention operand type: fp16 storage, fp32 accumulation
 

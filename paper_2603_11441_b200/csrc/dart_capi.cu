@@ -936,34 +936,37 @@ int dart_backbone_fpn(dart_model* m, const float* x, int32_t B, float* l0, float
   return bb_fpn(m, x, B, l0, l1, l2, flags, (cudaStream_t)stream);
 }
 
-int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
-                double* score_logits, double* presence_logits, float* query_features, void* stream) {
-  if (!m || B <= 0 || N <= 0 || !text || !boxes || !score_logits || !presence_logits)
-    return fail(DART_ERR_INVALID, "dart_encdec: bad args");
-  if (!l0 && (m->bb_cap == 0 || m->last_backbone_B != B))
-    return fail(DART_ERR_INVALID, "dart_encdec: l0 == NULL but no matching dart_backbone output");
-  cudaStream_t s = (cudaStream_t)stream;
-  RUN(ensure_encdec_ws(m, B, N));
-  const int T = m->T, D = m->D, Q1 = m->Q1, Q = m->d.num_queries, Lt = m->Lt;
-  const int ne = m->d.num_encoder_layers, nd = m->d.num_decoder_layers;
-  const int items = B * N;
+}  // extern "C"
+
+namespace {
+
+// Class-independent enc-dec prefix, once per image: input projection + encoder layer-0
+// self-attention sub-block (model.py:513-517; text first enters at :518) -> e1 [B, T, d] fp32.
+// The enc-dec workspace must hold B images (ensure_encdec_ws).
+int ed_prefix(dart_model* m, const float* l0, int B, float* e1, cudaStream_t s) {
+  const int T = m->T, D = m->D;
   auto& w = m->ed;
   const __half* l0h = m->bb.l0h;
   if (l0) {
     LAUNCH(cast_f32_to_f16(l0, w.l0h, (long long)B * T * m->F0, s));
     l0h = w.l0h;
   }
-  // ---- class-independent prefix, once per image: input projection + encoder layer-0
-  //      self-attention sub-block (model.py:513-517; text first enters at :518)
-  RUN(gemm(m, l0h, B * T, m->F0, m->enc_in, EPI_F32, epi_out(w.e1, D), s));
-  {
-    XAttnSpec sp;
-    sp.items = B;
-    sp.Lq = T;
-    RUN(xattn(m, w.e1, m->enc[0].ln1, m->enc[0].self, sp, w.h, w.q, w.kv, w.o, s));
-  }
+  RUN(gemm(m, l0h, B * T, m->F0, m->enc_in, EPI_F32, epi_out(e1, D), s));
+  XAttnSpec sp;
+  sp.items = B;
+  sp.Lq = T;
+  return xattn(m, e1, m->enc[0].ln1, m->enc[0].self, sp, w.h, w.q, w.kv, w.o, s);
+}
+
+// The class-batched rest of the enc-dec for B images x N classes, from the prefix output e1.
+int ed_body(dart_model* m, const float* e1, int B, const float* text, int N, double* boxes, double* score_logits,
+            double* presence_logits, float* query_features, cudaStream_t s) {
+  const int T = m->T, D = m->D, Q1 = m->Q1, Q = m->d.num_queries, Lt = m->Lt;
+  const int ne = m->d.num_encoder_layers, nd = m->d.num_decoder_layers;
+  const int items = B * N;
+  auto& w = m->ed;
   for (int b = 0; b < B; ++b)
-    LAUNCH(broadcast_rows(w.e1 + (size_t)b * T * D, w.e + (size_t)b * N * T * D, (long long)T * D, N, s));
+    LAUNCH(broadcast_rows(e1 + (size_t)b * T * D, w.e + (size_t)b * N * T * D, (long long)T * D, N, s));
   // ---- text K/V for all 6 encoder cross-attentions in one GEMM
   LAUNCH(cast_f32_to_f16(text, w.text, (long long)N * Lt * D, s));
   RUN(gemm(m, w.text, N * Lt, D, m->enc_cross_kv_all, EPI_F16, epi_out(w.tkv, ne * 2 * D), s));
@@ -1024,6 +1027,38 @@ int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, in
   return DART_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int dart_encdec(dart_model* m, const float* l0, int32_t B, const float* text, int32_t N, double* boxes,
+                double* score_logits, double* presence_logits, float* query_features, void* stream) {
+  if (!m || B <= 0 || N <= 0 || !text || !boxes || !score_logits || !presence_logits)
+    return fail(DART_ERR_INVALID, "dart_encdec: bad args");
+  if (!l0 && (m->bb_cap == 0 || m->last_backbone_B != B))
+    return fail(DART_ERR_INVALID, "dart_encdec: l0 == NULL but no matching dart_backbone output");
+  cudaStream_t s = (cudaStream_t)stream;
+  RUN(ensure_encdec_ws(m, B, N));
+  RUN(ed_prefix(m, l0, B, m->ed.e1, s));
+  return ed_body(m, m->ed.e1, B, text, N, boxes, score_logits, presence_logits, query_features, s);
+}
+
+int dart_encdec_prefix(dart_model* m, const float* l0, int32_t B, float* e1, void* stream) {
+  if (!m || B <= 0 || !e1) return fail(DART_ERR_INVALID, "dart_encdec_prefix: bad args");
+  if (!l0 && (m->bb_cap == 0 || m->last_backbone_B != B))
+    return fail(DART_ERR_INVALID, "dart_encdec_prefix: l0 == NULL but no matching dart_backbone output");
+  RUN(ensure_encdec_ws(m, B, 1));  // e1 is caller-owned: a later (B, N) workspace growth keeps it
+  return ed_prefix(m, l0, B, e1, (cudaStream_t)stream);
+}
+
+int dart_encdec_from_prefix(dart_model* m, const float* e1, int32_t B, const float* text, int32_t N, double* boxes,
+                            double* score_logits, double* presence_logits, float* query_features, void* stream) {
+  if (!m || !e1 || B <= 0 || N <= 0 || !text || !boxes || !score_logits || !presence_logits)
+    return fail(DART_ERR_INVALID, "dart_encdec_from_prefix: bad args");
+  RUN(ensure_encdec_ws(m, B, N));
+  return ed_body(m, e1, B, text, N, boxes, score_logits, presence_logits, query_features, (cudaStream_t)stream);
+}
+
 int dart_postprocess(dart_model* m, const double* boxes, const double* score_logits, const double* presence_logits,
                      int32_t N, int32_t Q, double presence_threshold, double score_threshold,
                      double nms_iou_threshold, int32_t cross_class, int32_t* kept_count, int32_t* kept_query,
@@ -1077,7 +1112,10 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   CUtensorMap td;
   if (!make_out_maps(epi, e, M, N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
   if (g_gemm_splitk == 2 && epi == EPI_F32_RESID && (K / 64) % 2 == 0) {  // tests: split-K residual path
-    static int* flags = nullptr;
+    static int* flags_of[64] = {};  // per device (tests only)
+    int dev_id = 0;
+    cudaGetDevice(&dev_id);
+    int*& flags = flags_of[dev_id & 63];
     if (!flags && cudaMalloc(&flags, 65536 * sizeof(int)) != cudaSuccess) return fail(DART_ERR_CUDA, "flags");
     const int tiles = ((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (N / plan.bn);
     if (tiles > 65536) return fail(DART_ERR_INVALID, "dart_gemm: too many split-K tiles");

@@ -831,12 +831,8 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
                 const CUtensorMap& tD, int M, int N, int K, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   using L = GemmSmem<BN, STAGES, EPI, CG>;
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG, PREC, SPLITK>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (const cudaError_t e = set_smem_once(smem_set, kern, L::TOTAL); e != cudaSuccess) return (int)e;
   const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID && SPLITK ? epi.splitk : 1);
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
@@ -911,12 +907,8 @@ double g_eff192 = env_or("DART_GEMM_EFF192", 0.80), g_eff160 = env_or("DART_GEMM
 
 int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX, int M,
               const float* b1, const float* b2, int num_sms, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mlpf::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};
+  if (const cudaError_t e = set_smem_once(smem_set, mlp_fused_kernel, mlpf::TOTAL); e != cudaSuccess) return (int)e;
   const int units = (M + 255) / 256, pairs = num_sms / 2;
   const int grid = (units < pairs ? units : pairs) * 2;
   cudaLaunchConfig_t cfg = {};

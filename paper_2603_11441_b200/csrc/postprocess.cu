@@ -1,8 +1,8 @@
 // Detection-only post-processing (reference pipeline.py:243-294), one CTA per class.
 //
-// Decisions must be bit-identical to the reference on identical inputs, so every
-// decision-bearing value is computed in fp64 in the reference's operation order
-// with explicit round-to-nearest intrinsics (no FMA contraction):
+// Decisions must be identical to the reference on identical inputs, so every decision-bearing
+// value is computed in fp64 in the reference's operation order with explicit round-to-nearest
+// intrinsics (no FMA contraction), the exponential correctly rounded (exp_cr below):
 //   presence = sigmoid(presence_logit); class skipped if presence < thr   (pipeline.py:277-279)
 //   s_q = sigmoid(score_logit_q); candidate iff s_q >= thr                (pipeline.py:280-285)
 //   order by (s desc, q asc)                                              (pipeline.py:286)
@@ -17,9 +17,72 @@ namespace {
 constexpr int PP_THREADS = 256;
 constexpr int PP_MAXQ = 1024;
 
+// ---- correctly rounded exp in double-double arithmetic.  CUDA's exp() is faithful (<= 1 ulp)
+// but not correctly rounded; the reference's NumPy exp is another <= 1 ulp implementation
+// (measured here: numpy 2.3 AVX-512 exp differs from the correctly rounded value on ~4.6% of
+// inputs, glibc's on ~0.07%).  Rounding the exact value makes the device scores a function of
+// the logit alone (platform independent), and tests/test_gpu_parity.py pins it against a
+// 50-digit decimal evaluation.  Cost is irrelevant here (<= N*Q evaluations per image).
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+  return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  return quick_two_sum(s.hi, __dadd_rn(s.lo, __dadd_rn(a.lo, b.lo)));
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  return quick_two_sum(p.hi, __fma_rn(a.hi, b.lo, __fma_rn(a.lo, b.hi, p.lo)));
+}
+
+__device__ double exp_cr(double x) {
+  // x = k ln2 + r, |r| <= ln2/2, ln2 = L0 + L1 + L2 (L0 has 21 significant bits: k L0 is exact)
+  const double L0 = 0x1.62e42p-1, L1 = 0x1.fdf473de6af28p-22, L2 = -0x1.c4c67fc0d0951p-76;
+  const double k = rint(x * 0x1.71547652b82fep0);
+  dd r = two_sum(x, -k * L0);
+  r = dd_add(r, two_prod(-k, L1));
+  r = dd_add(r, dd{__dmul_rn(-k, L2), 0.0});
+  // exp(r) = exp(r / 2^10)^(2^10); Taylor to degree 10 at |r / 2^10| < 3.4e-4 (tail < 1e-41)
+  r.hi = ldexp(r.hi, -10);
+  r.lo = ldexp(r.lo, -10);
+  const dd c[11] = {{1.0, 0.0},
+                    {1.0, 0.0},
+                    {0.5, 0.0},
+                    {0x1.5555555555555p-3, 0x1.5555555555555p-57},
+                    {0x1.5555555555555p-5, 0x1.5555555555555p-59},
+                    {0x1.1111111111111p-7, 0x1.1111111111111p-63},
+                    {0x1.6c16c16c16c17p-10, -0x1.f49f49f49f49fp-65},
+                    {0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-73},
+                    {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76},
+                    {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73},
+                    {0x1.27e4fb7789f5cp-22, 0x1.cbbc05b4fa99ap-76}};
+  dd e = c[10];
+#pragma unroll
+  for (int i = 9; i >= 0; --i) e = dd_add(dd_mul(e, r), c[i]);
+#pragma unroll
+  for (int i = 0; i < 10; ++i) e = dd_mul(e, e);
+  // hi = fl(hi + lo): the double nearest the ~1e-29-accurate value, i.e. the correctly
+  // rounded exp except within 1e-29 (relative) of a rounding midpoint; 2^k scaling is exact
+  // in the used range |x| <= 60
+  return ldexp(__dadd_rn(e.hi, e.lo), (int)k);
+}
+
+// sigmoid with the reference's clip and operation order (model.py:351-353)
 __device__ __forceinline__ double sigmoid_d(double x) {
   x = fmin(fmax(x, -60.0), 60.0);
-  return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+  return __ddiv_rn(1.0, __dadd_rn(1.0, exp_cr(-x)));
 }
 
 __device__ __forceinline__ double iou_d(const double* a, const double* b) {

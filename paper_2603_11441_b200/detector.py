@@ -19,6 +19,41 @@ import numpy as np
 from . import _native
 from .model import DetectorModel, _device, _stream_ptr, native_handle, raise_for_flags, text_encode
 from .pipeline import Detection, PipelineConfig, _require_classes
+from .tensors import device_mode, precision_code
+
+
+def _on_device(fn):
+    """Run a Detector method with its GPU as the current device: the C ABI allocates
+    workspaces and sets kernel attributes on the CURRENT device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        import torch
+
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **kw)
+
+    return wrapped
+
+
+def _on_device_gen(fn):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        import torch
+
+        gen = fn(self, *a, **kw)
+        while True:
+            with torch.cuda.device(self.device):
+                try:
+                    item = next(gen)
+                except StopIteration:
+                    return
+            yield item
+
+    return wrapped
 
 
 class Detector:
@@ -35,7 +70,12 @@ class Detector:
             self.chunks = [list(class_names)]
         self.class_names = list(class_names)
         self.device = device or _device()
-        self.handle = native_handle(model, self.device)
+        # the same precision semantics as run_batched (pipeline.py): the enc-dec runs the fp32-
+        # accumulate discipline or rejects the request; the backbone's discipline is the handle's
+        device_mode(self.cfg.encdec_mode)
+        self._bb_precision = precision_code(self.cfg.backbone_mode)
+        with torch.cuda.device(self.device):
+            self.handle = native_handle(model, self.device)
         self.lib = self.handle.lib
         emb = text_encode(model, self.class_names)
         self.text = [torch.from_numpy(np.stack(emb.stack(ch)).astype(np.float32)).to(self.device)
@@ -83,8 +123,14 @@ class Detector:
     def _enqueue_backbone(self, h, images, b, st: int) -> None:
         """dart_backbone of one batch into slot `b` on stream `st` (the call clears the flags)."""
         B = int(images.shape[0])
-        _native.check(self.lib.dart_backbone(h.ptr, images.data_ptr(), B, b["l0"].data_ptr(), b["l1"].data_ptr(),
-                                             b["l2"].data_ptr(), b["flags"].data_ptr(), st))
+        if self._bb_precision:
+            _native.check(self.lib.dart_model_set_precision(h.ptr, self._bb_precision))
+        try:
+            _native.check(self.lib.dart_backbone(h.ptr, images.data_ptr(), B, b["l0"].data_ptr(),
+                                                 b["l1"].data_ptr(), b["l2"].data_ptr(), b["flags"].data_ptr(), st))
+        finally:
+            if self._bb_precision:
+                _native.check(self.lib.dart_model_set_precision(h.ptr, 0))
 
     def _enqueue_decode(self, h, b, B: int, st: int, l0_ptr) -> None:
         """Class-batched enc-dec (one pass per n_max chunk) and post-processing of slot `b` on
@@ -127,6 +173,7 @@ class Detector:
                 b["kq"].data_ptr(), b["ks"].data_ptr(), b["pp"].data_ptr(), b["kf"].data_ptr(),
                 b["scratch"].data_ptr(), st))
 
+    @_on_device
     def detect_device(self, images):
         """images: device float32 [B, S, S, 3].  Enqueues backbone, class-batched enc-dec and
         post-processing on the current stream; returns the buffer dict (no sync)."""
@@ -188,6 +235,7 @@ class Detector:
         for h in ([self.handle] if p is None else p["h_bb"] + [p["h_dec"]]):
             self.lib.dart_reset_launch_count(h.ptr)
 
+    @_on_device
     def detect_device_pipelined(self, images):
         """Enqueue one batch (device float32 [B, S, S, 3]) into the two-stream pipeline; returns
         its slot buffers, valid once the returned event (recorded on the decode stream) has
@@ -213,6 +261,7 @@ class Detector:
         p["ev_dec"][k] = ev
         return b, ev
 
+    @_on_device
     def pipeline_join(self) -> None:
         """Make the caller's current stream wait for everything enqueued in the pipeline."""
         import torch
@@ -266,6 +315,7 @@ class Detector:
         self._gpipe = gp
         return gp
 
+    @_on_device
     def detect_device_graph(self, images):
         """One pipelined step through the captured graphs: the batch (device [B, S, S, 3]) is
         copied into input buffer k and G_k replayed on the current stream.  Returns the slot
@@ -279,6 +329,7 @@ class Detector:
         gp["graphs"][k].replay()
         return gp["slots"][1 - k]
 
+    @_on_device
     def graph_drain(self):
         """Decode the last batch fed to detect_device_graph (eager, current stream); returns its
         slot buffers."""
@@ -291,6 +342,7 @@ class Detector:
                              gp["slots"][k]["l0"].data_ptr())
         return gp["slots"][k]
 
+    @_on_device_gen
     def detect_stream(self, batches):
         """Generator over host (NumPy / CPU torch) or device image batches [B, S, S, 3]: yields
         one list of per-image detection lists per batch, in order, with the backbone of batch
@@ -329,6 +381,11 @@ class Detector:
                 src = arr
             if p["ev_dec"][k] is not None:
                 s_in.wait_event(p["ev_dec"][k])
+            # a device source may still be being produced on the caller's stream; and the caching
+            # allocator must not hand its block to anyone else before this copy has run
+            s_in.wait_stream(torch.cuda.current_stream(self.device))
+            if src.is_cuda:
+                src.record_stream(s_in)
             with torch.cuda.stream(s_in):
                 hs["dimg"].copy_(src, non_blocking=True)
             b, _ = self.detect_device_pipelined(hs["dimg"])
@@ -355,6 +412,7 @@ class Detector:
         return sum(t.numel() * t.element_size() for t in self.result_tensors(b).values())
 
     # ------------------------------------------------------------------ host API
+    @_on_device
     def detect(self, images) -> list[list[Detection]]:
         """images: [B, S, S, 3] or [S, S, 3] in [0, 1] (NumPy or pinned/host torch).  Returns
         one detection list per image, in the reference's order (class order, then NMS order)."""

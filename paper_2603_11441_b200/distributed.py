@@ -5,16 +5,18 @@ the CPU tests, with an oracle-backed engine standing in for the CUDA one):
 
 * image data parallelism -- images never interact: image i runs entirely on rank
   i mod W; no collective on the data path (`shard_images`, `gather_detections`).
-* class sharding for large N -- after the class-agnostic backbone, classes are
-  independent (reference model.py:559-564).  Each rank runs the backbone for its own
-  image, the W level-0 feature blocks are all-gathered ([T, F0] per image), every rank
-  decodes ITS class shard for all W images in one class-batched pass, and the raw
-  outputs are all-gathered so each image's owner post-processes all N classes
-  (identical semantics to run_batched, including cross-class NMS).
+* class sharding for large N -- after the class-agnostic backbone and the class-independent
+  enc-dec prefix (input projection + encoder layer-0 self-attention, model.py:513-517),
+  classes are independent (model.py:559-564).  Each rank runs backbone + prefix for its own
+  image, the W prefix outputs e1 ([T, d] per image) are all-gathered, every rank decodes
+  ITS class shard for all W images in one class-batched pass, and the raw outputs are
+  all-gathered so each image's owner post-processes all N classes (identical semantics to
+  run_batched, including cross-class NMS).
 
-The engine is anything with `backbone(images) -> l0 [B,T,F0]`, `decode(l0, names) ->
-(boxes [B,n,Q,4], scores [B,n,Q], presence [B,n])` and `postprocess(boxes, scores,
-presence, names, cfg) -> list[Detection]` on torch tensors (see `NativeEngine`).
+The engine is anything with `prefix(images) -> (e1 [B,T,d], flags int32 [1])`,
+`decode(e1, names) -> (boxes [B,n,Q,4], scores [B,n,Q], presence [B,n])`,
+`postprocess(boxes, scores, presence, names, cfg) -> list[Detection]` and
+`check_flags(int)` on torch tensors (see `NativeEngine`).
 """
 
 from __future__ import annotations
@@ -66,30 +68,30 @@ def gather_detections(local: dict, group=None) -> dict | None:
     return dict(sorted(merged.items()))
 
 
-def detect_class_sharded(engine, image, class_names, cfg, group=None):
-    """Class-sharded detection of one image per rank (W images in flight).
-
-    `image` is this rank's [1, S, S, 3] tensor; returns the detections for it.  Data
-    movement per round: all_gather of W x [T, F0] fp32 features, all_gather of the raw
-    outputs W x [W, N/W, Q, 5] fp64 (both tiny next to the decode FLOPs)."""
+def class_sharded_raw(engine, image, class_names, group=None):
+    """The collective part of `detect_class_sharded`, fully asynchronous on the device:
+    returns this rank's image's raw outputs over ALL classes (boxes [N, Q, 4], score logits
+    [N, Q], presence logits [N], float64) and the rank-reduced status flags (int32 [1])."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     plan = ClassShardPlan(len(class_names), world)
-    l0 = engine.backbone(image).contiguous()  # [1, T, F0]
-    gathered = [torch.empty_like(l0) for _ in range(world)]
-    dist.all_gather(gathered, l0, group=group)
-    l0_all = torch.cat(gathered)  # [W, T, F0], image w owned by rank w
+    e1, flags = engine.prefix(image)  # [1, T, d], int32 [1] (device, asynchronous)
+    e1 = e1.contiguous()
+    gathered = [torch.empty_like(e1) for _ in range(world)]
+    dist.all_gather(gathered, e1, group=group)
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    e1_all = torch.cat(gathered)  # [W, T, d], image w owned by rank w
     s, e = plan.bounds(rank)
     width = plan.width
     Q = engine.num_queries
-    boxes = torch.zeros((world, width, Q, 4), dtype=torch.float64, device=l0.device)
-    scores = torch.zeros((world, width, Q), dtype=torch.float64, device=l0.device)
-    pres = torch.zeros((world, width), dtype=torch.float64, device=l0.device)
+    boxes = torch.zeros((world, width, Q, 4), dtype=torch.float64, device=e1.device)
+    scores = torch.zeros((world, width, Q), dtype=torch.float64, device=e1.device)
+    pres = torch.zeros((world, width), dtype=torch.float64, device=e1.device)
     if e > s:
-        b, sc, p = engine.decode(l0_all, class_names[s:e])
+        b, sc, p = engine.decode(e1_all, class_names[s:e])
         boxes[:, : e - s] = b
         scores[:, : e - s] = sc
         pres[:, : e - s] = p
@@ -105,11 +107,30 @@ def detect_class_sharded(engine, image, class_names, cfg, group=None):
     my_boxes = mine[:, : 4 * Q].reshape(n, Q, 4).contiguous()
     my_scores = mine[:, 4 * Q: 5 * Q].contiguous()
     my_pres = mine[:, 5 * Q].contiguous()
-    return engine.postprocess(my_boxes, my_scores, my_pres, class_names, cfg)
+    return my_boxes, my_scores, my_pres, flags
+
+
+def detect_class_sharded(engine, image, class_names, cfg, group=None):
+    """Class-sharded detection of one image per rank (W images in flight).
+
+    `image` is this rank's [1, S, S, 3] tensor; returns the detections for it.  Each rank
+    runs the backbone and the class-independent enc-dec prefix (model.py:513-517) of its own
+    image; the W prefix outputs e1 [T, d] fp32 are all-gathered (5.3 MB per image at full
+    size; fp32 so the sharded outputs stay bitwise equal to run_batched); every rank decodes
+    ITS class shard for all W images in one class-batched pass; the raw outputs
+    (W x [W, N/W, Q, 5] fp64) are all-gathered so each image's owner post-processes all N
+    classes.  The backbone status flags are MAX-reduced across ranks with the features and
+    checked only after the results reach the host, so a bad image raises on every rank (no
+    rank left blocked in a collective) and there is no extra host synchronisation."""
+    my_boxes, my_scores, my_pres, flags = class_sharded_raw(engine, image, class_names, group)
+    dets = engine.postprocess(my_boxes, my_scores, my_pres, class_names, cfg)  # host results (synchronises)
+    engine.check_flags(int(flags.reshape(-1)[0].item()))
+    return dets
 
 
 class NativeEngine:
-    """The CUDA engine for the sharded modes: one model handle on this rank's GPU."""
+    """The CUDA engine for the sharded modes: one model handle on this rank's GPU.  Every
+    method but `postprocess` only enqueues work on the current stream (no host sync)."""
 
     def __init__(self, model, device=None):
         from .model import _device, native_handle
@@ -117,29 +138,80 @@ class NativeEngine:
         self.model = model
         self.device = device or _device()
         self.handle = native_handle(model, self.device)
+        self.lib = self.handle.lib
         self.num_queries = model.config.num_queries
+        self._bufs = {}
 
-    def backbone(self, images):
-        from .model import backbone_forward_batch
-
-        (l0, _, _), _ = backbone_forward_batch(self.model, images, check=True)
-        return l0
-
-    def decode(self, l0, names):
+    def _buffers(self, B: int):
         import torch
 
-        from .model import device_text, encdec_forward_device, text_encode
+        b = self._bufs.get(B)
+        if b is None:
+            cfg, dev = self.model.config, self.device
+            T, g = cfg.tokens, cfg.grid
+            b = self._bufs[B] = {
+                "l0": torch.empty((B, T, cfg.fpn_dims[0]), device=dev, dtype=torch.float32),
+                "l1": torch.empty((B, (g // 2) ** 2, cfg.fpn_dims[1]), device=dev, dtype=torch.float32),
+                "l2": torch.empty((B, (g // 4) ** 2, cfg.fpn_dims[2]), device=dev, dtype=torch.float32),
+            }
+        return b
+
+    def prefix(self, images):
+        """images [B, S, S, 3] device float32 -> (e1 [B, T, d] fp32, flags int32 [1]): the
+        backbone and the class-independent enc-dec prefix (dart_backbone + dart_encdec_prefix)."""
+        import torch
+
+        from . import _native
+        from .model import _stream_ptr
+
+        cfg = self.model.config
+        imgs = images.to(device=self.device, dtype=torch.float32).contiguous()
+        B = int(imgs.shape[0])
+        b = self._buffers(B)
+        flags = torch.zeros((1,), device=self.device, dtype=torch.int32)
+        e1 = torch.empty((B, cfg.tokens, cfg.text_dim), device=self.device, dtype=torch.float32)
+        st = _stream_ptr(self.device)
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.dart_backbone(self.handle.ptr, imgs.data_ptr(), B, b["l0"].data_ptr(),
+                                                 b["l1"].data_ptr(), b["l2"].data_ptr(), flags.data_ptr(), st))
+            _native.check(self.lib.dart_encdec_prefix(self.handle.ptr, None, B, e1.data_ptr(), st))
+        return e1, flags
+
+    def decode(self, e1, names, out=None):
+        """e1 [B, T, d] fp32 (device) x names -> raw outputs (boxes [B,n,Q,4], score logits [B,n,Q],
+        presence logits [B,n]) float64 on the device (dart_encdec_from_prefix)."""
+        import torch
+
+        from . import _native
+        from .model import _stream_ptr, device_text, text_encode
 
         emb = text_encode(self.model, list(names))
         text = device_text(self.model, emb.stack(list(names)), self.device)
-        B = int(l0.shape[0])
-        raw = encdec_forward_device(self.model, l0, text, B, len(names), with_query_features=False)
-        n, Q = len(names), self.num_queries
-        return (raw.d_boxes.reshape(B, n, Q, 4), raw.d_score_logits.reshape(B, n, Q),
-                raw.d_presence_logits.reshape(B, n))
+        B, n, Q = int(e1.shape[0]), len(names), self.num_queries
+        if out is None:
+            out = (torch.empty((B, n, Q, 4), device=self.device, dtype=torch.float64),
+                   torch.empty((B, n, Q), device=self.device, dtype=torch.float64),
+                   torch.empty((B, n), device=self.device, dtype=torch.float64))
+        boxes, scores, pres = out
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.dart_encdec_from_prefix(
+                self.handle.ptr, e1.contiguous().data_ptr(), B, text.contiguous().data_ptr(), n, boxes.data_ptr(),
+                scores.data_ptr(), pres.data_ptr(), None, _stream_ptr(self.device)))
+        return boxes, scores, pres
+
+    def postprocess_device(self, boxes, scores, presence, cfg):
+        from .pipeline import postprocess_device
+
+        return postprocess_device(boxes, scores, presence, cfg, self.model)
 
     def postprocess(self, boxes, scores, presence, names, cfg):
-        from .pipeline import detections_from_result, postprocess_device
+        from .pipeline import detections_from_result
 
-        res = postprocess_device(boxes, scores, presence, cfg, self.model)
+        res = self.postprocess_device(boxes, scores, presence, cfg)
         return detections_from_result(res.to_host(), boxes.cpu().numpy(), list(names), cfg.cross_class_nms)
+
+    @staticmethod
+    def check_flags(flags: int) -> None:
+        from .model import raise_for_flags
+
+        raise_for_flags(flags)

@@ -149,17 +149,26 @@ class DetectorModel:
 class FpnFeatures:
     """Three class-agnostic feature levels plus provenance (model.py:152-166).
 
-    The levels live on the GPU (`device_levels`, float32 [T_l, F_l] torch tensors);
-    `.levels` is the reference-compatible float64 NumPy view, copied on first access.
-    Non-finite features raise ValueError at construction, as in the reference."""
+    The levels are GPU tensors (`device_levels`, float32 [T_l, F_l]) when produced by
+    `backbone_forward`, or host arrays when a caller builds the record itself (the reference's
+    distill.py:109-113 does); `.levels` is the reference-compatible float64 NumPy view, copied
+    on first access.  Non-finite features raise ValueError at construction, as in the
+    reference (the backbone's device-side finiteness flag is checked before it builds one)."""
 
     __slots__ = ("device_levels", "model_seed", "mode", "plan_id", "_host", "_l0_resident")
 
-    def __init__(self, device_levels, model_seed: int, mode: PrecisionMode, plan_id: str | None = None,
-                 l0_resident: bool = False):
-        if len(device_levels) != 3:
+    def __init__(self, levels, model_seed: int, mode: PrecisionMode, plan_id: str | None = None,
+                 l0_resident: bool = False, _finite_checked: bool = False):
+        if len(levels) != 3:
             raise ValueError("fpn features must carry exactly 3 levels")
-        self.device_levels = tuple(device_levels)
+        levels = tuple(levels)
+        on_device = [hasattr(t, "is_cuda") and t.is_cuda for t in levels]
+        if not _finite_checked:
+            for t, dev in zip(levels, on_device):
+                finite = bool(t.isfinite().all().item()) if dev else bool(np.all(np.isfinite(np.asarray(t))))
+                if not finite:
+                    raise ValueError("fpn features must be finite")
+        self.device_levels = levels
         self.model_seed = model_seed
         self.mode = mode
         self.plan_id = plan_id
@@ -169,7 +178,9 @@ class FpnFeatures:
     @property
     def levels(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         if self._host is None:
-            self._host = tuple(t.detach().double().cpu().numpy() for t in self.device_levels)
+            self._host = tuple(
+                t.detach().double().cpu().numpy() if hasattr(t, "detach") else np.asarray(t, dtype=np.float64)
+                for t in self.device_levels)
         return self._host
 
 
@@ -466,8 +477,9 @@ def backbone_forward(model: DetectorModel, image: np.ndarray, mode: PrecisionMod
     image = _check_image(model.config, image)
     if image.ndim != 3:
         raise ValueError(f"image shape {image.shape} does not match {(model.config.image_size,) * 2 + (3,)}")
-    (l0, l1, l2), _ = backbone_forward_batch(model, image, mode)
-    return FpnFeatures((l0[0], l1[0], l2[0]), model.config.seed, device_mode(mode, backbone=True), model.plan_id)
+    (l0, l1, l2), _ = backbone_forward_batch(model, image, mode)  # raises on the device flags
+    return FpnFeatures((l0[0], l1[0], l2[0]), model.config.seed, device_mode(mode, backbone=True), model.plan_id,
+                       _finite_checked=True)
 
 
 def _text_rows(name: str, text_tokens: int) -> list[int]:

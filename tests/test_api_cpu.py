@@ -88,3 +88,21 @@ def test_host_iou_matches_oracle():
     for _ in range(200):
         a, b = rng.uniform(0, 1, 4), rng.uniform(0, 1, 4)
         assert D.box_iou(a, b) == O.box_iou(a, b)
+
+
+def test_fpn_features_host_arrays_and_finiteness():
+    """Reference model.py:152-166: FpnFeatures built from host arrays (as distill.py:109-113 does)
+    exposes float64 `.levels`, and any non-finite level raises ValueError at construction."""
+    import paper_2603_11441_b200 as D
+
+    lv = (np.ones((16, 8), np.float32), np.zeros((4, 8)), np.full((1, 8), 2.0))
+    f = D.FpnFeatures(lv, 0, D.PrecisionMode.FP32)
+    assert all(a.dtype == np.float64 for a in f.levels)
+    np.testing.assert_array_equal(f.levels[0], np.ones((16, 8)))
+    for bad in (np.nan, np.inf, -np.inf):
+        b = lv[1].copy()
+        b[0, 0] = bad
+        with pytest.raises(ValueError, match="finite"):
+            D.FpnFeatures((lv[0], b, lv[2]), 0, D.PrecisionMode.FP32)
+    with pytest.raises(ValueError):
+        D.FpnFeatures(lv[:2], 0, D.PrecisionMode.FP32)

@@ -24,13 +24,15 @@ class OracleEngine:
         self.P = O.build_params(self.cfg)
         self.num_queries = self.cfg.num_queries
 
-    def backbone(self, images):
-        l0, _, _ = self.O.backbone(self.P, self.cfg, images[0].numpy())
-        return torch.from_numpy(l0)[None]
+    def prefix(self, images):
+        img = images[0].numpy()
+        flag = int(img.min() < 0 or img.max() > 1)  # like the device range flag: compute anyway, raise later
+        l0, _, _ = self.O.backbone(self.P, self.cfg, np.clip(img, 0.0, 1.0))
+        return torch.from_numpy(self.O.encoder_prefix(self.P, self.cfg, l0))[None], torch.tensor([flag], dtype=torch.int32)
 
-    def decode(self, l0, names):
+    def decode(self, e1, names):
         texts = [self.O.text_embedding(self.P, self.cfg, n) for n in names]
-        outs = [self.O.encdec(self.P, self.cfg, l0[w].numpy(), texts) for w in range(l0.shape[0])]
+        outs = [self.O.encdec(self.P, self.cfg, None, texts, e1=e1[w].numpy()) for w in range(e1.shape[0])]
         boxes = torch.from_numpy(np.stack([o[1] for o in outs]))
         scores = torch.from_numpy(np.stack([o[3] for o in outs]))
         pres = torch.from_numpy(np.stack([o[2] for o in outs]))
@@ -39,6 +41,11 @@ class OracleEngine:
     def postprocess(self, boxes, scores, presence, names, cfg):
         return self.O.postprocess(boxes.numpy(), scores.numpy(), presence.numpy(), presence_thr=cfg["p"],
                                   score_thr=cfg["s"], cross_class=cfg["x"])
+
+    @staticmethod
+    def check_flags(flags):
+        if flags:
+            raise ValueError("image values must lie in [0, 1]")
 
 
 NAMES = ["car", "person", "dog", "cat", "bus"]
@@ -97,6 +104,43 @@ def test_class_sharded_matches_single_process():
                 assert abs(a[3] - b[3]) < 1e-12
     assert got[0][1] == {0: "img0@0", 1: "img1@1", 2: "img2@0", 3: "img3@1", 4: "img4@0"}
     assert got[1][1] is None
+
+
+def _bad_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import dart_oracle as O
+
+        eng = OracleEngine()
+        img, _ = O.scene(100 + rank, 64, num_classes=3)
+        if rank == 1:
+            img = img.copy()
+            img[0, 0, 0] = 1.5  # out of range on rank 1 only
+        try:
+            detect_class_sharded(eng, torch.from_numpy(img)[None], NAMES, {"p": 0.0, "s": 0.0, "x": False})
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_class_sharded_bad_image_raises_on_every_rank():
+    """Reference model.py:432-433: a value outside [0, 1] raises ValueError.  In class-sharded
+    mode the flag is reduced across ranks, so every rank raises (none is left in a collective)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bad_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: "image values must lie in [0, 1]", 1: "image values must lie in [0, 1]"}
 
 
 def test_shard_plan_covers_all_classes():

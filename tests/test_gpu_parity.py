@@ -52,24 +52,109 @@ def dets_rows(dets):
     return np.array([[d.class_id, d.query, *d.box, d.score, d.presence] for d in dets], dtype=np.float64).reshape(-1, 8)
 
 
-def check_decisions(g, raw, delta):
-    """Contract (3) with gates open: one detection per class survives when all boxes overlap;
-    compare labels, counts and the kept query index under the margin rule."""
+# Tensor gates per golden config: ~3x the errors measured on the B200,
+# far inside SURVEY 8(c)(1)'s bf16-emulation bounds (toy 5.2e-3 / 1.46e-2 / 1.12e-2, full size
+# 5.1e-3 / 2.0e-2 / 2.0e-3 for box / score logit / presence logit).
+TOL = {  # L0 max rel err, |d box|, |d score logit|, |d presence logit|
+    "A": (6e-3, 1.5e-3, 6e-3, 4e-3),
+    "A2": (6e-3, 1.5e-3, 6e-3, 4e-3),
+    "B": (3e-3, 1e-3, 3e-3, 2e-3),
+    "C": (3e-3, 1e-3, 3e-3, 2e-3),
+}
+
+
+def _logit(p):
+    if p <= 0.0:
+        return -np.inf
+    if p >= 1.0:
+        return np.inf
+    return float(np.log(p / (1.0 - p)))
+
+
+def _iou_matrix(b):
+    x0, x1 = b[:, 0] - b[:, 2] / 2, b[:, 0] + b[:, 2] / 2
+    y0, y1 = b[:, 1] - b[:, 3] / 2, b[:, 1] + b[:, 3] / 2
+    iw = np.minimum(x1[:, None], x1[None]) - np.maximum(x0[:, None], x0[None])
+    ih = np.minimum(y1[:, None], y1[None]) - np.maximum(y0[:, None], y0[None])
+    inter = np.where((iw > 0) & (ih > 0), iw * ih, 0.0)
+    area = b[:, 2] * b[:, 3]
+    return inter / (area[:, None] + area[None] - inter)
+
+
+def _class_decidable(g, c, cfg, ds, dp, db):
+    """the reference's decisions for class c are decidable at error levels
+    (ds, dp, db) when the presence gate, every score gate, every ordering between a kept
+    detection and a candidate it suppresses, and every IoU-vs-threshold test have margins
+    larger than the errors."""
+    pl = float(g["presence_logits"][c])
+    if abs(pl - _logit(cfg.presence_threshold)) <= dp:
+        return False
+    if 1.0 / (1.0 + np.exp(-pl)) < cfg.presence_threshold:
+        return True  # skipped class, decidably
+    s = g["score_logits"][c]
+    gate = _logit(cfg.score_threshold)
+    if np.any(np.abs(s - gate) <= ds):
+        return False
+    cand = np.nonzero(s > gate)[0] if np.isfinite(gate) else np.arange(s.shape[0])
+    if cand.size == 0:
+        return True
+    order = cand[np.lexsort((cand, -s[cand]))]
+    boxes = g["boxes"][c][order]
+    iou = _iou_matrix(boxes)
+    wmin = max(1e-6, float(boxes[:, 2:].min()))
+    diou = 8.0 * db / wmin  # conservative IoU sensitivity to a db box error
+    kept = []
+    for i in range(order.size):
+        sup = [k for k in kept if iou[k, i] >= cfg.nms_iou_threshold]
+        if any(abs(iou[k, i] - cfg.nms_iou_threshold) <= diou for k in kept):
+            return False
+        if sup:
+            if min(s[order[k]] - s[order[i]] for k in sup) <= ds:
+                return False  # a suppressor and its victim could swap places
+        else:
+            kept.append(i)
+    return True
+
+
+def check_decisions(g, raw, ds, dp, db, keys=None):
+    """Contract (3) for every threshold set stored in the golden (gates open, the reference's
+    defaults, a mid setting; with and without cross-class NMS): labels, per-class kept
+    counts and kept query indices must equal the reference's exactly for every decidable class
+    (margins > the measured errors); an undecidable class's pick must lie in the reference's
+    2*ds tie set.  Returns the decided fraction of (class, threshold set) decisions."""
     names = [str(n) for n in g["names"]]
-    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
-    got = D.postprocess(raw, names, cfg)
-    ref = g["dets_open"]
-    assert [d.class_id for d in got] == [int(r[0]) for r in ref]
-    decided = 0
-    for d, r in zip(got, ref):
-        c, q_ref = int(r[0]), int(r[1])
-        s = g["score_logits"][c]
-        if d.query == q_ref:
-            decided += 1
+    n = len(names)
+    decided = total = 0
+    keys = keys or [k for k in g if k.startswith("dets_") and not k.endswith("_cfg")]
+    for key in keys:
+        kw = json.loads(str(g[key + "_cfg"]))
+        xc = key.endswith("_xc")
+        cfg = D.PipelineConfig(cross_class_nms=xc, **kw)
+        got = D.postprocess(raw, names, cfg)
+        ref = g[key]
+        dec = [_class_decidable(g, c, cfg, ds, dp, db) for c in range(n)]
+        if xc:  # cross-class NMS couples the classes: decide the whole list at once
+            total += 1
+            if all(dec):
+                decided += 1
+                assert [(d.class_id, d.query) for d in got] == [(int(r[0]), int(r[1])) for r in ref], key
             continue
-        # undecidable pick: the device winner must be inside the oracle's delta-tie set
-        assert s[q_ref] - s[d.query] <= 2 * delta, (c, q_ref, d.query, s[q_ref] - s[d.query], delta)
-    return decided / max(1, len(ref))
+        for c in range(n):
+            total += 1
+            gq = [d.query for d in got if d.class_id == c]
+            rq = [int(r[1]) for r in ref if int(r[0]) == c]
+            if dec[c]:
+                decided += 1
+                assert gq == rq, (key, c, gq, rq)
+            elif rq:
+                s = g["score_logits"][c]
+                assert gq and s[rq[0]] - s[gq[0]] <= 2 * ds, (key, c, gq, rq)
+    return decided / max(1, total)
+
+
+def raw_errors(g, raw, rows=slice(None)):
+    return (np.abs(raw.boxes[rows] - g["boxes"]).max(), np.abs(raw.score_logits[rows] - g["score_logits"]).max(),
+            np.abs(raw.presence_logits[rows] - g["presence_logits"]).max())
 
 
 @pytest.mark.parametrize("name", ["A", "A2"])
@@ -85,13 +170,11 @@ def test_toy_end_to_end(name):
     assert cosine(fpn.levels[2][g["L2_rows"]], g["L2"]) > 0.9999
     names = [str(n) for n in g["names"]]
     raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
-    err_b = np.abs(raw.boxes - g["boxes"]).max()
-    err_s = np.abs(raw.score_logits - g["score_logits"]).max()
-    err_p = np.abs(raw.presence_logits - g["presence_logits"]).max()
-    print(f"{name}: box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}")
-    # toy bf16 emulation bounds are 5.2e-3 / 1.46e-2 / 1.12e-2; gate at 2x
-    assert err_b < 1.04e-2 and err_s < 2.9e-2 and err_p < 2.2e-2
-    check_decisions(g, raw, err_s)
+    err_b, err_s, err_p = raw_errors(g, raw)
+    frac = check_decisions(g, raw, err_s, err_p, err_b)
+    print(f"{name}: box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}; decided {frac:.2f}")
+    _, tb, ts, tp = TOL[name]
+    assert err_b < tb and err_s < ts and err_p < tp
 
 
 @pytest.mark.parametrize("name", ["A", "A2", "B", "C"])
@@ -206,15 +289,14 @@ def test_full_width_parity(name):
     e0 = np.abs(l0 - g["L0"]).max() / np.abs(g["L0"]).max()
     names = [str(n) for n in g["names"]]
     raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
-    err_b = np.abs(raw.boxes - g["boxes"]).max()
-    err_s = np.abs(raw.score_logits - g["score_logits"]).max()
-    err_p = np.abs(raw.presence_logits - g["presence_logits"]).max()
-    frac = check_decisions(g, raw, err_s)
+    err_b, err_s, err_p = raw_errors(g, raw)
+    frac = check_decisions(g, raw, err_s, err_p, err_b)
     print(f"{name}: L0 cos {c0:.6f} rel {e0:.2e}; box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}; "
           f"decided {frac:.2f}")
-    # SURVEY 8(c)(1) full-size bf16 emulation: cos 0.99992, |dbox| 5.1e-3, |dscore| 2.0e-2; gate at 2x
-    assert c0 > 0.9998 and e0 < 3.2e-2
-    assert err_b < 1.02e-2 and err_s < 4.0e-2 and err_p < 4.0e-2
+    te, tb, ts, tp = TOL[name]
+    assert c0 > 0.99999 and e0 < te
+    assert err_b < tb and err_s < ts and err_p < tp
+    assert frac == 1.0  # every decision of B and C is decidable at the measured error levels
 
 
 def hashlib_image(img):
@@ -235,9 +317,9 @@ def test_many_classes_class_shared_text_attention():
     allnames = extra[:7] + names + extra[7:]
     raw = D.encdec_forward(model, fpn, D.text_encode(model, allnames).stack(allnames))
     sl = slice(7, 7 + len(names))
-    assert np.abs(raw.boxes[sl] - g["boxes"]).max() < 1.02e-2
-    assert np.abs(raw.score_logits[sl] - g["score_logits"]).max() < 4.0e-2
-    assert np.abs(raw.presence_logits[sl] - g["presence_logits"]).max() < 4.0e-2
+    eb, es, ep = raw_errors(g, raw, sl)
+    _, tb, ts, tp = TOL["B"]
+    assert eb < tb and es < ts and ep < tp
 
 
 def test_backbone_determinism_batch_independence_and_identity_trunk():
@@ -328,3 +410,72 @@ def test_ragged_class_counts(n, n_max):
     ref = D.run_batched(model, image, names, D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0))
     assert dets == ref
     assert sorted({d.class_id for d in dets}) == list(range(n))  # gates open: every class keeps >= 1
+
+
+@pytest.fixture(scope="module")
+def model_C():
+    g = load_golden("C")
+    return g, model_for(g)
+
+
+def test_full_size_80_classes(model_C):
+    """BASELINE configs[2] (N=80, model.py:559-564): golden C's four classes embedded
+    at spread positions (0, 27, 53, 79) of an 80-class batch, 76 COCO names elsewhere.  Their rows
+    equal the N=4 run's rows bitwise (classes never mix), stay within C's gates, and every kept
+    query / label of those classes equals the reference's."""
+    import bench
+
+    g, model = model_C
+    image = scene_for("C", model.config)
+    fpn = D.backbone_forward(model, image)
+    names = [str(n) for n in g["names"]]
+    pos = [0, 27, 53, 79]
+    others = [c for c in bench.coco80() if c not in names]
+    allnames = list(others[:76])
+    for p, nme in zip(pos, names):
+        allnames.insert(p, nme)
+    assert len(allnames) == 80 and [allnames[p] for p in pos] == names
+    emb = D.text_encode(model, allnames)
+    raw80 = D.encdec_forward(model, fpn, emb.stack(allnames))
+    raw4 = D.encdec_forward(model, fpn, emb.stack(names))
+    np.testing.assert_array_equal(raw80.boxes[pos], raw4.boxes)
+    np.testing.assert_array_equal(raw80.score_logits[pos], raw4.score_logits)
+    np.testing.assert_array_equal(raw80.presence_logits[pos], raw4.presence_logits)
+    err_b, err_s, err_p = raw_errors(g, raw80, pos)
+    _, tb, ts, tp = TOL["C"]
+    assert err_b < tb and err_s < ts and err_p < tp
+    cfg = D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0)
+    dets = D.postprocess(raw80, allnames, cfg)
+    assert sorted({d.class_id for d in dets}) == list(range(80))
+    sub = [(pos.index(d.class_id), d.query) for d in dets if d.class_id in pos]
+    assert sub == [(int(r[0]), int(r[1])) for r in g["dets_open"]]
+    # run_batched over the same 80 names, with and without n_max chunking (16 = the paper's N_max)
+    for n_max in (None, 16):
+        rb = D.run_batched(model, image, allnames, D.PipelineConfig(presence_threshold=0.0, score_threshold=0.0,
+                                                                     n_max=n_max))
+        assert rb == dets
+
+
+def test_full_size_detect_stream(model_C):
+    """The timed public API (Detector.detect_stream: pinned host images, inter-frame pipeline,
+    tcgen05 attention at hd 80 and hd 16) against golden C at every stored threshold set."""
+    from paper_2603_11441_b200.detector import Detector
+
+    g, model = model_C
+    image = scene_for("C", model.config).astype(np.float32)
+    names = [str(n) for n in g["names"]]
+    _, tb, ts, tp = TOL["C"]
+    for key in ("dets_open", "dets_default", "dets_mid", "dets_open_xc", "dets_mid_xc"):
+        cfg = D.PipelineConfig(cross_class_nms=key.endswith("_xc"), **json.loads(str(g[key + "_cfg"])))
+        det = Detector(model, names, cfg)
+        outs = list(det.detect_stream([image, image, image]))  # 3 frames through the pipeline
+        assert all(o == outs[0] for o in outs)
+        got = outs[0][0]
+        ref = g[key]
+        assert [(d.class_id, d.query) for d in got] == [(int(r[0]), int(r[1])) for r in ref], key
+        for d, r in zip(got, ref):
+            assert np.abs(np.array(d.box) - r[2:6]).max() < tb
+            assert abs(d.score - r[6]) < ts / 4 and abs(d.presence - r[7]) < tp / 4  # sigmoid' <= 1/4
+        # and identical to the drop-in run_batched path
+        assert [(d.class_id, d.query, d.box, d.score) for d in got] == \
+            [(d.class_id, d.query, d.box, d.score) for d in D.run_batched(model, scene_for("C", model.config), names, cfg)]
