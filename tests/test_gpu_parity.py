@@ -56,8 +56,10 @@ def dets_rows(dets):
 # far inside SURVEY 8(c)(1)'s bf16-emulation bounds (toy 5.2e-3 / 1.46e-2 / 1.12e-2, full size
 # 5.1e-3 / 2.0e-2 / 2.0e-3 for box / score logit / presence logit).
 TOL = {  # L0 max rel err, |d box|, |d score logit|, |d presence logit|
-    "A": (6e-3, 1.5e-3, 6e-3, 4e-3),
-    "A2": (6e-3, 1.5e-3, 6e-3, 4e-3),
+    # measured (B200, round 2): A 1.5e-4 / 4.8e-4 / 2.1e-4, A2 2.3e-4 / 7.8e-4 / 8.1e-4,
+    # B L0 6.6e-4, 3.0e-4 / 5.3e-4 / 8.4e-4, C L0 7.9e-4, 2.3e-4 / 9.0e-4 / 6.5e-4
+    "A": (6e-3, 7e-4, 2.5e-3, 2.5e-3),
+    "A2": (6e-3, 7e-4, 2.5e-3, 2.5e-3),
     "B": (3e-3, 1e-3, 3e-3, 2e-3),
     "C": (3e-3, 1e-3, 3e-3, 2e-3),
 }
