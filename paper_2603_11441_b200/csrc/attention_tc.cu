@@ -102,7 +102,7 @@ __device__ __forceinline__ void wait_sel(uint64_t* bar, uint32_t parity, int tag
     mbar_wait_dbg(bar, parity, tag, dbg);
 }
 
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN>
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK>
 __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREADS, CTAS)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
   // SPIN bit 4 (PROD): the debug / trace / microbenchmark hooks compiled out -- every kernel
@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   const int warp = warp_id(), lane = lane_id();
   const int q_tiles = (a.Lq + BQ - 1) / BQ;
   const int n_items = q_tiles * a.heads * a.items;
-  const int nkv = a.Lkv / BKV;
+  // MASK: Lkv not a multiple of BKV (decoder self-attention over 201 tokens, text cross-attention
+  // over 32): the last key tile is partial and its keys >= Lkv are masked to P = 0
+  const int nkv = MASK ? (a.Lkv + BKV - 1) / BKV : a.Lkv / BKV;
   // TMA and MMA warps (SMSPs 0 / 1).  The tcgen05.mma stream costs its SMSP issue time, which the
   // softmax warp sharing that SMSP loses; the second CTA of an SM (blocks are placed round-robin,
   // so blockIdx >= grid/2) swaps the two roles to put its MMA issue on the other SMSP.
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           const int qt = item % q_tiles;
           const int h = (item / q_tiles) % a.heads;
           const int z = item / (q_tiles * a.heads) + a.z_base;
-          const int row0 = z * a.Lkv;
+          const int row0 = (a.kv_mod > 0 ? z % a.kv_mod : z) * a.Lkv;  // kv_mod: K/V shared per class
           if (do_qk) {
             const int qb = p_it & 1;
             mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, dbg);
@@ -361,6 +363,14 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             float v[L::COLS];
             tmem_ld_cols<L::COLS>(sbase, v);
             tmem_ld_wait();
+            if constexpr (MASK) {  // keys past Lkv in a partial last tile: score -inf -> P = 0
+              const int valid = a.Lkv - j * BKV - part * L::COLS;
+              if (valid < L::COLS) {
+  #pragma unroll
+                for (int k = 0; k < L::COLS; ++k)
+                  if (k >= valid) v[k] = -INFINITY;
+              }
+            }
             uint32_t p[L::COLS / 2];
             if (PASS == 0) {
               if (j == 0) {
@@ -480,10 +490,10 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
 
 // Kernel variants per head dim; variant 0 is the production choice, the others exist for A/B
 // measurement (DART_FA_VARIANT, scripts/bench_attn.py).
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN>
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK = false>
 int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
   using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
-  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN>;
+  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN, MASK>;
   static std::atomic<uint64_t> smem_set{0};
   if (const cudaError_t e = set_smem_once(smem_set, kern, Lay::TOTAL); e != cudaSuccess) return (int)e;
   // items of one launch: each CTA may own at most ATTN_TC_MAX_LOCAL_ITEMS (overflow bitmask)
@@ -555,11 +565,18 @@ int kv_tile_of(int hd, int var) {
 
 void attention_tc_set_variant(int v) { g_fa_variant = v < 0 ? 0 : v; }
 
-int attention_tc_kv_tile(int head_dim) { return kv_tile_of(head_dim, fa_variant()); }
+// Short key sets at hd 16 (the encoder's text cross-attention over L_t = 32 tokens, model.py:518)
+// run on 32-key tiles at 4 CTAs per SM (TMEM 2 x 32 + 32 columns per CTA).
+constexpr int SHORT_KV = 32;
+
+int attention_tc_kv_tile(int head_dim, int Lkv) {
+  if (head_dim == 16 && Lkv <= SHORT_KV) return SHORT_KV;
+  return kv_tile_of(head_dim, fa_variant());
+}
 
 bool attention_tc_supported(int head_dim, int Lkv) {
-  const int t = attention_tc_kv_tile(head_dim);
-  return t > 0 && Lkv % t == 0 && Lkv >= t;
+  const int t = attention_tc_kv_tile(head_dim, Lkv);
+  return t > 0 && Lkv >= 1 && (Lkv % t == 0 || fa_variant() == 0);  // ragged Lkv: masked production kernel
 }
 
 int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
@@ -573,12 +590,20 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
   // the production instantiations (SPIN bit 4) carry no debug / trace / microbenchmark hooks;
   // a launch that asks for one of them runs the hooked twin (identical arithmetic)
   const bool hooks = a.dbg != nullptr || a.trace != nullptr || a.softmax_only != 0;
-  if (head_dim == 80)
+  if (head_dim == 80) {
+    if (a.Lkv % 64 != 0) return launch_v<80, 64, 3, 2, 2, 1, 0, 16, 0, true>(tmQ, tmKV, a, num_sms, stream);
     return hooks ? launch_v<80, 64, 3, 2, 2, 1, 0, 0, 0>(tmQ, tmKV, a, num_sms, stream)
                  : launch_v<80, 64, 3, 2, 2, 1, 0, 16, 0>(tmQ, tmKV, a, num_sms, stream);
-  if (head_dim == 16)
+  }
+  if (head_dim == 16) {
+    if (a.Lkv <= SHORT_KV)  // text cross-attention: one (possibly partial) 32-key tile per item
+      return a.Lkv == SHORT_KV ? launch_v<16, SHORT_KV, 2, 4, 2, 1, 0, 16, 0>(tmQ, tmKV, a, num_sms, stream)
+                               : launch_v<16, SHORT_KV, 2, 4, 2, 1, 0, 16, 0, true>(tmQ, tmKV, a, num_sms, stream);
+    if (a.Lkv % 96 != 0)  // decoder self-attention (201 = 2 x 96 + 9 keys)
+      return launch_v<16, 96, 4, 2, 2, 1, 6, 16, 0, true>(tmQ, tmKV, a, num_sms, stream);
     return hooks ? launch_v<16, 96, 4, 2, 2, 1, 6, 0, 0>(tmQ, tmKV, a, num_sms, stream)
                  : launch_v<16, 96, 4, 2, 2, 1, 6, 16, 0>(tmQ, tmKV, a, num_sms, stream);
+  }
   return (int)cudaErrorInvalidValue;
 }
 

@@ -111,11 +111,13 @@ long long* g_attn_trace = nullptr;
 // tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
 // [items*Lkv, kv_ld] (k at k_col, v at v_col), output [items*Lq, o_ld] at column h*hd.
 int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv_ld, int k_col, int v_col, __half* o,
-            int o_ld, int items, int heads, int Lq, int Lkv, int hd, int num_sms, cudaStream_t s, int* dbg = nullptr) {
+            int o_ld, int items, int heads, int Lq, int Lkv, int hd, int num_sms, cudaStream_t s, int* dbg = nullptr,
+            int kv_mod = 0) {
   CUtensorMap tq, tkv;  // maps cover exactly the used column ranges
   const int q_inner = q_col + heads * hd, kv_inner = (k_col > v_col ? k_col : v_col) + heads * hd;
+  const int kv_items = kv_mod > 0 ? kv_mod : items;
   if (!make_tmap_ex(&tq, qbuf, q_inner, (uint64_t)items * Lq, q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
-      !make_tmap_ex(&tkv, kvbuf, kv_inner, (uint64_t)items * Lkv, kv_ld, 16, attention_tc_kv_tile(hd),
+      !make_tmap_ex(&tkv, kvbuf, kv_inner, (uint64_t)kv_items * Lkv, kv_ld, 16, attention_tc_kv_tile(hd, Lkv),
                     CU_TENSOR_MAP_SWIZZLE_32B))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (attention)");
   AttnTcArgs a;
@@ -132,6 +134,7 @@ int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv
   a.dbg = dbg;
   a.force_safe = g_attn_force_safe;
   a.trace = g_attn_trace;
+  a.kv_mod = kv_mod;
   {
     const char* e = getenv("DART_FA_SOFTMAX_ONLY");  // microbenchmarks: 1 softmax alone, 2 MMA alone
     a.softmax_only = e ? atoi(e) : 0;
@@ -574,16 +577,18 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
     return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
   }
   RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
-  if (tc_attention_enabled() && sp.kv_mod == 0 && attention_tc_supported(hd, Lk) &&
+  if (tc_attention_enabled() && attention_tc_supported(hd, Lk) &&
       (sp.kv16 == nullptr || sp.kv_batch_stride == (long long)Lk * sp.kv_tok_stride)) {
-    // tcgen05 path: encoder self-attention (T x T) and decoder cross-attention (201 x T)
+    // tcgen05 path: encoder self-attention (T x T), decoder cross-attention (201 x T) and the
+    // encoder's text cross-attention (T x 32, K/V of class c shared by every image: kv_mod = N)
     if (sp.kv16 == nullptr) {
       RUN(gemm(m, h, rows, D, w.kv, EPI_F16, epi_out(kv, 2 * D), s));
       m->launches++;
       RUN(attn_tc(q, D, 0, kv, 2 * D, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
     } else {
       m->launches++;
-      RUN(attn_tc(q, D, 0, sp.kv16, sp.kv_tok_stride, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
+      RUN(attn_tc(q, D, 0, sp.kv16, sp.kv_tok_stride, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s, nullptr,
+                  sp.kv_mod));
     }
     return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
   }

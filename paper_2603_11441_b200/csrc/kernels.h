@@ -110,7 +110,7 @@ bool attention_short_supported(const AttnArgs& a, int head_dim);
 
 // tcgen05 flash attention over contiguous row blocks of a token-major QKV buffer.
 struct AttnTcArgs {
-  int Lq, Lkv;                 // query / key rows per item; Lkv a multiple of attention_tc_kv_tile(hd)
+  int Lq, Lkv;                 // query / key rows per item (a partial last key tile is masked)
   int heads, items;
   int q_col, k_col, v_col;     // column offsets of q / k / v in the QKV buffer
   __half* o;                   // [items * L, o_ld]
@@ -121,9 +121,10 @@ struct AttnTcArgs {
   int z_base = 0;              // first item of this launch (items are chunked on the host)
   int softmax_only = 0;        // microbenchmark: softmax warps run on stale S without MMA / TMA
   long long* trace = nullptr;  // microbenchmark: CTA 0 clock64 stamps [7][256] of the first 256 tiles
+  int kv_mod = 0;              // > 0: item z reads K/V item z % kv_mod (text K/V shared by a class's images)
 };
 constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
-int attention_tc_kv_tile(int head_dim);  // key tile of the selected variant (64 hd 80, 96 hd 16), 0 = unsupported
+int attention_tc_kv_tile(int head_dim, int Lkv);  // key tile (64 hd 80, 96 hd 16, 32 hd 16 short), 0 = unsupported
 void attention_tc_set_variant(int v);  // microbenchmarks (DART_FA_VARIANT otherwise)
 bool attention_tc_supported(int head_dim, int Lkv);
 // tmQ: 2-D map over the Q buffer [items*Lq, cols] fp16, box {16, 128}, 32B swizzle;

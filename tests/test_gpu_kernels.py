@@ -259,6 +259,25 @@ def test_attention_tcgen05_packed_qkv(lib, items, L, hd):
     assert float((o.float() - ref).abs().max()) < 1e-2
 
 
+@pytest.mark.parametrize("items,L,hd", [(3, 201, 16), (5, 16, 16), (2, 32, 16), (7, 20, 16), (4, 64, 16),
+                                        (2, 100, 80), (1, 201, 80)])
+def test_attention_tcgen05_ragged_keys(lib, items, L, hd):
+    """Key counts that are not a multiple of the key tile run the masked tcgen05 kernel (keys past L
+    in the last tile get P = 0): the decoder's 201-token self-attention (model.py:525), the short
+    32-key tile path (text cross-attention, model.py:518) and toy-size windows, vs fp32 torch."""
+    H = 16
+    E = H * hd
+    g = torch.Generator(device="cuda").manual_seed(L * 7 + items)
+    qkv = (torch.randn(items, L, 3, H, hd, device="cuda", generator=g) * 2).half()
+    o = torch.full((items, L, E), float("nan"), device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), items, H, L, hd, None, stream()))
+    torch.cuda.synchronize()
+    x = qkv.permute(2, 0, 3, 1, 4)
+    ref = ref_attention(x[0], x[1], x[2]).permute(0, 2, 1, 3).reshape(items, L, E)
+    assert bool(torch.isfinite(o).all())
+    assert float((o.float() - ref).abs().max()) < 1e-2
+
+
 @pytest.mark.parametrize("hd,L", [(80, 576), (16, 576), (80, 5184)])
 @pytest.mark.parametrize("mixed", [False, True])
 def test_attention_tcgen05_large_logits(lib, hd, L, mixed):

@@ -78,10 +78,11 @@ def test_device_sigmoid_is_correctly_rounded():
     ref = np.array([sigmoid_cr(v) for v in x])
     np.testing.assert_array_equal(s_dev, ref)
     np.testing.assert_array_equal(p_dev, ref)
-    # and within 1 ulp of the reference's NumPy value everywhere (faithful NumPy exp)
+    # and within 2 ulps of the reference's NumPy value everywhere: NumPy's exp is faithful (<= 1 ulp),
+    # and 1 / (1 + e) can turn one ulp of e into two ulps of the quotient across a binade boundary
     npy = sigmoid_numpy(x)
     ulps = np.abs(s_dev - npy) / np.spacing(np.maximum(np.maximum(np.abs(npy), np.abs(s_dev)), 1e-300))
-    assert ulps.max() <= 1.0, ulps.max()
+    assert ulps.max() <= 2.0, ulps.max()
     print(f"device == correctly rounded on {x.size} logits; NumPy differs by 1 ulp on "
           f"{int((s_dev != npy).sum())} of them")
 
