@@ -158,6 +158,12 @@ int dart_mask_head(dart_model* m, const float* query_features, int32_t B, int32_
 int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* out2, int32_t M, int32_t N,
               int32_t K, int32_t epi, const float* rope_cos, const float* rope_sin, int32_t rope_T, int32_t rope_hd,
               int32_t rope_cols, void* stream);
+/* The enc-dec's sub-block-closing residual GEMM with the NEXT sub-block's LayerNorm fused into its
+ * epilogue (d = 256, whole rows per tile): x[M, 256] += A[M, K] . W[256, K]^T + bias, then
+ * h[M, 256] (fp16) = LayerNorm(x) * ln_g + ln_b (population variance, eps 1e-6; reference
+ * tensors.py:215-227, model.py:516-527). */
+int dart_gemm_resid_ln(const void* A, const void* W, const float* bias, float* x, void* h, const float* ln_g,
+                       const float* ln_b, int32_t M, int32_t K, void* stream);
 void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
 void dart_gemm_force_plan(int32_t bn, int32_t cg);
 /* Fused enc-dec MLP (reference _mlp_forward, model.py:505-508, d = 256, hidden 1024):
@@ -165,6 +171,11 @@ void dart_gemm_force_plan(int32_t bn, int32_t cg);
  * (both [out, in]), x fp32; the hidden activations never leave the SM (TMEM). */
 int dart_mlp_fused(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x, int32_t M,
                    void* stream);
+/* The same with the next sub-block's LayerNorm fused into the residual epilogue: also
+ * h_out[M, 256] (fp16) = LayerNorm(x) * ln_g + ln_b of the new rows (h_out may alias h).
+ * ln_g == NULL: plain dart_mlp_fused. */
+int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,
+                      void* h_out, const float* ln_g, const float* ln_b, int32_t M, void* stream);
 /* y = LayerNorm(x) per row (population variance, eps 1e-6; reference tensors.py:215-227), fp32 in,
  * fp16 (out_f16 = 1) or fp32 out; dim in {32, 64, 128, 256, 512, 1024, 1280}. */
 int dart_layernorm(const float* x, const float* gamma, const float* beta, void* y, int32_t rows, int32_t dim,

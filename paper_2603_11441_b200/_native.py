@@ -40,9 +40,11 @@ EXPORTS = (
     "dart_mask_head",
     "dart_gemm",
     "dart_gemm_plan",
+    "dart_gemm_resid_ln",
     "dart_gemm_force_plan",
     "dart_layernorm",
     "dart_mlp_fused",
+    "dart_mlp_fused_ln",
     "dart_gemm_force_splitk",
     "dart_gemm_force_precision",
     "dart_attention_force_safe",
@@ -156,6 +158,8 @@ def load() -> ctypes.CDLL:
     lib.dart_mask_head.restype = ctypes.c_int
     lib.dart_gemm.argtypes = [P, P, P, P, P, I32, I32, I32, I32, P, P, I32, I32, I32, P]
     lib.dart_gemm.restype = ctypes.c_int
+    lib.dart_gemm_resid_ln.argtypes = [P, P, P, P, P, P, P, I32, I32, P]
+    lib.dart_gemm_resid_ln.restype = ctypes.c_int
     lib.dart_gemm_plan.argtypes = [I32, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
     lib.dart_gemm_plan.restype = None
     lib.dart_gemm_force_plan.argtypes = [I32, I32]
@@ -164,6 +168,8 @@ def load() -> ctypes.CDLL:
     lib.dart_layernorm.restype = ctypes.c_int
     lib.dart_mlp_fused.argtypes = [P, P, P, P, P, P, I32, P]
     lib.dart_mlp_fused.restype = ctypes.c_int
+    lib.dart_mlp_fused_ln.argtypes = [P, P, P, P, P, P, P, P, P, I32, P]
+    lib.dart_mlp_fused_ln.restype = ctypes.c_int
     lib.dart_gemm_force_splitk.argtypes = [I32]
     lib.dart_gemm_force_splitk.restype = None
     lib.dart_gemm_force_precision.argtypes = [I32]

@@ -106,6 +106,7 @@ int g_splitk_enabled = getenv("DART_SPLITK") != nullptr;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
+int g_fused_ln = getenv("DART_NO_FUSED_LN") == nullptr;    // enc-dec LayerNorms in the residual epilogues
 long long* g_attn_trace = nullptr;
 
 // tcgen05 attention: Q rows [items*Lq, q_ld] (q at column q_col, head h at +h*hd), K/V rows
@@ -394,6 +395,9 @@ int check_desc(const dart_model_desc* d) {
 // ---------------------------------------------------------------- launch helpers
 // Output tensor maps of a GEMM epilogue (see gemm_tc): fp32 box 32x32 SW128, fp16 box 32x32 SW64.
 bool make_out_maps(int epi, const GemmEpi& e, int M, int N, CUtensorMap* tc, CUtensorMap* td) {
+  if (epi == EPI_F32_RESID_LN)  // residual stream in/out + the fp16 LayerNorm rows
+    return make_tmap_f32(tc, e.out, N, M, e.ldo) &&
+           make_tmap_ex(td, e.out2, N, M, e.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (epi == EPI_F32_RESID || (epi == EPI_F32 && !e.wm_scatter))
     return make_tmap_f32(tc, e.out, N, M, e.ldo);
   if (epi == EPI_F16 || epi == EPI_F16_RELU || epi == EPI_QKV_ROPE)
@@ -549,11 +553,31 @@ struct XAttnSpec {
   long long kv_batch_stride = 0;
 };
 
+// The residual GEMM that closes an enc-dec sub-block: x += o W + b, and with `next` also
+// h = LN_next(x) in the same epilogue (d = 256: whole rows per tile), so the next sub-block's
+// LayerNorm pass disappears (reference model.py:516-527: every sub-block starts with an LN).
+int resid_gemm(dart_model* m, const __half* A, int rows, int lda, const GemmW& W, float* x, const LNW* next, __half* h,
+               cudaStream_t s) {
+  GemmEpi e = epi_out(x, m->D);
+  if (next && g_fused_ln && W.N == 256) {
+    e.out2 = h;
+    e.ldo2 = m->D;
+    e.ln_g = next->g;
+    e.ln_b = next->b;
+    return gemm(m, A, rows, lda, W, EPI_F32_RESID_LN, e, s);
+  }
+  RUN(gemm(m, A, rows, lda, W, EPI_F32_RESID, e, s));
+  if (next) LAUNCH(layernorm_f32_to_f16(x, next->g, next->b, h, rows, m->D, m->D, m->D, s));
+  return 0;
+}
+
+// One pre-LN sub-block.  h_ready: h already holds LN(x) (fused into the previous sub-block's
+// residual epilogue); next: also leave LN_next(x) in h for the following sub-block.
 int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpec& sp, __half* h, __half* q,
-          __half* kv, __half* o, cudaStream_t s) {
+          __half* kv, __half* o, cudaStream_t s, bool h_ready = false, const LNW* next = nullptr) {
   const int D = m->D, H = m->H, hd = D / H;
   const int rows = sp.items * sp.Lq;
-  LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
+  if (!h_ready) LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
   const int Lk = sp.kv16 == nullptr ? sp.Lq : sp.Lk;
   if (sp.kv16 == nullptr && w.qkv.w) {  // self-attention: one [q | k | v] GEMM into kv (3D wide)
     RUN(gemm(m, h, rows, D, w.qkv, EPI_F16, epi_out(kv, 3 * D), s));
@@ -574,7 +598,7 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
       a.batch = sp.items;
       RUN(attn(m, a, hd, s));
     }
-    return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+    return resid_gemm(m, o, rows, D, w.out, x, next, h, s);
   }
   RUN(gemm(m, h, rows, D, w.q, EPI_F16, epi_out(q, D), s));
   if (tc_attention_enabled() && attention_tc_supported(hd, Lk) &&
@@ -590,7 +614,7 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
       RUN(attn_tc(q, D, 0, sp.kv16, sp.kv_tok_stride, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s, nullptr,
                   sp.kv_mod));
     }
-    return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+    return resid_gemm(m, o, rows, D, w.out, x, next, h, s);
   }
   AttnArgs a = attn_base(H, hd);
   a.q = q;
@@ -617,31 +641,38 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
     a.kv_batch_mod = sp.kv_mod;
   }
   RUN(attn(m, a, hd, s));
-  return gemm(m, o, rows, D, w.out, EPI_F32_RESID, epi_out(x, D), s);
+  return resid_gemm(m, o, rows, D, w.out, x, next, h, s);
 }
 
 // x += relu(h W1 + b1) W2 + b2 on the fused kernel (hidden activations stay in TMEM)
 int mlp_fused_call(dart_model* m, const __half* h, const GemmW& fc1, const GemmW& fc2, float* x, int rows,
-                   cudaStream_t s) {
-  CUtensorMap th, tw1, tw2, tx;
+                   cudaStream_t s, const LNW* next = nullptr, __half* h_out = nullptr) {
+  CUtensorMap th, tw1, tw2, tx, tln;
   if (!make_tmap(&th, h, 256, rows, 256, 128) || !make_tmap(&tw1, fc1.w, 256, 1024, 256, 64) ||
-      !make_tmap(&tw2, fc2.w, 1024, 256, 1024, 128) || !make_tmap_f32(&tx, x, 256, rows, 256))
+      !make_tmap(&tw2, fc2.w, 1024, 256, 1024, 128) || !make_tmap_f32(&tx, x, 256, rows, 256) ||
+      !make_tmap_ex(&tln, next ? h_out : h, 256, rows, 256, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (fused MLP)");
   m->launches++;
-  const int rc = mlp_fused(th, tw1, tw2, tx, rows, fc1.b, fc2.b, m->num_sms, s);
+  const int rc = mlp_fused(th, tw1, tw2, tx, tln, rows, fc1.b, fc2.b, next ? next->g : nullptr,
+                           next ? next->b : nullptr, m->num_sms, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("mlp_fused: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }
 
 int xmlp(dart_model* m, float* x, const LNW& ln, const GemmW& fc1, const GemmW& fc2, int rows, __half* h,
-         __half* hid, cudaStream_t s) {
+         __half* hid, cudaStream_t s, bool h_ready = false, const LNW* next = nullptr) {
   const int D = m->D;
-  LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
-  // fused above ~2 waves of 256-row units (N=80: 423 vs 580 us per layer; N=4 equal)
-  if (g_fused_mlp && D == 256 && fc1.N == 1024 && fc2.K == 1024 && fc2.N == 256 && rows >= 256 * m->num_sms)
-    return mlp_fused_call(m, h, fc1, fc2, x, rows, s);
+  if (!h_ready) LAUNCH(layernorm_f32_to_f16(x, ln.g, ln.b, h, rows, D, D, D, s));
+  // fused above ~2 waves of 256-row units (N=80: 423 vs 580 us per layer; N=4 equal); both forms
+  // fuse the next sub-block's LN into their residual epilogue with identical arithmetic
+  if (g_fused_mlp && D == 256 && fc1.N == 1024 && fc2.K == 1024 && fc2.N == 256 && rows >= 256 * m->num_sms) {
+    if (next && g_fused_ln) return mlp_fused_call(m, h, fc1, fc2, x, rows, s, next, h);
+    RUN(mlp_fused_call(m, h, fc1, fc2, x, rows, s));
+    if (next) LAUNCH(layernorm_f32_to_f16(x, next->g, next->b, h, rows, D, D, D, s));
+    return 0;
+  }
   RUN(gemm(m, h, rows, D, fc1, EPI_F16_RELU, epi_out(hid, 4 * D), s));
-  return gemm(m, hid, rows, 4 * D, fc2, EPI_F32_RESID, epi_out(x, D), s);
+  return resid_gemm(m, hid, rows, 4 * D, fc2, x, next, h, s);
 }
 
 }  // namespace
@@ -976,13 +1007,15 @@ int ed_body(dart_model* m, const float* e1, int B, const float* text, int N, dou
   LAUNCH(cast_f32_to_f16(text, w.text, (long long)N * Lt * D, s));
   RUN(gemm(m, w.text, N * Lt, D, m->enc_cross_kv_all, EPI_F16, epi_out(w.tkv, ne * 2 * D), s));
   const int rows = items * T;
+  // every LayerNorm after the first is fused into the residual epilogue of the sub-block before it
+  // (h then already holds it: `ready`), except after the fused MLP kernel (xmlp)
   for (int l = 0; l < ne; ++l) {
     const XLayerW& L = m->enc[l];
     if (l > 0) {
       XAttnSpec sp;
       sp.items = items;
       sp.Lq = T;
-      RUN(xattn(m, w.e, L.ln1, L.self, sp, w.h, w.q, w.kv, w.o, s));
+      RUN(xattn(m, w.e, L.ln1, L.self, sp, w.h, w.q, w.kv, w.o, s, true, &L.ln2));
     }
     XAttnSpec cx;
     cx.items = items;
@@ -992,11 +1025,11 @@ int ed_body(dart_model* m, const float* e1, int B, const float* text, int N, dou
     cx.kv_batch_stride = (long long)Lt * ne * 2 * D;
     cx.Lk = Lt;
     cx.kv_mod = N;
-    RUN(xattn(m, w.e, L.ln2, L.cross, cx, w.h, w.q, w.kv, w.o, s));
-    RUN(xmlp(m, w.e, L.ln3, L.fc1, L.fc2, rows, w.h, w.hid, s));
+    RUN(xattn(m, w.e, L.ln2, L.cross, cx, w.h, w.q, w.kv, w.o, s, l > 0, &L.ln3));
+    RUN(xmlp(m, w.e, L.ln3, L.fc1, L.fc2, rows, w.h, w.hid, s, true, l + 1 < ne ? &m->enc[l + 1].ln1 : &m->enc_final));
   }
-  // ---- encoder memory: final LN, then K/V of all 6 decoder cross-attentions in one GEMM
-  LAUNCH(layernorm_f32_to_f16(w.e, m->enc_final.g, m->enc_final.b, w.h, rows, D, D, D, s));
+  // ---- encoder memory: final LN (h, from the last MLP's epilogue), then K/V of all 6 decoder
+  //      cross-attentions in one GEMM
   RUN(gemm(m, w.h, rows, D, m->dec_cross_kv_all, EPI_F16, epi_out(w.dkv, nd * 2 * D), s));
   // ---- decoder: layer-0 self-attention over the learned queries is class-independent
   CK(cudaMemcpyAsync(w.qd0, m->queries, (size_t)Q1 * D * 4, cudaMemcpyDeviceToDevice, s));
@@ -1014,7 +1047,7 @@ int ed_body(dart_model* m, const float* e1, int B, const float* text, int N, dou
       XAttnSpec sp;
       sp.items = items;
       sp.Lq = Q1;
-      RUN(xattn(m, w.qd, L.ln1, L.self, sp, w.dh, w.dq, w.dkvs, w.do_, s));
+      RUN(xattn(m, w.qd, L.ln1, L.self, sp, w.dh, w.dq, w.dkvs, w.do_, s, true, &L.ln2));
     }
     XAttnSpec cx;
     cx.items = items;
@@ -1023,8 +1056,8 @@ int ed_body(dart_model* m, const float* e1, int B, const float* text, int N, dou
     cx.kv_tok_stride = nd * 2 * D;
     cx.kv_batch_stride = (long long)T * nd * 2 * D;
     cx.Lk = T;
-    RUN(xattn(m, w.qd, L.ln2, L.cross, cx, w.dh, w.dq, w.dkvs, w.do_, s));
-    RUN(xmlp(m, w.qd, L.ln3, L.fc1, L.fc2, drows, w.dh, w.dhid, s));
+    RUN(xattn(m, w.qd, L.ln2, L.cross, cx, w.dh, w.dq, w.dkvs, w.do_, s, l > 0, &L.ln3));
+    RUN(xmlp(m, w.qd, L.ln3, L.fc1, L.fc2, drows, w.dh, w.dhid, s, true, l + 1 < nd ? &m->dec[l + 1].ln1 : nullptr));
   }
   LAUNCH(layernorm_f32_to_f32(w.qd, m->dec_final.g, m->dec_final.b, w.qf, drows, D, s));
   LAUNCH(heads_forward(w.qf, Q1, Q, items, D, m->box_w, m->box_b, m->score_w, m->score_b, m->pres_w, m->pres_b, boxes,
@@ -1084,6 +1117,31 @@ int dart_postprocess(dart_model* m, const double* boxes, const double* score_log
                                  scratch, s);
     if (rc) return fail(DART_ERR_CUDA, std::string("cross-class NMS: ") + cudaGetErrorString((cudaError_t)rc));
   }
+  return DART_OK;
+}
+
+int dart_gemm_resid_ln(const void* A, const void* W, const float* bias, float* x, void* h, const float* ln_g,
+                       const float* ln_b, int32_t M, int32_t K, void* stream) {
+  if (!A || !W || !x || !h || !ln_g || !ln_b || M <= 0 || K % 64) return fail(DART_ERR_INVALID, "dart_gemm_resid_ln: bad args");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int N = 256;
+  const GemmPlan plan = gemm_plan(M, N, EPI_F32_RESID_LN, sms);
+  GemmEpi e;
+  e.bias = bias;
+  e.out = x;
+  e.ldo = N;
+  e.out2 = h;
+  e.ldo2 = N;
+  e.ln_g = ln_g;
+  e.ln_b = ln_b;
+  CUtensorMap ta, tb, tc, td;
+  if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, plan.bn / plan.cg) ||
+      !make_out_maps(EPI_F32_RESID_LN, e, M, N, &tc, &td))
+    return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  const int rc = gemm_tc(ta, tb, nullptr, &tc, &td, M, N, K, plan, EPI_F32_RESID_LN, e, sms, (cudaStream_t)stream);
+  if (rc) return fail(DART_ERR_CUDA, std::string("gemm_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
 }
 
@@ -1158,19 +1216,26 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
-int dart_mlp_fused(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x, int32_t M,
-                   void* stream) {
-  if (!h || !w1 || !b1 || !w2 || !b2 || !x || M <= 0) return fail(DART_ERR_INVALID, "dart_mlp_fused: bad args");
+int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,
+                      void* h_out, const float* ln_g, const float* ln_b, int32_t M, void* stream) {
+  if (!h || !w1 || !b1 || !w2 || !b2 || !x || M <= 0 || (ln_g && (!ln_b || !h_out)))
+    return fail(DART_ERR_INVALID, "dart_mlp_fused: bad args");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  CUtensorMap th, tw1, tw2, tx;
+  CUtensorMap th, tw1, tw2, tx, tln;
   if (!make_tmap(&th, h, 256, M, 256, 128) || !make_tmap(&tw1, w1, 256, 1024, 256, 64) ||
-      !make_tmap(&tw2, w2, 1024, 256, 1024, 128) || !make_tmap_f32(&tx, x, 256, M, 256))
+      !make_tmap(&tw2, w2, 1024, 256, 1024, 128) || !make_tmap_f32(&tx, x, 256, M, 256) ||
+      !make_tmap_ex(&tln, ln_g ? h_out : h, 256, M, 256, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (fused MLP)");
-  const int rc = mlp_fused(th, tw1, tw2, tx, M, b1, b2, sms, (cudaStream_t)stream);
+  const int rc = mlp_fused(th, tw1, tw2, tx, tln, M, b1, b2, ln_g, ln_b, sms, (cudaStream_t)stream);
   if (rc) return fail(DART_ERR_CUDA, std::string("mlp_fused: ") + cudaGetErrorString((cudaError_t)rc));
   return DART_OK;
+}
+
+int dart_mlp_fused(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x, int32_t M,
+                   void* stream) {
+  return dart_mlp_fused_ln(h, w1, b1, w2, b2, x, nullptr, nullptr, nullptr, M, stream);
 }
 
 int dart_attention(const void* q, const void* k, const void* v, void* o, int32_t batch, int32_t heads, int32_t Lq,

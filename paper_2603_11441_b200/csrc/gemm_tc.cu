@@ -37,14 +37,18 @@ struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr bool RESID = EPI == EPI_F32_RESID;
+  static constexpr bool RESID = EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN;
+  static constexpr bool LNO = EPI == EPI_F32_RESID_LN;  // fused LayerNorm output of full rows
   // staging buffers per epilogue warp; 4 for the residual epilogue (3 chunks prefetched) measured
   // slower: the extra 64 KB costs two operand stages (out-proj 24.8 -> 27.1 us, fc2 63.4 -> 80 us)
   static constexpr int NBUF = 2;
   // staging buffer per chunk: 32x32 fp32 (4 KB), or 32x32 fp16 (2 KB) for the fp16-only epilogues
   static constexpr int BUF_BYTES = (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) ? 2048 : 4096;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x NBUF staging buffers
-  static constexpr int ROPE_OFF = EPI_OFF + 8 * NBUF * BUF_BYTES;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
+  // fused LN: 2 fp16 32x32 staging chunks per epilogue warp + the row-statistics exchange
+  static constexpr int LN_OFF = EPI_OFF + 8 * NBUF * BUF_BYTES;
+  static constexpr int LN_BYTES = LNO ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : 0;
+  static constexpr int ROPE_OFF = LN_OFF + LN_BYTES;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
   static constexpr int ROPE_BYTES = EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0;
   static constexpr int BAR_OFF = ROPE_OFF + ROPE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 512 + 1024;  // barriers + 1 KB alignment slack
@@ -234,6 +238,83 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Fused LayerNorm epilogue over whole 256-column rows (the enc-dec's d = 256; reference
+// tensors.py:215-227: two-pass mean / population variance, eps 1e-6, then * gamma + beta).
+// Called by each of the 8 epilogue warps after it stashed its chunks of the NEW residual rows
+// (columns half*32 + 64 i, i < 4, relative to `taddr`) back into TMEM and summed them into
+// `row_sum`: the two warps of a lane quarter combine their partial sums through `red`
+// ([4 quarters][2 halves][32] floats) in a fixed order, re-read the stash for the variance and
+// the normalisation, and store the fp16 rows with TMA (tmOut, box 32x32, 64B swizzle) through
+// two 2 KB staging chunks `lnbuf`, `stride` floats apart.  Every operation is pinned to an IEEE
+// intrinsic, so the GEMM epilogue and the fused-MLP epilogue produce identical bits.
+__device__ __forceinline__ void ln_rows_epilogue(uint32_t taddr, int quarter, int half, int lane, float row_sum,
+                                                 const float* gamma, const float* beta, float* red, float* lnbuf,
+                                                 int stride, const CUtensorMap* tmOut, int col0, int row0) {
+  tmem_st_wait();  // the stash is in TMEM before any warp re-reads it
+  float* r = red + quarter * 64;
+  r[half * 32 + lane] = row_sum;
+  named_bar_sync(2 + quarter, 64);
+  const float mu = __fmul_rn(__fadd_rn(r[lane], r[32 + lane]), 1.0f / 256.0f);
+  named_bar_sync(2 + quarter, 64);  // both partners have read the sums before `r` is reused
+  float q = 0.f;
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    float x[32];
+    tmem_ld32(taddr + half * 32 + 64 * i, x);
+    tmem_ld_wait();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const float d = __fsub_rn(x[k], mu);
+      q = __fmaf_rn(d, d, q);
+    }
+  }
+  r[half * 32 + lane] = q;
+  named_bar_sync(2 + quarter, 64);
+  const float var = __fmul_rn(__fadd_rn(r[lane], r[32 + lane]), 1.0f / 256.0f);
+  named_bar_sync(2 + quarter, 64);  // the variances are read before the next row block's sums land
+  const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-6f)));
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int c = half * 32 + 64 * i;
+    float x[32];
+    tmem_ld32(taddr + c, x);
+    tmem_ld_wait();
+    const float4* g4 = reinterpret_cast<const float4*>(gamma + c);
+    const float4* b4 = reinterpret_cast<const float4*>(beta + c);
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      const float4 gg = __ldg(g4 + qq), bb = __ldg(b4 + qq);
+      x[4 * qq] = __fmaf_rn(__fmul_rn(__fsub_rn(x[4 * qq], mu), rstd), gg.x, bb.x);
+      x[4 * qq + 1] = __fmaf_rn(__fmul_rn(__fsub_rn(x[4 * qq + 1], mu), rstd), gg.y, bb.y);
+      x[4 * qq + 2] = __fmaf_rn(__fmul_rn(__fsub_rn(x[4 * qq + 2], mu), rstd), gg.z, bb.z);
+      x[4 * qq + 3] = __fmaf_rn(__fmul_rn(__fsub_rn(x[4 * qq + 3], mu), rstd), gg.w, bb.w);
+    }
+    float* lb = lnbuf + (i & 1) * stride;
+    if (lane == 0) {  // the stores that last used this staging chunk have read it
+      if (i == 0)
+        bulk_wait_read0();
+      else
+        bulk_wait_read1();
+    }
+    __syncwarp();
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      uint4 u;
+      u.x = pack_half2(x[8 * qq + 0], x[8 * qq + 1]);
+      u.y = pack_half2(x[8 * qq + 2], x[8 * qq + 3]);
+      u.z = pack_half2(x[8 * qq + 4], x[8 * qq + 5]);
+      u.w = pack_half2(x[8 * qq + 6], x[8 * qq + 7]);
+      *slot16_sw64(lb, lane, qq) = u;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmOut, lb, col0 + c, row0);
+      tma_store_commit();
+    }
+  }
+}
+
 constexpr int GEMM_THREADS = 384;
 
 // PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
@@ -287,7 +368,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tmB);
     if (TF > 0) tma_prefetch_desc(&tmB2);
     if (RESID || EPI == EPI_F32) tma_prefetch_desc(&tmC);
-    if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) tma_prefetch_desc(&tmD);
+    if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE || EPI == EPI_F32_RESID_LN) tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -441,6 +522,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      [[maybe_unused]] float ln_sum = 0.f;
       const float2 *rt = nullptr, *ct = nullptr;
       if (EPI == EPI_QKV_ROPE) {
         int tok = row % epi.rope_T;
@@ -469,7 +551,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             v[j] = __half2float(__ushort_as_half((unsigned short)(__float_as_uint(v[j]) & 0xFFFFu)));
         }
-        if (c + 64 >= bn_eff) {
+        if (!L::LNO && c + 64 >= bn_eff) {
           // all of this warp's accumulator columns are in registers: hand TMEM back early
           tc_fence_before();
           __syncwarp();
@@ -505,6 +587,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             x.w += v[4 * q + 3];
             if ((PREC && epi.round_f16)) x = make_float4(round_f16(x.x), round_f16(x.y), round_f16(x.z), round_f16(x.w));
             *sp = x;
+            if constexpr (L::LNO) {
+              v[4 * q] = x.x;
+              v[4 * q + 1] = x.y;
+              v[4 * q + 2] = x.z;
+              v[4 * q + 3] = x.w;
+            }
+          }
+          if constexpr (L::LNO) {  // the new residual row values stay in TMEM for the LN passes
+            tmem_st16(taddr + c, reinterpret_cast<const uint32_t*>(v));
+            tmem_st16(taddr + c + 16, reinterpret_cast<const uint32_t*>(v + 16));
+#pragma unroll
+            for (int k = 0; k < 32; ++k) ln_sum = __fadd_rn(ln_sum, v[k]);
           }
         } else if constexpr (EPI == EPI_F32 || EPI == EPI_F32_F16) {
 #pragma unroll
@@ -529,6 +623,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           else
             tma_store_2d(&tmD, buf, n0 + c, row0);
           tma_store_commit();
+        }
+      }
+      if constexpr (L::LNO) {
+        ln_rows_epilogue(taddr, quarter, half, lane, ln_sum, epi.ln_g + n0, epi.ln_b + n0,
+                         reinterpret_cast<float*>(smem + L::LN_OFF + 8 * 2 * 2048),
+                         reinterpret_cast<float*>(smem + L::LN_OFF) + (warp - 4) * 2 * 512, 512, &tmD, n0, row0);
+        tc_fence_before();  // every TMEM read of this accumulator is done: release it
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) {
+            mbar_arrive(&tempty[acc]);
+          } else {
+            mbar_arrive_leader(&tempty[acc]);
+          }
         }
       }
       if (SK > 1 && kh == 0) {  // half 0 of a split-K tile: publish once this warp's stores landed
@@ -572,14 +680,18 @@ constexpr int STAGES = 6;
 constexpr int OFF_RING = A_BYTES;
 constexpr int OFF_EPI = OFF_RING + STAGES * RING_BYTES;
 constexpr int OFF_BAR = OFF_EPI + 16 * 4096;
-constexpr int TOTAL = OFF_BAR + 512 + 1024;
+constexpr int OFF_RED = OFF_BAR + 512;  // fused-LN row statistics exchange [4][2][32] floats
+constexpr int TOTAL = OFF_RED + 1024 + 1024;
 static_assert(TOTAL <= 227 * 1024, "shared memory budget");
 }  // namespace mlpf
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     mlp_fused_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW1,
-                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmX, int M,
-                     const float* __restrict__ b1, const float* __restrict__ b2) {
+                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmLN, int M, const float* __restrict__ b1,
+                     const float* __restrict__ b2, const float* __restrict__ ln_g, const float* __restrict__ ln_b) {
+  // ln_g != nullptr: also LayerNorm(x) * ln_g + ln_b of the new residual rows -> tmLN (fp16), the
+  // next sub-block's LN, with the same arithmetic as the GEMM's EPI_F32_RESID_LN epilogue
   using namespace mlpf;
   constexpr int CG = 2;
   extern __shared__ uint8_t smem_raw[];
@@ -777,6 +889,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // residual epilogue: x += acc2 + b2 (this warp: 32-column chunks half, half + 2, ...)
       mbar_wait(o_full, it & 1);
       tc_fence_after();
+      const bool lno = ln_g != nullptr;
+      float ln_sum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c, ++g) {
         const int col = (c * 2 + half) * 32;
@@ -789,7 +903,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
         tmem_ld32(lane_base + 256 + col, v);
         tmem_ld_wait();
-        if (c == 3) {
+        if (c == 3 && !lno) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(o_empty);
@@ -806,6 +920,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           x.z += v[4 * q + 2] + bq.z;
           x.w += v[4 * q + 3] + bq.w;
           *sp = x;
+          v[4 * q] = x.x;
+          v[4 * q + 1] = x.y;
+          v[4 * q + 2] = x.z;
+          v[4 * q + 3] = x.w;
+        }
+        if (lno) {  // the new residual row values stay in TMEM for the LN passes
+          tmem_st16(lane_base + 256 + col, reinterpret_cast<const uint32_t*>(v));
+          tmem_st16(lane_base + 256 + col + 16, reinterpret_cast<const uint32_t*>(v + 16));
+#pragma unroll
+          for (int k = 0; k < 32; ++k) ln_sum = __fadd_rn(ln_sum, v[k]);
         }
         fence_proxy_async();
         __syncwarp();
@@ -813,6 +937,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tma_store_2d(&tmX, buf, col, row0);
           tma_store_commit();
         }
+      }
+      if (lno) {
+        ln_rows_epilogue(lane_base + 256, quarter, half, lane, ln_sum, ln_g, ln_b,
+                         reinterpret_cast<float*>(smem + OFF_RED), bufs, 1024, &tmLN, 0, row0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(o_empty);
       }
     }
     if (lane == 0) bulk_wait_all();
@@ -862,7 +993,8 @@ template <int BN, int EPI, int CG>
 constexpr int stages_for() {
   constexpr int stage = BM * BK * 2 + (BN / CG) * BK * 2;
   constexpr int fixed = 8 * 2 * ((EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) ? 2048 : 4096) +
-                        (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) + 512 + 1024;
+                        (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) +
+                        (EPI == EPI_F32_RESID_LN ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : 0) + 512 + 1024;
   constexpr int n = (227 * 1024 - fixed) / stage;
   return n > 8 ? 8 : n;
 }
@@ -889,6 +1021,9 @@ int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, con
     case EPI_F32_RESID: return launch_planned<BN, EPI_F32_RESID, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
     case EPI_QKV_ROPE: return launch_planned<BN, EPI_QKV_ROPE, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
     case EPI_F32_F16: return launch_planned<BN, EPI_F32_F16, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_RESID_LN:
+      if constexpr (BN == 256) return launch_planned<BN, EPI_F32_RESID_LN, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+      return (int)cudaErrorInvalidValue;
   }
   return (int)cudaErrorInvalidValue;
 }
@@ -905,8 +1040,9 @@ double g_eff192 = env_or("DART_GEMM_EFF192", 0.80), g_eff160 = env_or("DART_GEMM
 
 }  // namespace
 
-int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX, int M,
-              const float* b1, const float* b2, int num_sms, cudaStream_t stream) {
+int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX,
+              const CUtensorMap& tLN, int M, const float* b1, const float* b2, const float* ln_g, const float* ln_b,
+              int num_sms, cudaStream_t stream) {
   static std::atomic<uint64_t> smem_set{0};
   if (const cudaError_t e = set_smem_once(smem_set, mlp_fused_kernel, mlpf::TOTAL); e != cudaSuccess) return (int)e;
   const int units = (M + 255) / 256, pairs = num_sms / 2;
@@ -923,7 +1059,7 @@ int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_fused_kernel, tH, tW1, tW2, tX, M, b1, b2);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_fused_kernel, tH, tW1, tW2, tX, tLN, M, b1, b2, ln_g, ln_b);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
@@ -940,7 +1076,7 @@ int gemm_bn_for(int N) {
 // re-reads (measured MMA efficiency relative to BN = 256 on B200: 0.66 at 128, 0.45 at 64);
 // the CTA-pair form wins ties (lower operand traffic per FLOP).
 GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
-  (void)epi_mode;
+  if (epi_mode == EPI_F32_RESID_LN) return GemmPlan{N == 256 ? 256 : 0, 2};  // whole rows per tile
   GemmPlan best{0, 1};
   double best_cost = 0;
   for (int cg = 2; cg >= 1; --cg) {
@@ -977,15 +1113,17 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2
                                    epi.rope_grid * epi.rope_grid != epi.rope_T || epi.rope_hd % 4 != 0 ||
                                    epi.rope_hd / 4 > ROPE_MAX_Q))
     return (int)cudaErrorInvalidValue;
-  const bool f32_out = epi_mode == EPI_F32_RESID || (epi_mode == EPI_F32 && !epi.wm_scatter);
-  const bool f16_out = epi_mode == EPI_F16 || epi_mode == EPI_F16_RELU || epi_mode == EPI_QKV_ROPE;
+  const bool f32_out = epi_mode == EPI_F32_RESID || epi_mode == EPI_F32_RESID_LN || (epi_mode == EPI_F32 && !epi.wm_scatter);
+  const bool f16_out = epi_mode == EPI_F16 || epi_mode == EPI_F16_RELU || epi_mode == EPI_QKV_ROPE ||
+                       epi_mode == EPI_F32_RESID_LN;
+  if (epi_mode == EPI_F32_RESID_LN && (N != BN || BN != 256 || !epi.ln_g || !epi.ln_b)) return (int)cudaErrorInvalidValue;
   if ((f32_out && !tC) || (f16_out && !tD)) return (int)cudaErrorInvalidValue;
   const CUtensorMap& c = tC ? *tC : tA;
   const CUtensorMap& d = tD ? *tD : tA;
   const CUtensorMap& b2 = tB2 ? *tB2 : tB;
   // tail halves: when the tiles leave a last wave at most half full, run it as half-width units
   epi.tail_full = 0;
-  if (tB2 && g_tail_halves && epi.splitk == 1 && (BN == 256 || BN == 128)) {
+  if (tB2 && g_tail_halves && epi.splitk == 1 && (BN == 256 || BN == 128) && epi_mode != EPI_F32_RESID_LN) {
     const int tiles = ((M + BM * plan.cg - 1) / (BM * plan.cg)) * (N / BN);
     const int units = num_sms / plan.cg;
     const int rem = tiles % units;

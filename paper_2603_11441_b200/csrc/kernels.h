@@ -14,6 +14,9 @@ enum EpiMode {
   EPI_F32_RESID = 3,  // out32 += acc + bias       (fp32 residual stream)
   EPI_QKV_ROPE = 4,   // out16 = rope(acc + bias) on columns < rope_cols
   EPI_F32_F16 = 5,    // out32 = acc + bias, out2_16 = same in fp16
+  // out32 += acc + bias, then out2_16 = LayerNorm(out32) * ln_g + ln_b over each full row
+  // (N == BN: the enc-dec's d = 256 rows sit in one tile; fuses the NEXT sub-block's LN)
+  EPI_F32_RESID_LN = 6,
 };
 
 struct GemmEpi {
@@ -50,6 +53,10 @@ struct GemmEpi {
   // to fp16-representable values (fp16 storage).
   int acc_f16 = 0;
   int round_f16 = 0;
+  // EPI_F32_RESID_LN: affine of the fused LayerNorm (population variance, eps 1e-6; out2 / ldo2
+  // receive the fp16 normalised rows)
+  const float* ln_g = nullptr;
+  const float* ln_b = nullptr;
 };
 
 // window-major row index <-> token index within one image
@@ -82,8 +89,11 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2
 // Fused enc-dec MLP: x[M,256] += relu(h W1^T + b1) W2^T + b2 with W1 [1024, 256], W2 [256, 1024]
 // fp16 K-major, hidden activations kept in TMEM.  tH: box {64, 128} over h [M, 256];
 // tW1: box {64, 64} over W1; tW2: box {64, 128} over W2; tX: fp32 box {32, 32} 128B swizzle over x.
-int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX, int M,
-              const float* b1, const float* b2, int num_sms, cudaStream_t stream);
+// tLN / ln_g / ln_b: with ln_g != nullptr the epilogue also writes h = LayerNorm(x) * ln_g + ln_b
+// (fp16 [M, 256], box {32, 32} 64B swizzle) -- the next sub-block's LN (tLN unused otherwise).
+int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& tW2, const CUtensorMap& tX,
+              const CUtensorMap& tLN, int M, const float* b1, const float* b2, const float* ln_g, const float* ln_b,
+              int num_sms, cudaStream_t stream);
 
 // Flash attention (fp16 operands, fp32 softmax/accumulation).
 struct AttnArgs {

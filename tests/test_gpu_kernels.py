@@ -259,6 +259,31 @@ def test_attention_tcgen05_packed_qkv(lib, items, L, hd):
     assert float((o.float() - ref).abs().max()) < 1e-2
 
 
+@pytest.mark.parametrize("M,K", [(300, 256), (20736, 256), (804, 1024), (5184 * 3, 256)])
+def test_gemm_residual_layernorm_epilogue(lib, M, K):
+    """EPI_F32_RESID_LN: x += A W^T + b and h = LN(x) g + beta in the same epilogue (the enc-dec's
+    fused sub-block boundary) vs fp32 torch; x also equals the plain residual GEMM's x bitwise."""
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    W = (torch.randn(256, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(256, device="cuda", generator=g) * 0.1
+    x0 = torch.randn(M, 256, device="cuda", generator=g) * 3 + 1.5  # offset rows: the mean matters
+    gam = torch.rand(256, device="cuda", generator=g) + 0.5
+    bet = torch.randn(256, device="cuda", generator=g) * 0.2
+    x = x0.clone()
+    h = torch.empty(M, 256, device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_gemm_resid_ln(A.data_ptr(), W.data_ptr(), bias.data_ptr(), x.data_ptr(), h.data_ptr(),
+                                         gam.data_ptr(), bet.data_ptr(), M, K, stream()))
+    x_plain = x0.clone()
+    run_gemm(lib, A, W, bias, 3, x_plain)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_plain)
+    ref_x = x0 + A.float() @ W.float().t() + bias
+    assert rel_err(x, ref_x) < 2e-3
+    ref_h = torch.nn.functional.layer_norm(x, (256,), gam, bet, eps=1e-6)
+    assert float((h.float() - ref_h).abs().max()) < 2e-2
+
+
 @pytest.mark.parametrize("items,L,hd", [(3, 201, 16), (5, 16, 16), (2, 32, 16), (7, 20, 16), (4, 64, 16),
                                         (2, 100, 80), (1, 201, 80)])
 def test_attention_tcgen05_ragged_keys(lib, items, L, hd):
@@ -380,3 +405,32 @@ def test_mlp_fused(lib, M):
                                      out.data_ptr(), M, stream()))
     torch.cuda.synchronize()
     assert rel_err(out, ref) < 2e-3
+
+
+@pytest.mark.parametrize("M", [300, 20736, 41472])
+def test_mlp_fused_layernorm_equals_gemm_path(lib, M):
+    """The fused MLP kernel's LN epilogue and the GEMM path (fc1 GEMM + fc2 GEMM with the
+    EPI_F32_RESID_LN epilogue) give identical bits for x and h = LN(x): the enc-dec picks one or
+    the other by row count (i.e. by class count), and a class's outputs must not depend on N."""
+    g = torch.Generator(device="cuda").manual_seed(M + 1)
+    h = torch.randn(M, 256, device="cuda", generator=g).half()
+    w1 = (torch.randn(1024, 256, device="cuda", generator=g) / 16).half()
+    w2 = (torch.randn(256, 1024, device="cuda", generator=g) / 32).half()
+    b1 = torch.randn(1024, device="cuda", generator=g) * 0.1
+    b2 = torch.randn(256, device="cuda", generator=g) * 0.1
+    x0 = torch.randn(M, 256, device="cuda", generator=g) * 2 + 0.7
+    gam = torch.rand(256, device="cuda", generator=g) + 0.5
+    bet = torch.randn(256, device="cuda", generator=g) * 0.2
+    x_f, h_f = x0.clone(), h.clone()  # fused kernel, LN written over its own input (as the enc-dec does)
+    _native.check(lib.dart_mlp_fused_ln(h_f.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                                        x_f.data_ptr(), h_f.data_ptr(), gam.data_ptr(), bet.data_ptr(), M, stream()))
+    hid = torch.empty(M, 1024, device="cuda", dtype=torch.float16)
+    run_gemm(lib, h, w1, b1, 1, hid)
+    x_g, h_g = x0.clone(), torch.empty(M, 256, device="cuda", dtype=torch.float16)
+    _native.check(lib.dart_gemm_resid_ln(hid.data_ptr(), w2.data_ptr(), b2.data_ptr(), x_g.data_ptr(), h_g.data_ptr(),
+                                         gam.data_ptr(), bet.data_ptr(), M, 1024, stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(x_f, x_g)
+    assert torch.equal(h_f, h_g)
+    ref = torch.nn.functional.layer_norm(x_g, (256,), gam, bet, eps=1e-6)
+    assert float((h_g.float() - ref).abs().max()) < 2e-2
