@@ -645,16 +645,23 @@ def gemm_roofline(cfg, dev, args, stream):
     M, E = args.batch * cfg.tokens, cfg.embed_dim
     out = torch.zeros(M, E, device=dev, dtype=torch.float32)
     bias = torch.zeros(E, device=dev)
-    res = {}
+    res, res_pdl = {}, {}
     for name, K in (("attn.out", E), ("mlp.fc2", 4 * E)):
         A = torch.randn(M, K, device=dev).half()
         W = (torch.randn(E, K, device=dev) / K ** 0.5).half()
         call = lambda A=A, W=W, K=K: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(),
                                                                  out.data_ptr(), None, M, E, K, 3, None, None, 0, 0,
                                                                  0, stream.cuda_stream))
+        # kernel boundaries as in the headline's pipeline (programmatic dependent launch off) ...
+        lib.dart_set_pdl(0)
         res[name] = (2.0 * M * E * K, _time_launches(call, stream))
+        # ... and as on a single stream (PDL on: each launch's prologue overlaps the previous tail)
+        lib.dart_set_pdl(1)
+        res_pdl[name] = (2.0 * M * E * K, _time_launches(call, stream))
+        lib.dart_set_pdl(-1)
     flop = sum(f for f, _ in res.values())
     t = sum(s for _, s in res.values())
+    t_pdl = sum(s for _, s in res_pdl.values())
     achieved = flop / t / 1e12
     peak = pk["bf16_tflops"]
     traffic = None
@@ -670,6 +677,8 @@ def gemm_roofline(cfg, dev, args, stream):
             "peak_kind": f"{pk_kind} burst bf16/fp16 dense",
             "flop_per_launch": flop / 2, "us_per_launch": t / 2 * 1e6,
             "per_shape": {k: {"flop": f, "us": s * 1e6, "tflops": f / s / 1e12} for k, (f, s) in res.items()},
+            "launches": "back to back on one stream, programmatic dependent launch off (as in the pipeline)",
+            "frac_with_pdl": flop / t_pdl / 1e12 / peak,
             "traffic": traffic,
             "traffic_note": "mean dram read+write bytes per launch of the two shapes, ncu --set full "
                             "(profiles/r02/roofline_traffic.json)"}

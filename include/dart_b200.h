@@ -207,6 +207,13 @@ void dart_attention_trace(int64_t* device_buf);
 /* Microbenchmarks: select the tcgen05 attention kernel variant (0 = production). */
 void dart_attention_variant(int32_t v);
 
+/* Programmatic dependent launch for the calling host thread's later launches: 1 = on (each GEMM /
+ * attention / LayerNorm kernel may start its prologue while its predecessor drains: +2% on one
+ * stream), 0 = off (fully serialised kernel boundaries: measured better when several streams
+ * share the GPU, as in the inter-frame pipeline), -1 = the process default (on; DART_NO_PDL=1
+ * turns it off). */
+void dart_set_pdl(int32_t mode);
+
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */
 int64_t dart_launch_count(const dart_model* m);

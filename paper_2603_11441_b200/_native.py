@@ -46,6 +46,7 @@ EXPORTS = (
     "dart_mlp_fused",
     "dart_mlp_fused_ln",
     "dart_gemm_force_splitk",
+    "dart_set_pdl",
     "dart_gemm_force_precision",
     "dart_attention_force_safe",
     "dart_attention_trace",
@@ -172,6 +173,8 @@ def load() -> ctypes.CDLL:
     lib.dart_mlp_fused_ln.restype = ctypes.c_int
     lib.dart_gemm_force_splitk.argtypes = [I32]
     lib.dart_gemm_force_splitk.restype = None
+    lib.dart_set_pdl.argtypes = [I32]
+    lib.dart_set_pdl.restype = None
     lib.dart_gemm_force_precision.argtypes = [I32]
     lib.dart_gemm_force_precision.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,

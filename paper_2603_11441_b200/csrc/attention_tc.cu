@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // Q / K / V of the previous kernel complete
 
   // pipeline state, continued across the two passes
   int p_it = 0, p_g = 0, pv_g = 0;  // producer (Q/K thread, V thread)
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         softmax_pass(std::integral_constant<int, 1>{});
     }
   }
+  pdl_launch_dependents();  // every item of this CTA is done: the next kernel may start its prologue
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -507,7 +509,18 @@ int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& 
     b.z_base = a.z_base + z0;
     const long long items = per_z * b.items;
     const int grid = (int)(items < max_grid ? items : max_grid);
-    kern<<<grid, Lay::THREADS, Lay::TOTAL, stream>>>(tmQ, tmKV, b);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Lay::THREADS);
+    cfg.dynamicSmemBytes = Lay::TOTAL;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    if (pdl_enabled()) {
+      pdl_attr(attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, kern, tmQ, tmKV, b);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
   }

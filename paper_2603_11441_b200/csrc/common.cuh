@@ -55,6 +55,21 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-stream-serialization
+// attribute may start (prologue: barrier init, TMEM allocation, descriptor prefetch) while its
+// predecessor on the stream is still draining; pdl_wait() then blocks until the predecessor has
+// completed and its memory is visible, so every global access of such a kernel comes after it.
+// pdl_launch_dependents() lets the NEXT kernel be scheduled from this point on.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Host side: DART_NO_PDL=1 launches everything fully serialised (A/B).
+bool pdl_enabled();
+void pdl_set_thread(int mode);  // dart_set_pdl
+inline void pdl_attr(cudaLaunchAttribute& a) {
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -1214,6 +1214,7 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
   return DART_OK;
 }
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
+void dart_set_pdl(int32_t mode) { pdl_set_thread(mode); }
 void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
 int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,

@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the previous kernel's outputs (our A / residual) are complete from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (lane == 0) bulk_wait_all();  // output writes landed before the CTA retires
   }
+  pdl_launch_dependents();  // this CTA's work is issued: the next kernel may start its prologue
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync_all();  // the peer's MMAs / arrivals are done
@@ -737,6 +739,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
 
   // Ring sequence per unit: W1(0) W1(1) W2(0) W1(2) W2(1) ... W1(7) W2(6) W2(7); W1(e) = 4 k-blocks
   // (K = 256), W2(e) = 2 k-blocks (K = 128 hidden units of slice e).
@@ -948,6 +951,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (lane == 0) bulk_wait_all();
   }
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
@@ -967,24 +971,25 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
   const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID && SPLITK ? epi.splitk : 1);
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
-  if constexpr (CG == 1) {
-    kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(tA, tB, tB2, tC, tD, M, N, K, epi);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = L::TOTAL;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tB2, tC, tD, M, N, K, epi);
-    if (e != cudaSuccess) return (int)e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if constexpr (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (pdl_enabled()) pdl_attr(attr[na++]);
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tB2, tC, tD, M, N, K, epi);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 
@@ -1052,13 +1057,15 @@ int mlp_fused(const CUtensorMap& tH, const CUtensorMap& tW1, const CUtensorMap& 
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = mlpf::TOTAL;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_enabled()) pdl_attr(attr[na++]);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, mlp_fused_kernel, tH, tW1, tW2, tX, tLN, M, b1, b2, ln_g, ln_b);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();

@@ -23,6 +23,7 @@ template <int VPL, typename OutT, int RPW = 1>
 __global__ void layernorm_vec_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                      const float* __restrict__ beta, OutT* __restrict__ y, int rows, int ld_in,
                                      int ld_out) {
+  pdl_wait();
   constexpr int V4 = VPL / 4;
   const int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW;
   const int lane = threadIdx.x & 31;
@@ -86,6 +87,7 @@ template <int VPL, typename OutT>
 __global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                  const float* __restrict__ beta, OutT* __restrict__ y, int rows, int ld_in,
                                  int ld_out) {
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -134,21 +136,35 @@ int ln_dispatch(const float* x, const float* g, const float* b, OutT* y, int row
   if (rows <= 0) return 0;
   const int warps = g_ln_warps;
   const int rpw = g_ln_rpw;
+  // every LN launch may overlap its predecessor's tail (PDL; the kernel waits before reading x)
+  auto go = [&](auto kern, dim3 gr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = gr;
+    cfg.blockDim = dim3(warps * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (pdl_enabled()) {
+      pdl_attr(attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, kern, x, g, b, y, rows, ld_in, ld_out);
+  };
   dim3 grid((rows + warps - 1) / warps);
   if (rpw == 2 && (dim == 256 || dim == 1280)) {
     dim3 g2((rows + 2 * warps - 1) / (2 * warps));
-    if (dim == 256) layernorm_vec_kernel<8, OutT, 2><<<g2, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out);
-    else layernorm_vec_kernel<40, OutT, 2><<<g2, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out);
+    if (dim == 256) go(layernorm_vec_kernel<8, OutT, 2>, g2);
+    else go(layernorm_vec_kernel<40, OutT, 2>, g2);
     return (int)cudaGetLastError();
   }
   switch (dim) {
-    case 32: layernorm_kernel<1, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 64: layernorm_kernel<2, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 128: layernorm_kernel<4, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 256: layernorm_vec_kernel<8, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 512: layernorm_vec_kernel<16, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 1024: layernorm_vec_kernel<32, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
-    case 1280: layernorm_vec_kernel<40, OutT><<<grid, warps * 32, 0, st>>>(x, g, b, y, rows, ld_in, ld_out); break;
+    case 32: go(layernorm_kernel<1, OutT>, grid); break;
+    case 64: go(layernorm_kernel<2, OutT>, grid); break;
+    case 128: go(layernorm_kernel<4, OutT>, grid); break;
+    case 256: go(layernorm_vec_kernel<8, OutT>, grid); break;
+    case 512: go(layernorm_vec_kernel<16, OutT>, grid); break;
+    case 1024: go(layernorm_vec_kernel<32, OutT>, grid); break;
+    case 1280: go(layernorm_vec_kernel<40, OutT>, grid); break;
     default: return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
@@ -337,6 +353,14 @@ int heads_forward(const float* qf, int rows_per_item, int nq, int items, int d, 
       qf, rows_per_item, nq, items, d, w_box, b_box, w_score, b_score, w_pres, b_pres, boxes, scores, presence,
       qf_out);
   return (int)cudaGetLastError();
+}
+
+// -1: the process default (on unless DART_NO_PDL is set); 0 / 1: this host thread's launches
+thread_local int g_pdl_thread = -1;
+void pdl_set_thread(int mode) { g_pdl_thread = mode < 0 ? -1 : (mode ? 1 : 0); }
+bool pdl_enabled() {
+  static const bool on = getenv("DART_NO_PDL") == nullptr;
+  return g_pdl_thread >= 0 ? g_pdl_thread == 1 : on;
 }
 
 }  // namespace dart
