@@ -285,10 +285,15 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             }
             tc_fence_after();
             const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
+            if constexpr (SPLIT == 1) {  // P of key 16*kc at column 8*kc, V rows 16*kc at +512 B
+              umma_f16_ts_seq_w<BKV / 16, 8, 512 / 16>(tmem + L::OCOL, tmem + sb * BKV, desc_sw32(sv, L::KV_BLOCK, 256),
+                                                       idesc_pv, j != 0);
+            } else {
 #pragma unroll
-            for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
-              umma_f16_ts_w(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16), desc_sw32(sv + kc * 512, L::KV_BLOCK, 256),
-                          idesc_pv, (j | kc) != 0);
+              for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
+                umma_f16_ts_w(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16),
+                              desc_sw32(sv + kc * 512, L::KV_BLOCK, 256), idesc_pv, (j | kc) != 0);
+            }
             if (trace && blockIdx.x == 0 && lane == 0 && m_g < 256) trace[1280 + m_g] = clock64();
             if constexpr (LEAN) {
               if (pass == 1) umma_commit_w(&o_done[m_g1++ % NS]);

@@ -230,6 +230,37 @@ __device__ __forceinline__ void umma_f16_ts_w(uint32_t tmem_d, uint32_t tmem_a, 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// NK back-to-back TS-form MMAs D += A_k * B_k, A_k = tmem_a + k*A_STEP columns, B_k = b_desc +
+// k*B_STEP (descriptor units of 16 bytes), the first accumulating iff acc_first: ONE elect and one
+// uniform conversion of the operands for the whole sequence (the per-MMA form costs ~20 issue
+// slots each on the issuing warp's SM sub-partition, which a softmax warp shares).
+#define DART_TS_NEXT                                   \
+  "add.u32 ta, ta, %5;\n\tadd.u64 bd, bd, %6;\n\t" \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, 1;\n\t"
+#define DART_TS_HEAD                                                                          \
+  "{\n\t.reg .pred p, e;\n\t.reg .b32 ta;\n\t.reg .b64 bd;\n\t"                              \
+  "setp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\tmov.b32 ta, %1;\n\tmov.b64 bd, %2;\n\t" \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %3, p;\n\t"
+template <int NK, int A_STEP, int B_STEP>
+__device__ __forceinline__ void umma_f16_ts_seq_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t acc_first) {
+  static_assert(NK == 2 || NK == 4 || NK == 6 || NK == 8, "sequence length");
+#define DART_TS_OPS                                                                                      \
+  ::"r"(tmem_d), "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(acc_first), "n"(A_STEP), "n"((uint64_t)B_STEP)
+  if constexpr (NK == 2)
+    asm volatile(DART_TS_HEAD DART_TS_NEXT "}" DART_TS_OPS);
+  else if constexpr (NK == 4)
+    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT "}" DART_TS_OPS);
+  else if constexpr (NK == 6)
+    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT "}" DART_TS_OPS);
+  else
+    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT
+                     DART_TS_NEXT "}" DART_TS_OPS);
+#undef DART_TS_OPS
+}
+#undef DART_TS_NEXT
+#undef DART_TS_HEAD
+
 __device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -431,7 +462,8 @@ __device__ __forceinline__ float ffma_sat(float a, float b, float c) {
   asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
 }
-// 2^(s*c+nb) for a pair on the FMA pipe; cr = c/R, br = (nb - XMIN)/R.
+// 2^(s*c+nb) for a pair on the FMA pipe; cr = c/R, br = (nb - XMIN)/R.  (Folding the rounding into
+// one FFMA2, t = fma(y, R, XMIN + M), saves one packed op but measured 3-5% slower at hd 16.)
 __device__ __forceinline__ void exp2_poly2_sat(float s0, float s1, float cr, float br, float& x0, float& x1) {
   const uint64_t y = f2_pack(ffma_sat(s0, cr, br), ffma_sat(s1, cr, br));
   const uint64_t x = ffma2(y, f2_pack(EXP_R, EXP_R), f2_pack(EXP_XMIN, EXP_XMIN));
