@@ -551,7 +551,9 @@ int fa_variant() {
   X(0, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
   X(1, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
   X(2, 16, 96, 4, 2, 2, 1, 8, 0, 0) \
-  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 0)
+  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 0)   \
+  X(4, 16, 96, 4, 2, 2, 2, 6, 16, 0)  \
+  X(5, 16, 80, 4, 2, 2, 1, 6, 16, 0)
 // Variant 0 issues MMAs from the converged warp 1 (warp-collective umma_*_w, one elected lane):
 // the per-MMA issue path shrank from ~77 to ~40 clk (no per-lane R2UR waterfall), which took hd 80
 // global attention 217 -> 193 us and windowed 36.5 -> 33.2 us (scripts/ab_attn.py); with it the
@@ -594,14 +596,16 @@ int attention_tc_kv_tile(int head_dim, int Lkv) {
 
 bool attention_tc_supported(int head_dim, int Lkv) {
   const int t = attention_tc_kv_tile(head_dim, Lkv);
-  return t > 0 && Lkv >= 1 && (Lkv % t == 0 || fa_variant() == 0);  // ragged Lkv: masked production kernel
+  return t > 0 && Lkv >= 1;  // ragged Lkv: masked instantiation
 }
 
 int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream) {
   const int var = fa_variant();
 #define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
-  if (V != 0 && head_dim == HD && var == V) return launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN>(tmQ, tmKV, a, num_sms, stream);
+  if (V != 0 && head_dim == HD && var == V)                                                  \
+    return a.Lkv % BKV ? launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN, true>(tmQ, tmKV, a, num_sms, stream) \
+                       : launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN>(tmQ, tmKV, a, num_sms, stream);
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
 #undef X

@@ -244,18 +244,31 @@ __device__ __forceinline__ void umma_f16_ts_w(uint32_t tmem_d, uint32_t tmem_a, 
 template <int NK, int A_STEP, int B_STEP>
 __device__ __forceinline__ void umma_f16_ts_seq_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b_desc, uint32_t idesc,
                                                   uint32_t acc_first) {
-  static_assert(NK == 2 || NK == 4 || NK == 6 || NK == 8, "sequence length");
+  static_assert(NK >= 1 && NK <= 8, "sequence length");
 #define DART_TS_OPS                                                                                      \
   ::"r"(tmem_d), "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(acc_first), "n"(A_STEP), "n"((uint64_t)B_STEP)
-  if constexpr (NK == 2)
-    asm volatile(DART_TS_HEAD DART_TS_NEXT "}" DART_TS_OPS);
+#define N1 DART_TS_NEXT
+#define N2 N1 N1
+#define N4 N2 N2
+  if constexpr (NK == 1)
+    asm volatile(DART_TS_HEAD "}" DART_TS_OPS);
+  else if constexpr (NK == 2)
+    asm volatile(DART_TS_HEAD N1 "}" DART_TS_OPS);
+  else if constexpr (NK == 3)
+    asm volatile(DART_TS_HEAD N2 "}" DART_TS_OPS);
   else if constexpr (NK == 4)
-    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT "}" DART_TS_OPS);
+    asm volatile(DART_TS_HEAD N2 N1 "}" DART_TS_OPS);
+  else if constexpr (NK == 5)
+    asm volatile(DART_TS_HEAD N4 "}" DART_TS_OPS);
   else if constexpr (NK == 6)
-    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT "}" DART_TS_OPS);
+    asm volatile(DART_TS_HEAD N4 N1 "}" DART_TS_OPS);
+  else if constexpr (NK == 7)
+    asm volatile(DART_TS_HEAD N4 N2 "}" DART_TS_OPS);
   else
-    asm volatile(DART_TS_HEAD DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT DART_TS_NEXT
-                     DART_TS_NEXT "}" DART_TS_OPS);
+    asm volatile(DART_TS_HEAD N4 N2 N1 "}" DART_TS_OPS);
+#undef N4
+#undef N2
+#undef N1
 #undef DART_TS_OPS
 }
 #undef DART_TS_NEXT
