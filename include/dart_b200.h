@@ -121,6 +121,36 @@ int dart_encdec_prefix(dart_model* m, const float* l0, int32_t B, float* e1, voi
 int dart_encdec_from_prefix(dart_model* m, const float* e1, int32_t B, const float* text, int32_t N, double* boxes,
                             double* score_logits, double* presence_logits, float* query_features, void* stream);
 
+/* The model description a handle was created with (dimensions of its workspaces). */
+const dart_model_desc* dart_model_get_desc(const dart_model* m);
+
+/* ---- NCCL helpers for class sharding across GPUs ----
+ * One communicator per rank (one rank per GPU); libnccl.so.2 is opened at first use, so a host
+ * without NCCL still loads the library (dart_nccl_available() == 0 then).  Every call only
+ * enqueues on `stream`.  Unique-id exchange between the ranks is the caller's (any side channel:
+ * torch.distributed, MPI, a file).  Replaces the torch.distributed collectives of
+ * paper_2603_11441_b200/distributed.py:class_sharded_raw for hosts without torch. */
+#define DART_NCCL_ID_BYTES 128
+typedef struct dart_comm dart_comm;
+int dart_nccl_available(void);
+int dart_nccl_unique_id(uint8_t* id /* [DART_NCCL_ID_BYTES], host */);
+int dart_nccl_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, dart_comm** out);
+void dart_nccl_comm_destroy(dart_comm* c);
+int32_t dart_nccl_comm_size(const dart_comm* c);
+int32_t dart_nccl_comm_rank(const dart_comm* c);
+/* recv [nranks * bytes_per_rank] <- send [bytes_per_rank] of every rank, in rank order */
+int dart_nccl_all_gather(dart_comm* c, const void* send, void* recv, int64_t bytes_per_rank, void* stream);
+int dart_nccl_all_reduce_max_i32(dart_comm* c, int32_t* buf, int64_t count, void* stream);
+/* One class-sharded round (model.py:513-517 prefix, 559-564 class loop): this rank's images
+ * [B, S, S, 3] -> backbone + enc-dec prefix -> all-gather of e1 (fp32) -> this rank's contiguous
+ * class shard (ClassShardPlan: the first N % W ranks get ceil(N/W) classes) of text [N, L_t, d]
+ * decoded for all W*B images -> all-gather of the raw outputs -> boxes [B*N, Q, 4], score_logits
+ * [B*N, Q], presence_logits [B*N] float64 of THIS rank's images over all N classes (item b*N+c,
+ * bitwise equal to dart_encdec on the same images), flags (zeroed by the caller) MAX-reduced
+ * over the ranks.  Every rank must call it with the same B and N. */
+int dart_class_sharded(dart_model* m, dart_comm* c, const float* images, int32_t B, const float* text, int32_t N,
+                       double* boxes, double* score_logits, double* presence_logits, int32_t* flags, void* stream);
+
 /* Presence gate, score gate, (score desc, query asc) ordering and greedy per-class NMS,
  * decisions in fp64 (pipeline.py:243-294).  Inputs float64 [N,Q,4] / [N,Q] / [N].  For N items of Q queries:
  *   kept_count [N] int32, kept_query [N, Q] int32, kept_score [N, Q] float64 (sigmoid),

@@ -36,6 +36,16 @@ EXPORTS = (
     "dart_encdec_prefix",
     "dart_encdec_from_prefix",
     "dart_postprocess",
+    "dart_model_get_desc",
+    "dart_nccl_available",
+    "dart_nccl_unique_id",
+    "dart_nccl_comm_create",
+    "dart_nccl_comm_destroy",
+    "dart_nccl_comm_size",
+    "dart_nccl_comm_rank",
+    "dart_nccl_all_gather",
+    "dart_nccl_all_reduce_max_i32",
+    "dart_class_sharded",
     "dart_model_set_mask_head",
     "dart_mask_head",
     "dart_gemm",
@@ -153,6 +163,26 @@ def load() -> ctypes.CDLL:
     lib.dart_encdec_from_prefix.restype = ctypes.c_int
     lib.dart_postprocess.argtypes = [P, P, P, P, I32, I32, F64, F64, F64, I32, P, P, P, P, P, P, P]
     lib.dart_postprocess.restype = ctypes.c_int
+    lib.dart_model_get_desc.argtypes = [P]
+    lib.dart_model_get_desc.restype = ctypes.POINTER(ModelDesc)
+    lib.dart_nccl_available.argtypes = []
+    lib.dart_nccl_available.restype = ctypes.c_int
+    lib.dart_nccl_unique_id.argtypes = [P]
+    lib.dart_nccl_unique_id.restype = ctypes.c_int
+    lib.dart_nccl_comm_create.argtypes = [P, I32, I32, ctypes.POINTER(ctypes.c_void_p)]
+    lib.dart_nccl_comm_create.restype = ctypes.c_int
+    lib.dart_nccl_comm_destroy.argtypes = [P]
+    lib.dart_nccl_comm_destroy.restype = None
+    lib.dart_nccl_comm_size.argtypes = [P]
+    lib.dart_nccl_comm_size.restype = I32
+    lib.dart_nccl_comm_rank.argtypes = [P]
+    lib.dart_nccl_comm_rank.restype = I32
+    lib.dart_nccl_all_gather.argtypes = [P, P, P, ctypes.c_int64, P]
+    lib.dart_nccl_all_gather.restype = ctypes.c_int
+    lib.dart_nccl_all_reduce_max_i32.argtypes = [P, P, ctypes.c_int64, P]
+    lib.dart_nccl_all_reduce_max_i32.restype = ctypes.c_int
+    lib.dart_class_sharded.argtypes = [P, P, P, I32, P, I32, P, P, P, P, P]
+    lib.dart_class_sharded.restype = ctypes.c_int
     lib.dart_model_set_mask_head.argtypes = [P, P, P, P, P]
     lib.dart_model_set_mask_head.restype = ctypes.c_int
     lib.dart_mask_head.argtypes = [P, P, I32, I32, P, P, P]

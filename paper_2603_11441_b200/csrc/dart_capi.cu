@@ -682,6 +682,7 @@ int xmlp(dart_model* m, float* x, const LNW& ln, const GemmW& fc1, const GemmW& 
 extern "C" {
 
 const char* dart_last_error(void) { return g_last_error.c_str(); }
+const dart_model_desc* dart_model_get_desc(const dart_model* m) { return m ? &m->d : nullptr; }
 const char* dart_version(void) { return "dart-b200 0.2 (sm_100a, tcgen05 GEMM + tcgen05 flash attention)"; }
 
 int32_t dart_expected_weight_count(const dart_model_desc* d) {
@@ -1344,3 +1345,8 @@ extern "C" int dart_attention_qkv(const void* qkv, void* o, int32_t items, int32
   return attn_tc_packed((const __half*)qkv, (__half*)o, items, heads, L, hd, heads * hd, sms, (cudaStream_t)stream,
                         debug_host);
 }
+
+// error channel of the other C-ABI translation units (nccl_shard.cu)
+namespace dart {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace dart

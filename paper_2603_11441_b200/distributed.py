@@ -215,3 +215,75 @@ class NativeEngine:
         from .model import raise_for_flags
 
         raise_for_flags(flags)
+
+
+class NcclComm:
+    """A communicator of the C ABI's own NCCL helpers (dart_nccl_*, include/dart_b200.h): the
+    class-sharded round without torch.distributed on the data path.  The 128-byte unique id is
+    created on rank 0 and handed to the other ranks over `group` (any torch.distributed backend;
+    host bytes only), or passed in directly (`unique_id`)."""
+
+    def __init__(self, world: int, rank: int, group=None, unique_id: bytes | None = None, device=None):
+        import ctypes
+
+        import torch
+
+        from . import _native
+
+        self.lib = _native.load()
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if not self.lib.dart_nccl_available():
+            raise RuntimeError("dart_nccl_*: libnccl.so.2 could not be opened")
+        if unique_id is None:
+            buf = (ctypes.c_uint8 * 128)()
+            if rank == 0:
+                _native.check(self.lib.dart_nccl_unique_id(buf))
+            if world > 1:
+                import torch.distributed as dist
+
+                obj = [bytes(buf)]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                buf = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        else:
+            buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        out = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.dart_nccl_comm_create(buf, world, rank, ctypes.byref(out)))
+        self.ptr = out.value
+        self.world, self.rank = world, rank
+
+    def close(self):
+        if self.ptr:
+            self.lib.dart_nccl_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def class_sharded_raw_native(engine, comm: NcclComm, images, class_names):
+    """`class_sharded_raw` through the C ABI (dart_class_sharded): one call per round, all
+    collectives inside the library.  images [B, S, S, 3] (this rank's); returns boxes [B, N, Q, 4],
+    score logits [B, N, Q], presence logits [B, N] (float64, device) of this rank's images over
+    all N classes, and the rank-reduced flags (int32 [1]).  Asynchronous on the current stream."""
+    import torch
+
+    from . import _native
+    from .model import _stream_ptr, device_text, text_encode
+
+    names = list(class_names)
+    imgs = images.to(device=engine.device, dtype=torch.float32).contiguous()
+    B, N, Q = int(imgs.shape[0]), len(names), engine.num_queries
+    text = device_text(engine.model, text_encode(engine.model, names).stack(names), engine.device).contiguous()
+    boxes = torch.empty((B, N, Q, 4), device=engine.device, dtype=torch.float64)
+    scores = torch.empty((B, N, Q), device=engine.device, dtype=torch.float64)
+    pres = torch.empty((B, N), device=engine.device, dtype=torch.float64)
+    flags = torch.zeros((1,), device=engine.device, dtype=torch.int32)
+    with torch.cuda.device(engine.device):
+        _native.check(engine.lib.dart_class_sharded(engine.handle.ptr, comm.ptr, imgs.data_ptr(), B, text.data_ptr(), N,
+                                                    boxes.data_ptr(), scores.data_ptr(), pres.data_ptr(),
+                                                    flags.data_ptr(), _stream_ptr(engine.device)))
+    return boxes, scores, pres, flags

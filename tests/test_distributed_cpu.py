@@ -153,3 +153,20 @@ def test_shard_plan_covers_all_classes():
                 assert 0 <= e - s <= plan.width
                 covered.extend(range(s, e))
             assert covered == list(range(n))
+
+
+def test_native_unpack_owner_arithmetic_matches_plan():
+    """The owner / shard-start arithmetic of nccl_shard.cu:unpack_raw_kernel, restated, agrees
+    with ClassShardPlan.bounds for every class of every (N, W) up to 9 ranks."""
+    from paper_2603_11441_b200.distributed import ClassShardPlan
+
+    for world in range(1, 10):
+        for n in range(1, 90):
+            plan = ClassShardPlan(n, world)
+            base, extra = divmod(n, world)
+            big = extra * (base + 1)
+            for cls in range(n):
+                owner = cls // (base + 1) if cls < big else extra + (cls - big) // (base if base > 0 else 1)
+                start = owner * base + min(owner, extra)
+                s, e = plan.bounds(owner)
+                assert s == start and s <= cls < e and cls - start < plan.width
