@@ -196,6 +196,10 @@ int dart_gemm_resid_ln(const void* A, const void* W, const float* bias, float* x
                        const float* ln_b, int32_t M, int32_t K, void* stream);
 void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg);
 void dart_gemm_force_plan(int32_t bn, int32_t cg);
+/* Timeline microbenchmarks: per-CTA %globaltimer stamps (8 int64 per CTA: entry, after the PDL
+ * wait, first operand stage landed, first / last accumulator committed, first accumulator seen by
+ * the epilogue, epilogue done, exit) of every following GEMM launch into device_buf; NULL = off. */
+int dart_gemm_trace(int64_t* device_buf);
 /* Fused enc-dec MLP (reference _mlp_forward, model.py:505-508, d = 256, hidden 1024):
  * x[M, 256] += relu(h W1^T + b1) W2^T + b2, h fp16 [M, 256], W1 fp16 [1024, 256], W2 fp16 [256, 1024]
  * (both [out, in]), x fp32; the hidden activations never leave the SM (TMEM). */

@@ -52,6 +52,7 @@ EXPORTS = (
     "dart_gemm_plan",
     "dart_gemm_resid_ln",
     "dart_gemm_force_plan",
+    "dart_gemm_trace",
     "dart_layernorm",
     "dart_mlp_fused",
     "dart_mlp_fused_ln",
@@ -195,6 +196,8 @@ def load() -> ctypes.CDLL:
     lib.dart_gemm_plan.restype = None
     lib.dart_gemm_force_plan.argtypes = [I32, I32]
     lib.dart_gemm_force_plan.restype = None
+    lib.dart_gemm_trace.argtypes = [P]
+    lib.dart_gemm_trace.restype = ctypes.c_int
     lib.dart_layernorm.argtypes = [P, P, P, P, I32, I32, I32, P]
     lib.dart_layernorm.restype = ctypes.c_int
     lib.dart_mlp_fused.argtypes = [P, P, P, P, P, P, I32, P]

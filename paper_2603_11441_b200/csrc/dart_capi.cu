@@ -1205,6 +1205,7 @@ void dart_gemm_plan(int32_t M, int32_t N, int32_t epi, int32_t* bn, int32_t* cg)
 }
 
 void dart_gemm_force_plan(int32_t bn, int32_t cg) { gemm_force_plan(bn, cg); }
+int dart_gemm_trace(int64_t* device_buf) { return gemm_set_trace((long long*)device_buf); }
 
 int dart_layernorm(const float* x, const float* gamma, const float* beta, void* y, int32_t rows, int32_t dim,
                    int32_t out_f16, void* stream) {

@@ -320,6 +320,20 @@ constexpr int GEMM_THREADS = 384;
 // PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
 // path's instantiations (PREC = false) carry none of that code.  SPLITK: the opt-in split-K
 // residual variant (GemmEpi::splitk); without it the split-K paths compile out.
+// dart_gemm_trace: per-CTA globaltimer stamps of the first GEMM launch after it is set (timeline
+// microbenchmarks; nullptr = off, one predicated global load per stamp site)
+__device__ long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GEMM_STAMP(k)                                                   \
+  do {                                                                  \
+    long long* _tr = g_gemm_trace;                                      \
+    if (_tr) _tr[blockIdx.x * 8 + (k)] = gtimer();                      \
+  } while (0)
+
 template <int BN, int STAGES, int EPI, int CG, bool PREC, bool SPLITK>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -386,7 +400,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GEMM_STAMP(0);
   pdl_wait();  // the previous kernel's outputs (our A / residual) are complete from here on
+  if (threadIdx.x == 0) GEMM_STAMP(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -443,6 +459,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (it == 0 && kb == 0 && lane == 0) GEMM_STAMP(2);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
           const uint32_t sb = sa + L::A_BYTES;
@@ -460,6 +477,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         umma_commit_cg<CG>(&tfull[acc]);
+        if (lane == 0) GEMM_STAMP(it == 0 ? 3 : 6);
       }
     }
   } else if (warp >= 4) {
@@ -520,6 +538,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0);
       const int row0 = m0 + quarter * 32;
       mbar_wait(&tfull[acc], acc_phase);
+      if (it == 0 && warp == 4 && lane == 0) GEMM_STAMP(4);
       tc_fence_after();
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
@@ -651,6 +670,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_all();  // output writes landed before the CTA retires
+    if (warp == 4 && lane == 0) GEMM_STAMP(5);
   }
   pdl_launch_dependents();  // this CTA's work is issued: the next kernel may start its prologue
   tc_fence_before();
@@ -660,6 +680,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc_cg<L::TMEM_COLS, CG>(tmem_base);
   }
+  if (threadIdx.x == 0) GEMM_STAMP(7);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1106,6 +1127,10 @@ GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
 }
 
 void gemm_force_plan(int bn, int cg) { g_forced = GemmPlan{bn, cg == 2 ? 2 : 1}; }
+
+int gemm_set_trace(long long* device_buf) {
+  return (int)cudaMemcpyToSymbol(g_gemm_trace, &device_buf, sizeof(device_buf));
+}
 
 int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2, const CUtensorMap* tC,
             const CUtensorMap* tD, int M, int N, int K, GemmPlan plan, int epi_mode, const GemmEpi& epi_in, int num_sms,

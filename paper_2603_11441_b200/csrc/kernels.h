@@ -76,7 +76,8 @@ struct GemmPlan {
   int bn, cg;
 };
 GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms);
-void gemm_force_plan(int bn, int cg);  // bn 0: automatic
+void gemm_force_plan(int bn, int cg);
+int gemm_set_trace(long long* device_buf);  // bn 0: automatic
 // tA: map over A [M, K] with box {64, 128}; tB: map over W [N, K] with box {64, plan.bn / plan.cg}.
 // Output maps over out [M, N] (row stride ldo), box {32, 32}: tC fp32 with 128B swizzle
 // (EPI_F32 / EPI_F32_F16 without wm_scatter, and the EPI_F32_RESID residual), tD fp16 with 64B
