@@ -646,7 +646,10 @@ def gemm_roofline(cfg, dev, args, stream):
     out = torch.zeros(M, E, device=dev, dtype=torch.float32)
     bias = torch.zeros(E, device=dev)
     res, res_pdl = {}, {}
-    for name, K in (("attn.out", E), ("mlp.fc2", 4 * E)):
+    # as the backbone runs them: split-K only when DART_SPLITK (mask bits 2 / 4; off by default) asks
+    mask = int(os.environ.get("DART_SPLITK", "0"))
+    for name, K, bit in (("attn.out", E, 2), ("mlp.fc2", 4 * E, 4)):
+        lib.dart_gemm_force_splitk(2 if mask & bit else 1)
         A = torch.randn(M, K, device=dev).half()
         W = (torch.randn(E, K, device=dev) / K ** 0.5).half()
         call = lambda A=A, W=W, K=K: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(),
@@ -659,6 +662,7 @@ def gemm_roofline(cfg, dev, args, stream):
         lib.dart_set_pdl(1)
         res_pdl[name] = (2.0 * M * E * K, _time_launches(call, stream))
         lib.dart_set_pdl(-1)
+        lib.dart_gemm_force_splitk(1)
     flop = sum(f for f, _ in res.values())
     t = sum(s for _, s in res.values())
     t_pdl = sum(s for _, s in res_pdl.values())
@@ -672,7 +676,8 @@ def gemm_roofline(cfg, dev, args, stream):
             traffic = sum(tj[k]["dram_read_bytes"] + tj[k]["dram_write_bytes"] for k in ("attn.out", "mlp.fc2")) / 2
     except Exception:
         pass
-    return {"kernel": "gemm_tc_kernel, fp32 residual epilogue (backbone attn.out + mlp.fc2; 1 of each per block)",
+    return {"kernel": "gemm_tc_kernel, fp32 residual epilogue (backbone attn.out + mlp.fc2; 1 of each per block)"
+                      + (", split-K" if mask & 6 else ""),
             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_kind": f"{pk_kind} burst bf16/fp16 dense",
             "flop_per_launch": flop / 2, "us_per_launch": t / 2 * 1e6,

@@ -100,9 +100,14 @@ bool tc_attention_enabled() {
 
 // Tests: route every tcgen05 attention item through the max-tracking (overflow-safe) pass too.
 int g_attn_force_safe = 0;
-// split-K for long-K residual GEMMs: measured slower on B200 (fc2 64.5 -> 68.4 us: the half-1
-// epilogue waits behind half 0's), so opt-in (DART_SPLITK=1) for A/B measurement only
-int g_splitk_enabled = getenv("DART_SPLITK") != nullptr;
+// Split-K (two K halves per tile, partial-accumulator combine; gemm_tc.cu) for the backbone GEMMs
+// whose tile count leaves a badly filled last wave at one image (5184 rows): bit 1 QKV (315
+// CTA-pair tiles = 4.26 waves on 74 pairs), bit 2 attn.out and bit 4 mlp.fc2 (105 tiles = 1.42
+// waves).  Chosen per (N, K) only, so the arithmetic of a row never depends on the batch size.
+// Off by default: measured slower on every shape (profiles/r02/gemm_splitk.log -- a CTA writes its
+// 128 KB fp32 partial at ~26 GB/s, ~5 us, as long as the attn.out half-tile main loop).
+// DART_SPLITK=<mask> enables it for A/B measurement.
+int g_splitk_mask = getenv("DART_SPLITK") ? atoi(getenv("DART_SPLITK")) : 0;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
@@ -263,11 +268,15 @@ struct dart_model {
   // 1 fp16 storage (outputs and residual rounded to fp16), 2 fp16 storage + fp16 accumulation
   int precision = 0;
   bool in_backbone = false;  // set while a backbone stage issues its GEMMs
-  int* splitk_flags = nullptr;  // per handle (a fork gets its own): split-K tile flags
-  int splitk_cap = 0;
+  // split-K claim flags and partial accumulators, per handle (a fork gets its own)
+  int* splitk_flags = nullptr;
+  long long splitk_cap = 0;  // flags
+  float* splitk_ws = nullptr;
+  long long splitk_ws_cap = 0;  // floats
 
   ~dart_model() {
     if (splitk_flags) cudaFree(splitk_flags);
+    if (splitk_ws) cudaFree(splitk_ws);
     bb_ws.release();
     ed_ws.release();
     mask_ws.release();
@@ -417,23 +426,41 @@ int gemm(dart_model* m, const __half* A, int M, int lda, const GemmW& W, int epi
   m->launches++;
   CUtensorMap tc, td;
   if (!make_out_maps(epi, e, M, W.N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
-  const GemmPlan plan = gemm_plan(M, W.N, epi, m->num_sms);
-  // long-K residual GEMMs (backbone fc2, K = 4E), opt-in: two K halves per tile on different CTA
-  // pairs (deterministic half-0-then-half-1 residual adds) to halve the wave-quantisation tail
-  if (epi == EPI_F32_RESID && W.K >= 4096 && (W.K / 64) % 2 == 0 && g_splitk_enabled) {
-    const int tiles = ((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (W.N / plan.bn);
-    if (!m->splitk_flags || tiles > m->splitk_cap) {
+  int bit = 0;
+  if (m->in_backbone && m->precision == 0 && (W.K / 64) % 2 == 0 && epi != EPI_F32_RESID_LN) {
+    if (W.N == 3 * m->E && W.K == m->E) bit = 1;    // attn.qkv
+    else if (W.N == m->E && W.K == m->E) bit = 2;   // attn.out
+    else if (W.N == m->E && W.K > m->E) bit = 4;    // mlp.fc2
+  }
+  const int splitk = (g_splitk_mask & bit) ? 2 : 1;
+  const GemmPlan plan = gemm_plan(M, W.N, epi, m->num_sms, splitk);
+  if (splitk == 2) {
+    const long long tiles = (long long)((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (W.N / plan.bn);
+    const long long nflags = splitk_flag_count(tiles, plan.cg), nws = splitk_ws_floats(tiles, plan.bn, plan.cg);
+    if (nflags > m->splitk_cap) {  // new flags start at zero; the combining warps reset them after use
       if (m->splitk_flags) cudaFree(m->splitk_flags);
-      m->splitk_cap = tiles < 4096 ? 4096 : tiles;
-      if (cudaMalloc(&m->splitk_flags, m->splitk_cap * sizeof(int)) != cudaSuccess) {
+      m->splitk_flags = nullptr;
+      m->splitk_cap = 0;
+      if (cudaMalloc(&m->splitk_flags, nflags * sizeof(int)) != cudaSuccess ||
+          cudaMemsetAsync(m->splitk_flags, 0, nflags * sizeof(int), s) != cudaSuccess) {
         m->splitk_flags = nullptr;
         return fail(DART_ERR_CUDA, "split-K flag allocation failed");
       }
+      m->splitk_cap = nflags;
     }
-    if (cudaMemsetAsync(m->splitk_flags, 0, tiles * sizeof(int), s) != cudaSuccess)
-      return fail(DART_ERR_CUDA, "split-K flag reset failed");
+    if (nws > m->splitk_ws_cap) {
+      if (m->splitk_ws) cudaFree(m->splitk_ws);
+      m->splitk_ws = nullptr;
+      m->splitk_ws_cap = 0;
+      if (cudaMalloc(&m->splitk_ws, nws * sizeof(float)) != cudaSuccess) {
+        m->splitk_ws = nullptr;
+        return fail(DART_ERR_CUDA, "split-K workspace allocation failed");
+      }
+      m->splitk_ws_cap = nws;
+    }
     e.splitk = 2;
     e.tile_flags = m->splitk_flags;
+    e.ws = m->splitk_ws;
   }
   const int half_rows = plan.bn / 2 / plan.cg;  // tail-halves B box (tiles of the last wave split in two)
   const CUtensorMap* tb2 = (half_rows == 128 || half_rows == 64 || half_rows == 32) && W.N % half_rows == 0
@@ -818,6 +845,8 @@ int dart_model_fork(const dart_model* parent, dart_model** out) {
   f->launches = 0;
   f->splitk_flags = nullptr;
   f->splitk_cap = 0;
+  f->splitk_ws = nullptr;
+  f->splitk_ws_cap = 0;
   *out = f;
   return DART_OK;
 }
@@ -1154,7 +1183,7 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const GemmPlan plan = gemm_plan(M, N, epi, sms);
+  const GemmPlan plan = gemm_plan(M, N, epi, sms, g_gemm_splitk == 2 && epi != EPI_F32_RESID_LN ? 2 : 1);
   CUtensorMap ta, tb, tc;
   if (!make_tmap(&ta, A, K, M, K, 128) || !make_tmap(&tb, W, K, N, K, plan.bn / plan.cg))
     return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -1175,17 +1204,29 @@ int dart_gemm(const void* A, const void* W, const float* bias, void* out, void* 
   e.acc_f16 = g_gemm_precision == 2;
   CUtensorMap td;
   if (!make_out_maps(epi, e, M, N, &tc, &td)) return fail(DART_ERR_CUDA, "cuTensorMapEncodeTiled failed (out)");
-  if (g_gemm_splitk == 2 && epi == EPI_F32_RESID && (K / 64) % 2 == 0) {  // tests: split-K residual path
-    static int* flags_of[64] = {};  // per device (tests only)
+  if (g_gemm_splitk == 2) {  // tests: the split-K path (flags and workspace per device, tests only)
+    static int* flags_of[64] = {};
+    static float* ws_of[64] = {};
+    static long long ws_cap_of[64] = {};
     int dev_id = 0;
     cudaGetDevice(&dev_id);
     int*& flags = flags_of[dev_id & 63];
-    if (!flags && cudaMalloc(&flags, 65536 * sizeof(int)) != cudaSuccess) return fail(DART_ERR_CUDA, "flags");
-    const int tiles = ((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (N / plan.bn);
-    if (tiles > 65536) return fail(DART_ERR_INVALID, "dart_gemm: too many split-K tiles");
-    cudaMemsetAsync(flags, 0, tiles * sizeof(int), (cudaStream_t)stream);
+    float*& ws = ws_of[dev_id & 63];
+    constexpr long long kFlags = 1 << 20;
+    const long long tiles = (long long)((M + 128 * plan.cg - 1) / (128 * plan.cg)) * (N / plan.bn);
+    if (splitk_flag_count(tiles, plan.cg) > kFlags) return fail(DART_ERR_INVALID, "dart_gemm: too many split-K tiles");
+    if (!flags && (cudaMalloc(&flags, kFlags * sizeof(int)) != cudaSuccess ||
+                   cudaMemset(flags, 0, kFlags * sizeof(int)) != cudaSuccess))
+      return fail(DART_ERR_CUDA, "flags");
+    const long long nws = splitk_ws_floats(tiles, plan.bn, plan.cg);
+    if (nws > ws_cap_of[dev_id & 63]) {
+      if (ws) cudaFree(ws);
+      if (cudaMalloc(&ws, nws * sizeof(float)) != cudaSuccess) return fail(DART_ERR_CUDA, "split-K workspace");
+      ws_cap_of[dev_id & 63] = nws;
+    }
     e.splitk = 2;
     e.tile_flags = flags;
+    e.ws = ws;
   }
   CUtensorMap tb2;
   const int half_rows = plan.bn / 2 / plan.cg;

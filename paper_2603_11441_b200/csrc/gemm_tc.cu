@@ -318,8 +318,9 @@ __device__ __forceinline__ void ln_rows_epilogue(uint32_t taddr, int quarter, in
 constexpr int GEMM_THREADS = 384;
 
 // PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
-// path's instantiations (PREC = false) carry none of that code.  SPLITK: the opt-in split-K
-// residual variant (GemmEpi::splitk); without it the split-K paths compile out.
+// path's instantiations (PREC = false) carry none of that code.  SPLITK: two K halves per tile
+// combined through a partial-accumulator workspace (GemmEpi::splitk); without it the split-K
+// paths compile out.
 // dart_gemm_trace: per-CTA globaltimer stamps of the first GEMM launch after it is set (timeline
 // microbenchmarks; nullptr = off, one predicated global load per stamp site)
 __device__ long long* g_gemm_trace = nullptr;
@@ -332,6 +333,12 @@ __device__ __forceinline__ long long gtimer() {
   do {                                                                  \
     long long* _tr = g_gemm_trace;                                      \
     if (_tr) _tr[blockIdx.x * 8 + (k)] = gtimer();                      \
+  } while (0)
+// per-unit stamps (first 8 units of a CTA) after the per-CTA block: [148 * 8][unit < 8][8]
+#define GEMM_STAMP_U(u, k)                                                              \
+  do {                                                                                  \
+    long long* _tr = g_gemm_trace;                                                      \
+    if (_tr && (u) < 8) _tr[148 * 8 + (blockIdx.x * 8 + (u)) * 8 + (k)] = gtimer();     \
   } while (0)
 
 template <int BN, int STAGES, int EPI, int CG, bool PREC, bool SPLITK>
@@ -360,11 +367,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
-  const int SK = (RESID && SPLITK) ? epi.splitk : 1;  // K slices per tile (work unit = tile x slice)
-  const int TF = epi.tail_full;           // tail halves: units >= TF are BN/2-wide halves of a tile
+  static_assert(!(SPLITK && L::LNO), "split-K is not combined with the full-row LayerNorm epilogue");
+  constexpr int SK = SPLITK ? 2 : 1;      // K halves per tile (work unit = tile x half)
+  const int TF = SPLITK ? 0 : epi.tail_full;  // tail halves: units >= TF are BN/2-wide halves of a tile
   const int num_units = TF > 0 ? TF + 2 * (num_tiles - TF) : num_tiles * SK;
   const int nk = K / BK / SK;             // k-blocks per unit
-  // unit -> (tile, K slice, n half or -1 for a full-width unit)
+  // unit -> (tile, K half, n half or -1 for a full-width unit).  Split-K: units 2t and 2t+1 are
+  // the two K halves of tile t, on neighbouring CTA pairs of the same wave, so a partial
+  // accumulator is consumed microseconds after it is written and stays in L2 (halves a wave
+  // apart keep ~a wave of partials in flight: 80 MB for the QKV shape, which spills to HBM)
   auto decode = [&](int u, int& tile, int& kh, int& nh) {
     if (TF > 0 && u >= TF) {
       tile = TF + ((u - TF) >> 1);
@@ -478,6 +489,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         umma_commit_cg<CG>(&tfull[acc]);
         if (lane == 0) GEMM_STAMP(it == 0 ? 3 : 6);
+        if (lane == 0) GEMM_STAMP_U(it, 0);  // unit's MMAs issued
       }
     }
   } else if (warp >= 4) {
@@ -504,25 +516,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const float2* rope_s = reinterpret_cast<const float2*>(smem + L::ROPE_OFF);
     // residual chunk g of this warp -> smem buffer g % NBUF (lane 0 issues; NBUF-1 chunks ahead)
     // residual prefetch iterator: (unit, chunk) of the next chunk this warp will process
-    int pf_u = cl, pf_c = 0;
+    // (split-K: no look-ahead across units -- only the half that combines reads the residual,
+    // and which half that is is decided when its epilogue starts)
+    int pf_u = SPLITK ? num_units : cl, pf_c = 0;
     auto resid_load = [&](int g) {  // prefetch the iterator's chunk into buffer g % NBUF, advance
       if (pf_u >= num_units) return;
       int t, kh, nh;
       decode(pf_u, t, kh, nh);
       const int bne = nh >= 0 ? BN / 2 : BN;
-      if (SK > 1 && kh == 1 && pf_c == 0) {  // split-K half 1 reads what half 0 of this tile stored
-        volatile int* f = epi.tile_flags + t;
-        while (*f < 8 * CG) __nanosleep(64);
-        __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
       const int rr = (t / num_n) * BM * CG + rank * BM + quarter * 32;
       const int cc = (t % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0) + (pf_c * 2 + half) * 32;
       mbar_arrive_expect_tx(&rbar[g % NBUF], 32 * 32 * 4);
       tma_load_2d(bufs + (g % NBUF) * BUF_F, &tmC, &rbar[g % NBUF], cc, rr);
       if (++pf_c == (bne - half * 32 + 63) / 64) {
         pf_c = 0;
-        pf_u += ncl;
+        pf_u = SPLITK ? num_units : pf_u + ncl;
       }
     };
     if (RESID && lane == 0)
@@ -539,9 +547,63 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row0 = m0 + quarter * 32;
       mbar_wait(&tfull[acc], acc_phase);
       if (it == 0 && warp == 4 && lane == 0) GEMM_STAMP(4);
+      if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 1);  // accumulator ready
       tc_fence_after();
       const int row = row0 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      [[maybe_unused]] int* sk_flag = nullptr;
+      [[maybe_unused]] const float4* sk_part = nullptr;
+      if constexpr (SPLITK) {
+        // claim: the first of the two K halves of this (tile, CTA, warp) to get here publishes
+        // its partial accumulator, the second combines (claim +1, publish +16)
+        sk_flag = epi.tile_flags + ((size_t)tile * CG + rank) * 8 + (warp - 4);
+        float4* part = reinterpret_cast<float4*>(epi.ws) + ((size_t)tile * CG + rank) * (BN / 32) * 4 * 256;
+        int old = 0;
+        if (lane == 0) old = atomicAdd(sk_flag, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if ((old & 15) == 0) {
+#pragma unroll 1
+          for (int c = half * 32; c < bn_eff; c += 64) {
+            float v[32];
+            tmem_ld32(taddr + c, v);
+            tmem_ld_wait();
+            if (c + 64 >= bn_eff) {  // accumulator fully read: hand TMEM back
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (CG == 1) {
+                  mbar_arrive(&tempty[acc]);
+                } else {
+                  mbar_arrive_leader(&tempty[acc]);
+                }
+              }
+            }
+            // [chunk column][quarter][float4 q][lane]: coalesced 512-byte rows for both halves
+            float4* p = part + ((c >> 5) * 4 + quarter) * 256 + lane;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcg(p + q * 32, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+          }
+          if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 2);  // partial stored
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(sk_flag, 16);
+          if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 3);  // published
+          continue;
+        }
+        if (RESID && lane == 0) {  // residual chunks of this unit only, from chunk 0
+          bulk_wait_read0();
+          pf_u = unit;
+          pf_c = 0;
+          for (int i = 0; i < NBUF - 1; ++i) resid_load(g + i);
+        }
+        if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 4);  // combining: before the wait
+        if (lane == 0 && old < 16)
+          while (*reinterpret_cast<volatile int*>(sk_flag) < 16) __nanosleep(32);
+        __syncwarp();
+        __threadfence();
+        if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 5);  // partial visible
+        sk_part = part + quarter * 256 + lane;
+      }
       [[maybe_unused]] float ln_sum = 0.f;
       const float2 *rt = nullptr, *ct = nullptr;
       if (EPI == EPI_QKV_ROPE) {
@@ -565,7 +627,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         __syncwarp();
         float v[32];
         tmem_ld32(taddr + c, v);
-        tmem_ld_wait();
+        if constexpr (SPLITK) {  // + the other K half's partial (commutative: same bits either way)
+          float4 pp[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pp[q] = __ldcg(sk_part + (c >> 5) * 4 * 256 + q * 32);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            v[4 * q] += pp[q].x;
+            v[4 * q + 1] += pp[q].y;
+            v[4 * q + 2] += pp[q].z;
+            v[4 * q + 3] += pp[q].w;
+          }
+        } else {
+          tmem_ld_wait();
+        }
         if ((PREC && epi.acc_f16)) {  // f16 accumulator: one value per 32-bit TMEM cell, low half
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -583,7 +659,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
-        if (kh == 0) epilogue_bias_act<EPI>(v, n0 + c, bias);  // split-K: bias once (half 0)
+        epilogue_bias_act<EPI>(v, n0 + c, bias);
         if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) rope_chunk(v, n0 + c, rope_hd, rt, ct);
         if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
 #pragma unroll
@@ -659,15 +735,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
-      if (SK > 1 && kh == 0) {  // half 0 of a split-K tile: publish once this warp's stores landed
-        if (lane == 0) {
-          bulk_wait_all();
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __threadfence();
-          atomicAdd(epi.tile_flags + tile, 1);
-        }
-        __syncwarp();
+      if constexpr (SPLITK) {
+        if (lane == 0) *sk_flag = 0;  // both halves done with this flag: ready for the next launch
       }
+      if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 6);  // unit's epilogue done
     }
     if (lane == 0) bulk_wait_all();  // output writes landed before the CTA retires
     if (warp == 4 && lane == 0) GEMM_STAMP(5);
@@ -989,7 +1060,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, CG, PREC, SPLITK>;
   static std::atomic<uint64_t> smem_set{0};
   if (const cudaError_t e = set_smem_once(smem_set, kern, L::TOTAL); e != cudaSuccess) return (int)e;
-  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (EPI == EPI_F32_RESID && SPLITK ? epi.splitk : 1);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN) * (SPLITK ? 2 : 1);
   const int units = num_sms / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   cudaLaunchConfig_t cfg = {};
@@ -1031,8 +1102,11 @@ int launch_planned(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorM
   constexpr int ST = stages_for<BN, EPI, CG>();
   if (epi.acc_f16 || epi.round_f16)
     return launch_gemm<BN, ST, EPI, CG, true, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
-  if constexpr (EPI == EPI_F32_RESID)
+  if constexpr (EPI != EPI_F32_RESID_LN && (BN == 256 || BN == 128)) {
     if (epi.splitk > 1) return launch_gemm<BN, ST, EPI, CG, false, true>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+  } else if (epi.splitk > 1) {
+    return (int)cudaErrorInvalidValue;
+  }
   return launch_gemm<BN, ST, EPI, CG, false, false>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
 }
 
@@ -1103,14 +1177,15 @@ int gemm_bn_for(int N) {
 // 2-SM 256 x BN tiles on SM pairs.  cost = waves * BN / eff(BN): narrow tiles pay for operand
 // re-reads (measured MMA efficiency relative to BN = 256 on B200: 0.66 at 128, 0.45 at 64);
 // the CTA-pair form wins ties (lower operand traffic per FLOP).
-GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms) {
+GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms, int splitk) {
   if (epi_mode == EPI_F32_RESID_LN) return GemmPlan{N == 256 ? 256 : 0, 2};  // whole rows per tile
   GemmPlan best{0, 1};
   double best_cost = 0;
   for (int cg = 2; cg >= 1; --cg) {
     for (int bn : {256, 192, 160, 128, 64}) {
       if (N % bn || (cg == 1 && (bn == 192 || bn == 160))) continue;
-      const long long tiles = (long long)((M + BM * cg - 1) / (BM * cg)) * (N / bn);
+      if (splitk > 1 && bn != 256 && bn != 128) continue;  // the split-K instantiations
+      const long long tiles = (long long)((M + BM * cg - 1) / (BM * cg)) * (N / bn) * splitk;
       const long long units = num_sms / cg;
       const long long waves = (tiles + units - 1) / units;
       const double eff = bn == 256 ? 1.0 : bn == 192 ? g_eff192 : bn == 160 ? g_eff160 : bn == 128 ? 0.66 : 0.45;
@@ -1139,7 +1214,8 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2
   if (M <= 0) return 0;
   const int BN = plan.bn;
   if (K % BK != 0 || N % BN != 0) return (int)cudaErrorInvalidValue;
-  if (epi.splitk != 1 && (epi_mode != EPI_F32_RESID || epi.splitk != 2 || (K / BK) % 2 != 0 || !epi.tile_flags))
+  if (epi.splitk != 1 && (epi.splitk != 2 || epi_mode == EPI_F32_RESID_LN || (K / BK) % 2 != 0 || !epi.tile_flags ||
+                          !epi.ws || epi.acc_f16 || epi.round_f16 || (BN != 256 && BN != 128)))
     return (int)cudaErrorInvalidValue;
   if (epi_mode == EPI_QKV_ROPE && (epi.rope_grid <= 0 || epi.rope_grid > ROPE_MAX_GRID ||
                                    epi.rope_grid * epi.rope_grid != epi.rope_T || epi.rope_hd % 4 != 0 ||

@@ -38,12 +38,18 @@ struct GemmEpi {
   int wm_win = 0;
   int wm_scatter = 0;
   int dbg_noload = 0;  // microbenchmarks only: after the first ring fill, stages are re-used without TMA
-  // Split-K residual GEMM (EPI_F32_RESID only): splitk = 2 runs each output tile as two K halves
-  // on different CTA pairs; half 0 does out += bias + acc0, half 1 waits for half 0's tile flag
-  // (tile_flags[tile] == 16: all epilogue warps of the pair have stored) and does out += acc1.
-  // Deterministic order, no workspace; tile_flags must be zeroed before the launch.
+  // Split-K (every epilogue but EPI_F32_RESID_LN): splitk = 2 runs each output tile as two K
+  // halves on neighbouring CTA pairs (units 2t, 2t+1).  Per epilogue warp, the half that reaches
+  // its epilogue first
+  // (atomic claim on tile_flags) writes its fp32 partial accumulator to `ws`; the second adds
+  // it to its own (fp32 addition commutes: the sum is the same bits whichever half finished
+  // first) and runs the normal epilogue.  Nothing waits on a unit that has not claimed, so the
+  // protocol cannot deadlock when the grid is only partly resident.  tile_flags:
+  // splitk_flag_count(tiles, cg) ints, zero before the first launch (the combining warp resets
+  // its flag); ws: splitk_ws_floats(tiles, bn, cg) floats.
   int splitk = 1;
   int* tile_flags = nullptr;
+  float* ws = nullptr;
   // Tail halves: the first tail_full tiles (a whole number of waves) run as BN-wide units, the
   // remaining tiles as two BN/2-wide units each, so the last wave is half as long (0 = off).
   int tail_full = 0;
@@ -75,7 +81,10 @@ int gemm_bn_for(int N);
 struct GemmPlan {
   int bn, cg;
 };
-GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms);
+GemmPlan gemm_plan(int M, int N, int epi_mode, int num_sms, int splitk = 1);
+// split-K workspace sizes for `tiles` output tiles of a plan (see GemmEpi::splitk)
+inline long long splitk_flag_count(long long tiles, int cg) { return tiles * cg * 8; }
+inline long long splitk_ws_floats(long long tiles, int bn, int cg) { return tiles * cg * 128LL * bn; }
 void gemm_force_plan(int bn, int cg);
 int gemm_set_trace(long long* device_buf);  // bn 0: automatic
 // tA: map over A [M, K] with box {64, 128}; tB: map over W [N, K] with box {64, plan.bn / plan.cg}.

@@ -82,32 +82,77 @@ def test_gemm_epilogues(lib, epi):
 PLANS = [(256, 1), (128, 1), (64, 1), (256, 2), (192, 2), (160, 2), (128, 2), (64, 2)]
 
 
-@pytest.mark.parametrize("bn,cg", [(256, 2), (128, 2), (256, 1), (64, 1)])
-@pytest.mark.parametrize("M,N,K", [(5184, 1280, 5120), (1333, 768, 640), (300, 256, 128)])
+@pytest.mark.parametrize("bn,cg", [(256, 2), (128, 2), (256, 1), (128, 1)])
+@pytest.mark.parametrize("M,N,K", [(5184, 1280, 5120), (5184, 1280, 1280), (1333, 768, 640), (300, 256, 128)])
 def test_gemm_split_k_residual(lib, bn, cg, M, N, K):
-    """Split-K residual epilogue: out += bias + A W^T as two K halves (half 0 adds bias + acc0,
-    half 1 waits for half 0's tile flag and adds acc1); equal to fp32 torch and deterministic."""
+    """Split-K residual epilogue: every tile as two K halves; the half that reaches its epilogue
+    second adds the first's partial accumulator and does out += bias + acc.  Equal to fp32 torch,
+    deterministic, and bitwise independent of M (rows computed inside a larger launch -- other
+    tiles, other claim orders -- are the same bits)."""
     g = torch.Generator(device="cuda").manual_seed(M + N + K + bn)
-    A = torch.randn(M, K, device="cuda", generator=g).half()
+    A = torch.randn(2 * M, K, device="cuda", generator=g).half()
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
     bias = torch.randn(N, device="cuda", generator=g)
-    x0 = torch.randn(M, N, device="cuda", generator=g)
-    ref = x0 + A.float() @ W.float().T + bias
+    x0 = torch.randn(2 * M, N, device="cuda", generator=g)
+    ref = x0[:M] + A[:M].float() @ W.float().T + bias
     outs = []
     lib.dart_gemm_force_plan(bn, cg)
     lib.dart_gemm_force_splitk(2)
     try:
-        for _ in range(2):
-            out = x0.clone()
-            _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N, K,
+        for rows in (M, M, 2 * M):
+            out = x0[:rows].clone()
+            _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, rows, N, K,
                                         3, None, None, 0, 0, 0, stream()))
-            outs.append(out)
+            outs.append(out[:M])
         torch.cuda.synchronize()
     finally:
         lib.dart_gemm_force_splitk(1)
         lib.dart_gemm_force_plan(0, 0)
-    assert rel_err(outs[0], ref) < 2e-3
+    assert rel_err(outs[0], ref) < 2e-5
     assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2, 4, 5])
+def test_gemm_split_k_epilogues(lib, epi):
+    """Split-K through every other epilogue (bias / ReLU / RoPE after the two halves combine), on the
+    backbone's QKV shape (315 CTA-pair tiles) and a ragged one; rows bitwise independent of M."""
+    T, E = 5184, 1280
+    M, N, K = (5184, 3840, 1280) if epi == 4 else (1700, 768, 640)
+    g = torch.Generator(device="cuda").manual_seed(epi + 11)
+    A = torch.randn(M + 700, K, device="cuda", generator=g).half()
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).half()
+    bias = torch.randn(N, device="cuda", generator=g)
+    ref = A[:M].float() @ W.float().T + bias
+    f16 = epi in (0, 1, 4)
+    rope = None
+    if epi == 4:
+        hd, H = 80, 16
+        cos, sin = rope_tables(72, hd)
+        rope = (cos, sin, T, hd, 2 * E)
+        y = ref.reshape(M, 3, H, hd)
+        tok = torch.arange(M, device="cuda") % T
+        c, s = cos[tok][:, None, None, :], sin[tok][:, None, None, :]
+        rot = y.clone()
+        rot[:, :2, :, 0::2] = (y[..., 0::2] * c - y[..., 1::2] * s)[:, :2]
+        rot[:, :2, :, 1::2] = (y[..., 0::2] * s + y[..., 1::2] * c)[:, :2]
+        ref = rot.reshape(M, N)
+    elif epi == 1:
+        ref = ref.clamp_min(0)
+    outs = []
+    lib.dart_gemm_force_splitk(2)
+    try:
+        for rows in (M, M + 700):
+            out = torch.empty(rows, N, device="cuda", dtype=torch.float16 if f16 else torch.float32)
+            out2 = torch.empty(rows, N, device="cuda", dtype=torch.float16) if epi == 5 else None
+            run_gemm(lib, A[:rows], W, bias, epi, out, out2, rope=rope)
+            outs.append((out[:M], out2[:M] if out2 is not None else None))
+    finally:
+        lib.dart_gemm_force_splitk(1)
+    assert rel_err(outs[0][0], ref) < (2e-3 if f16 else 2e-5)
+    assert torch.equal(outs[0][0], outs[1][0])
+    if epi == 5:
+        assert rel_err(outs[0][1], ref) < 2e-3 and torch.equal(outs[0][1], outs[1][1])
 
 
 @pytest.mark.parametrize("bn,cg", PLANS)
