@@ -316,6 +316,12 @@ __device__ __forceinline__ void ln_rows_epilogue(uint32_t taddr, int quarter, in
 }
 
 constexpr int GEMM_THREADS = 384;
+// fp32 residual epilogue through a TMA reduce-add (see RED in gemm_tc_kernel); -DDART_RESID_REDUCE=0
+// builds the load-add-store epilogue instead (A/B)
+#ifndef DART_RESID_REDUCE
+#define DART_RESID_REDUCE 1
+#endif
+constexpr bool RESID_REDUCE = DART_RESID_REDUCE != 0;
 
 // PREC: the precision-study variant (GemmEpi::acc_f16 / round_f16 honoured); the detection
 // path's instantiations (PREC = false) carry none of that code.  SPLITK: two K halves per tile
@@ -349,7 +355,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // tmC: fp32 [M, N] output / residual map (box 32x32, 128B swizzle); tmD: fp16 [M, N] output map
   // (box 32x32, 64B swizzle).  Outputs leave through per-warp smem chunks and TMA bulk stores.
   using L = GemmSmem<BN, STAGES, EPI, CG>;
-  constexpr bool RESID = L::RESID;
+  // RED: the fp32 residual add x += acc + bias as a TMA reduce-add (cp.reduce.async.bulk.tensor
+  // .add) -- the epilogue never loads x, the L2 adds on the way in.  Not for the fused-LN epilogue
+  // (it needs the new row values) nor the fp16-storage study variant (it rounds the sum).
+  constexpr bool RED = EPI == EPI_F32_RESID && !PREC && RESID_REDUCE;
+  constexpr bool RESID = L::RESID && !RED;  // epilogues that load the residual chunk
   static_assert(BN % 32 == 0, "32-column epilogue chunks");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (TF > 0) tma_prefetch_desc(&tmB2);
-    if (RESID || EPI == EPI_F32) tma_prefetch_desc(&tmC);
+    if (RESID || RED || EPI == EPI_F32) tma_prefetch_desc(&tmC);
     if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE || EPI == EPI_F32_RESID_LN) tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -671,7 +681,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             chunk_store_f16(buf, v, reinterpret_cast<act_t*>(epi.out2), epi.ldo2, row0, n0 + c, M, epi);
           continue;
         }
-        if constexpr (RESID) {
+        if constexpr (RED) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *slot32(buf, lane, q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else if constexpr (RESID) {
           mbar_wait(&rbar[g % NBUF], (g / NBUF) & 1);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -714,7 +728,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy) store
         __syncwarp();
         if (lane == 0) {
-          if (RESID || EPI == EPI_F32 || EPI == EPI_F32_F16)
+          if (RED)
+            tma_reduce_add_2d(&tmC, buf, n0 + c, row0);
+          else if (RESID || EPI == EPI_F32 || EPI == EPI_F32_F16)
             tma_store_2d(&tmC, buf, n0 + c, row0);
           else
             tma_store_2d(&tmD, buf, n0 + c, row0);
