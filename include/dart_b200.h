@@ -248,6 +248,13 @@ void dart_attention_variant(int32_t v);
  * turns it off). */
 void dart_set_pdl(int32_t mode);
 
+/* Backbone LayerNorms folded into the consuming GEMMs in dart_backbone (the residual producers
+ * also write fp16(x) and per-row chunk statistics).  Mask: bit 0 LN1 -> QKV, bit 1 LN2 -> fc1;
+ * 0 = the standalone LayerNorm passes (the default: measured faster on the B200; DART_LN_FOLD
+ * sets the process default).  Folded weights are built by handles created while the mask is
+ * non-zero.  Process wide; tests and A/B measurement. */
+void dart_set_ln_fold(int32_t mask);
+
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */
 int64_t dart_launch_count(const dart_model* m);

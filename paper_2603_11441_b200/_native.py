@@ -58,6 +58,7 @@ EXPORTS = (
     "dart_mlp_fused_ln",
     "dart_gemm_force_splitk",
     "dart_set_pdl",
+    "dart_set_ln_fold",
     "dart_gemm_force_precision",
     "dart_attention_force_safe",
     "dart_attention_trace",
@@ -208,6 +209,8 @@ def load() -> ctypes.CDLL:
     lib.dart_gemm_force_splitk.restype = None
     lib.dart_set_pdl.argtypes = [I32]
     lib.dart_set_pdl.restype = None
+    lib.dart_set_ln_fold.argtypes = [I32]
+    lib.dart_set_ln_fold.restype = None
     lib.dart_gemm_force_precision.argtypes = [I32]
     lib.dart_gemm_force_precision.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,

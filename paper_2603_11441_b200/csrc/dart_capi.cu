@@ -108,6 +108,13 @@ int g_attn_force_safe = 0;
 // 128 KB fp32 partial at ~26 GB/s, ~5 us, as long as the attn.out half-tile main loop).
 // DART_SPLITK=<mask> enables it for A/B measurement.
 int g_splitk_mask = getenv("DART_SPLITK") ? atoi(getenv("DART_SPLITK")) : 0;
+// Backbone LayerNorms folded into the GEMMs that consume them (see bb_blocks).  Mask: bit 0
+// LN1 -> QKV (producers: patch embed, mlp.fc2), bit 1 LN2 -> fc1 (producer: attn.out).  Off by
+// default: parity-equivalent but slower on the B200 (profiles/r02/ln_fold_ab.log) -- the residual
+// GEMM's epilogue, which bounds attn.out and the last fc2 wave, grows by the fp16 copy and the
+// statistics more than the LayerNorm pass it replaces costs.  The folded weights exist only in
+// handles created while the fold is enabled (DART_LN_FOLD=<mask> or dart_set_ln_fold).
+int g_ln_fold = getenv("DART_LN_FOLD") ? atoi(getenv("DART_LN_FOLD")) : 0;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
@@ -159,6 +166,7 @@ int attn_tc_packed(const __half* qkv, __half* o, int items, int heads, int L, in
 struct GemmW {
   __half* w = nullptr;  // [N, K] fp16
   float* b = nullptr;   // [N]
+  float* colsum = nullptr;  // LN-folded weights only: [N] column sums of the fp16 W' (GemmEpi::ln_colsum)
   int N = 0, K = 0;
   CUtensorMap tmap[6];  // box rows 256 / 128 / 64 / 32 / 96 / 80 (index = box_slot(rows)), built where N allows
 };
@@ -177,6 +185,7 @@ struct AttnW {
 struct BlockW {
   LNW ln1, ln2;
   GemmW qkv, out, fc1, fc2;
+  GemmW qkv_f, fc1_f;  // qkv / fc1 with LN1 / LN2 folded in (W' = diag(gamma) W, b' = b + beta W)
 };
 struct XLayerW {
   LNW ln1, ln2, ln3;
@@ -258,6 +267,9 @@ struct dart_model {
   struct {
     __half *patches, *h, *qkv, *ao, *hid, *pool1, *pool2, *l0h;
     float* x;
+    float2* lnst;  // LN fold: per-row chunk statistics of x [rows, E / 32] (h holds fp16(x))
+    float2* lnfin;  // LN fold: per-row (mean, rstd) of x [rows]
+    int* lncnt;     // LN fold: chunk counters per 32-row group [rows / 32] (zeroed at allocation)
   } bb{};
   struct {
     float *e1, *e, *qd, *qd0, *qf;
@@ -268,6 +280,7 @@ struct dart_model {
   // 1 fp16 storage (outputs and residual rounded to fp16), 2 fp16 storage + fp16 accumulation
   int precision = 0;
   bool in_backbone = false;  // set while a backbone stage issues its GEMMs
+  bool x16_valid = false;    // LN fold: bb.h holds fp16 of the backbone residual stream (last producer)
   // split-K claim flags and partial accumulators, per handle (a fork gets its own)
   int* splitk_flags = nullptr;
   long long splitk_cap = 0;  // flags
@@ -306,6 +319,39 @@ bool upload_wT(dart_model* m, const float* h, int in, int out, __half* dst, int 
   dim3 grid((out + 31) / 32, (kpad + 31) / 32);
   transpose_cast_kernel<<<grid, dim3(32, 8)>>>(scratch, dst + (size_t)row0 * kpad, in, out, kpad);
   return cudaGetLastError() == cudaSuccess;
+}
+
+// LayerNorm folded into the following linear (GemmEpi::ln_stats): from the host-layout fp32
+// [in, out] weight in `src`: wT[n, k] = fp16(gamma[k] W[k, n]), bias'[n] = b[n] + sum_k beta[k] W[k, n],
+// colsum[n] = sum_k float(wT[n, k]) -- the column sums of exactly the fp16 values the MMA reads.
+__global__ void ln_fold_kernel(const float* __restrict__ src, const float* __restrict__ g, const float* __restrict__ beta,
+                               const float* __restrict__ bias, int in, int out, __half* __restrict__ wT,
+                               float* __restrict__ bias_f, float* __restrict__ colsum) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= out) return;
+  float bacc = bias[n], cs = 0.f;
+  for (int k = 0; k < in; ++k) {
+    const float wv = src[(long long)k * out + n];
+    const __half h = __float2half_rn(g[k] * wv);
+    wT[(long long)n * in + k] = h;
+    cs += __half2float(h);
+    bacc = fmaf(beta[k], wv, bacc);
+  }
+  bias_f[n] = bacc;
+  colsum[n] = cs;
+}
+
+bool finish_gemmw(GemmW& g);
+// Folded twin of `g` (whose host fp32 [in, out] weight is still in `scratch`, see upload_wT).
+bool make_folded(dart_model* m, const GemmW& g, const LNW& ln, const float* scratch, GemmW& f) {
+  f.N = g.N;
+  f.K = g.K;
+  f.w = dev_alloc<__half>(m, (size_t)f.N * f.K);
+  f.b = dev_alloc<float>(m, f.N);
+  f.colsum = dev_alloc<float>(m, f.N);
+  if (!f.w || !f.b || !f.colsum) return false;
+  ln_fold_kernel<<<(f.N + 127) / 128, 128>>>(scratch, ln.g, ln.b, g.b, g.K, g.N, f.w, f.b, f.colsum);
+  return cudaGetLastError() == cudaSuccess && finish_gemmw(f);
 }
 
 bool finish_gemmw(GemmW& g) {
@@ -405,6 +451,9 @@ int check_desc(const dart_model_desc* d) {
 // Output tensor maps of a GEMM epilogue (see gemm_tc): fp32 box 32x32 SW128, fp16 box 32x32 SW64.
 bool make_out_maps(int epi, const GemmEpi& e, int M, int N, CUtensorMap* tc, CUtensorMap* td) {
   if (epi == EPI_F32_RESID_LN)  // residual stream in/out + the fp16 LayerNorm rows
+    return make_tmap_f32(tc, e.out, N, M, e.ldo) &&
+           make_tmap_ex(td, e.out2, N, M, e.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (epi == EPI_F32_RESID_X16)  // residual stream in/out + its fp16 copy
     return make_tmap_f32(tc, e.out, N, M, e.ldo) &&
            make_tmap_ex(td, e.out2, N, M, e.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (epi == EPI_F32_RESID || (epi == EPI_F32 && !e.wm_scatter))
@@ -520,8 +569,13 @@ int ensure_backbone_ws(dart_model* m, int B) {
   m->bb.pool1 = (__half*)w.get(rows / 4 * E * 2);
   m->bb.pool2 = (__half*)w.get(rows / 16 * E * 2);
   m->bb.l0h = (__half*)w.get(rows * m->F0 * 2);
+  m->bb.lnst = (float2*)w.get(rows * (E / 32) * sizeof(float2));
+  m->bb.lnfin = (float2*)w.get(rows * sizeof(float2));
+  m->bb.lncnt = (int*)w.get((rows / 32 + 1) * sizeof(int));
   if (!m->bb.patches || !m->bb.x || !m->bb.h || !m->bb.qkv || !m->bb.ao || !m->bb.hid || !m->bb.pool1 ||
-      !m->bb.pool2 || !m->bb.l0h) {
+      !m->bb.pool2 || !m->bb.l0h || !m->bb.lnst || !m->bb.lnfin || !m->bb.lncnt ||
+      cudaMemset(m->bb.lncnt, 0, (rows / 32 + 1) * sizeof(int)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {  // counters zero before any stream uses them
     m->bb_ws.release();
     m->bb_cap = 0;
     return fail(DART_ERR_CUDA, "backbone workspace allocation failed");
@@ -770,9 +824,11 @@ int dart_model_create(const dart_model_desc* desc, const float* const* weights, 
   m->blocks.resize(desc->num_blocks);
   for (int b = 0; ok && b < desc->num_blocks; ++b) {
     BlockW& B = m->blocks[b];
+    const bool fold = g_ln_fold != 0;  // folded twins only when the fold is enabled at creation
     ok = make_ln(m, c, E, B.ln1) && make_gemm(m, c, E, 3 * E, scratch, B.qkv) &&
-         make_gemm(m, c, E, E, scratch, B.out) && make_ln(m, c, E, B.ln2) &&
-         make_gemm(m, c, E, 4 * E, scratch, B.fc1) && make_gemm(m, c, 4 * E, E, scratch, B.fc2);
+         (!fold || make_folded(m, B.qkv, B.ln1, scratch, B.qkv_f)) && make_gemm(m, c, E, E, scratch, B.out) &&
+         make_ln(m, c, E, B.ln2) && make_gemm(m, c, E, 4 * E, scratch, B.fc1) &&
+         (!fold || make_folded(m, B.fc1, B.ln2, scratch, B.fc1_f)) && make_gemm(m, c, 4 * E, E, scratch, B.fc2);
   }
   for (int l = 0; ok && l < 3; ++l) ok = make_gemm(m, c, E, desc->fpn_dims[l], scratch, m->fpn[l]);
   if (ok) {
@@ -878,27 +934,69 @@ struct BackboneScope {
 // Backbone stages on a caller-chosen residual stream x [B*T, E] fp32 in window-major row order
 // (each 24x24 window a contiguous block; global attention, LN and the MLP are order-invariant,
 // the patchify / RoPE / FPN kernels map rows to tokens).
-int bb_embed(dart_model* m, const float* images, int B, float* x, int32_t* flags, cudaStream_t s) {
+// Backbone LayerNorms folded into the GEMMs that consume them (GemmEpi::ln_stats; LN1 -> QKV,
+// LN2 -> fc1): the producers of the residual stream x (patch embed, attn.out, mlp.fc2) also write
+// fp16(x) and per-row chunk statistics, so no LayerNorm pass runs.  Only the whole-backbone entry
+// point (dart_backbone) in the detection discipline folds (g_ln_fold); the staged entry points
+// (pruning) and the precision-study disciplines always run the LayerNorm kernels.
+int ln_fold_on(const dart_model* m) {
+  const bool ok = m->precision == 0 && m->E % 32 == 0 && !m->blocks.empty() && m->blocks[0].qkv_f.w != nullptr;
+  return ok ? g_ln_fold & 3 : 0;
+}
+
+int bb_embed(dart_model* m, const float* images, int B, float* x, int32_t* flags, cudaStream_t s, int fold = 0) {
   BackboneScope scope(m);
   auto& w = m->bb;
   const int rows = B * m->T, win = m->d.window_size;
   if (cudaMemsetAsync(flags, 0, sizeof(int32_t), s) != cudaSuccess) return fail(DART_ERR_CUDA, "flags memset");
   LAUNCH(patchify(images, w.patches, B, m->d.image_size, m->d.patch_size, m->kpad, win, flags, s));
+  m->x16_valid = (fold & 1) != 0;
+  if (fold & 1) {  // x, fp16(x) and its LN chunk statistics (block 0's LN1 is folded)
+    GemmEpi e = epi_out(x, m->E);
+    e.out2 = w.h;
+    e.ldo2 = m->E;
+    e.ln_stats_out = w.lnst;
+    e.ln_cnt = w.lncnt;
+    e.ln_final = w.lnfin;
+    e.ln_parts = m->E / 32;
+    return gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32_F16, e, s);
+  }
   return gemm(m, w.patches, rows, m->kpad, m->patch, EPI_F32, epi_out(x, m->E), s);
 }
 
+// fold (mask, see g_ln_fold): with bit 0, fp16(x) in w.h and its statistics are current on entry
+// (bb_embed with the same mask)
 int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* attn_on, const int32_t* mlp_on,
-              cudaStream_t s) {
+              cudaStream_t s, int fold = 0) {
   BackboneScope scope(m);
   const int T = m->T, E = m->E, H = m->H, hd = m->hd, G = m->G;
   const int rows = B * T;
   auto& w = m->bb;
   const int win = m->d.window_size, nwin = (G / win) * (G / win);
+  // the producer epilogue of x (fold: + fp16(x) into w.h and the LN statistics)
+  // the next LN's fold bit decides what the producer writes: attn.out feeds LN2 (bit 1), fc2 LN1
+  auto resid = [&](const __half* A, int K, const GemmW& W, int next_bit) {
+    GemmEpi e = epi_out(x, E);
+    m->x16_valid = (fold & next_bit) != 0;
+    if (!(fold & next_bit)) return gemm(m, A, rows, K, W, EPI_F32_RESID, e, s);
+    e.out2 = w.h;
+    e.ldo2 = E;
+    e.ln_stats_out = w.lnst;
+    e.ln_cnt = w.lncnt;
+    e.ln_final = w.lnfin;
+    e.ln_parts = E / 32;
+    return gemm(m, A, rows, K, W, EPI_F32_RESID_X16, e, s);
+  };
+  auto folded_in = [&](GemmEpi& e, const GemmW& Wf) {  // consumer of LN(x): (mean, rstd) + column sums
+    e.ln_stats = w.lnfin;
+    e.ln_colsum = Wf.colsum;
+  };
   for (int b = b0; b < b1; ++b) {
     const BlockW& bw = m->blocks[b];
     if (attn_on ? attn_on[b] : m->d.attn_enabled[b]) {
-      LAUNCH(layernorm_f32_to_f16(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
+      if (!(fold & 1)) LAUNCH(layernorm_f32_to_f16(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
       GemmEpi e = epi_out(w.qkv, 3 * E);
+      if (fold & 1) folded_in(e, bw.qkv_f);
       e.rope_cos = m->rope_cos;
       e.rope_sin = m->rope_sin;
       e.rope_T = T;
@@ -907,7 +1005,7 @@ int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* att
       e.rope_cols = 2 * E;  // q and k
       e.wm_grid = G;
       e.wm_win = win;
-      RUN(gemm(m, w.h, rows, E, bw.qkv, EPI_QKV_ROPE, e, s));
+      RUN(gemm(m, w.h, rows, E, (fold & 1) ? bw.qkv_f : bw.qkv, EPI_QKV_ROPE, e, s));
       AttnArgs a = attn_base(H, hd);
       a.q = w.qkv;
       a.k = w.qkv + E;
@@ -932,23 +1030,29 @@ int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* att
       } else {
         RUN(attn(m, a, hd, s));
       }
-      RUN(gemm(m, w.ao, rows, E, bw.out, EPI_F32_RESID, epi_out(x, E), s));
+      RUN(resid(w.ao, E, bw.out, 2));
     }
     if (mlp_on ? mlp_on[b] : m->d.mlp_enabled[b]) {
-      LAUNCH(layernorm_f32_to_f16(x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
-      RUN(gemm(m, w.h, rows, E, bw.fc1, EPI_F16_RELU, epi_out(w.hid, 4 * E), s));
-      RUN(gemm(m, w.hid, rows, 4 * E, bw.fc2, EPI_F32_RESID, epi_out(x, E), s));
+      GemmEpi e = epi_out(w.hid, 4 * E);
+      if (fold & 2)
+        folded_in(e, bw.fc1_f);
+      else
+        LAUNCH(layernorm_f32_to_f16(x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
+      RUN(gemm(m, w.h, rows, E, (fold & 2) ? bw.fc1_f : bw.fc1, EPI_F16_RELU, e, s));
+      RUN(resid(w.hid, 4 * E, bw.fc2, 1));
     }
   }
   return DART_OK;
 }
 
 // FPN (model.py:446-451): L0 from tokens, L1 / L2 from 2x2 / 4x4 mean-pooled tokens
-int bb_fpn(dart_model* m, const float* x, int B, float* l0, float* l1, float* l2, int32_t* flags, cudaStream_t s) {
+// fold: w.h already holds fp16(x) (the last producer's copy), so the cast is skipped
+int bb_fpn(dart_model* m, const float* x, int B, float* l0, float* l1, float* l2, int32_t* flags, cudaStream_t s,
+           int fold = 0) {
   BackboneScope scope(m);
   auto& w = m->bb;
   const int rows = B * m->T, E = m->E, G = m->G, win = m->d.window_size;
-  LAUNCH(cast_f32_to_f16(x, w.h, (long long)rows * E, s));
+  if (!fold) LAUNCH(cast_f32_to_f16(x, w.h, (long long)rows * E, s));
   GemmEpi e0 = epi_out(l0, m->F0);  // rows scattered back to token-major order
   e0.out2 = w.l0h;
   e0.ldo2 = m->F0;
@@ -976,9 +1080,10 @@ int dart_backbone(dart_model* m, const float* images, int32_t B, float* l0, floa
   if (!m || !images || B <= 0 || !l0 || !l1 || !l2 || !flags) return fail(DART_ERR_INVALID, "dart_backbone: bad args");
   cudaStream_t s = (cudaStream_t)stream;
   RUN(ensure_backbone_ws(m, B));
-  RUN(bb_embed(m, images, B, m->bb.x, flags, s));
-  RUN(bb_blocks(m, m->bb.x, B, 0, m->d.num_blocks, nullptr, nullptr, s));
-  return bb_fpn(m, m->bb.x, B, l0, l1, l2, flags, s);
+  const int fold = ln_fold_on(m);
+  RUN(bb_embed(m, images, B, m->bb.x, flags, s, fold));
+  RUN(bb_blocks(m, m->bb.x, B, 0, m->d.num_blocks, nullptr, nullptr, s, fold));
+  return bb_fpn(m, m->bb.x, B, l0, l1, l2, flags, s, m->x16_valid);  // last producer left fp16(x) in bb.h
 }
 
 int dart_backbone_embed(dart_model* m, const float* images, int32_t B, float* x, int32_t* flags, void* stream) {
@@ -1258,6 +1363,7 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
 }
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 void dart_set_pdl(int32_t mode) { pdl_set_thread(mode); }
+void dart_set_ln_fold(int32_t on) { g_ln_fold = on & 3; }
 void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
 int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,

@@ -37,8 +37,9 @@ struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr bool RESID = EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN;
+  static constexpr bool RESID = EPI == EPI_F32_RESID || EPI == EPI_F32_RESID_LN || EPI == EPI_F32_RESID_X16;
   static constexpr bool LNO = EPI == EPI_F32_RESID_LN;  // fused LayerNorm output of full rows
+  static constexpr bool X16 = EPI == EPI_F32_RESID_X16;  // + fp16 copy and LN chunk statistics
   // staging buffers per epilogue warp; 4 for the residual epilogue (3 chunks prefetched) measured
   // slower: the extra 64 KB costs two operand stages (out-proj 24.8 -> 27.1 us, fc2 63.4 -> 80 us)
   static constexpr int NBUF = 2;
@@ -47,7 +48,8 @@ struct GemmSmem {
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;  // 8 warps x NBUF staging buffers
   // fused LN: 2 fp16 32x32 staging chunks per epilogue warp + the row-statistics exchange
   static constexpr int LN_OFF = EPI_OFF + 8 * NBUF * BUF_BYTES;
-  static constexpr int LN_BYTES = LNO ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : 0;
+  // (X16: one fp16 32x32 staging chunk per epilogue warp for the fp16 copy of the new residual)
+  static constexpr int LN_BYTES = LNO ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : X16 ? 8 * 2048 : 0;
   static constexpr int ROPE_OFF = LN_OFF + LN_BYTES;  // [2][grid][ROPE_PAD] float2 (QKV epilogue only)
   static constexpr int ROPE_BYTES = EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0;
   static constexpr int BAR_OFF = ROPE_OFF + ROPE_BYTES;
@@ -315,6 +317,50 @@ __device__ __forceinline__ void ln_rows_epilogue(uint32_t taddr, int quarter, in
   }
 }
 
+// LayerNorm statistics of one 32-value chunk of a row (two-pass: mean, then the centred sum of
+// squares), the producer half of the LN fold (GemmEpi::ln_stats_out)
+__device__ __forceinline__ float2 chunk_ln_stats(const float* v) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) s += v[j];
+  const float mu = s * (1.0f / 32.0f);
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float d = v[j] - mu;
+    q = fmaf(d, d, q);
+  }
+  return make_float2(mu, q);
+}
+// Consumer half: the row's `parts` chunk statistics combined in order (Chan et al. pairwise
+// update, equal chunk sizes), -> (mean, 1/sqrt(var + eps)) with population variance (reference
+// tensors.py:215-227, eps 1e-6)
+__device__ __forceinline__ float2 ln_row_stats(const float2* st, int parts) {
+  // equal-size chunks: mean = mean of the chunk means; M2 = sum of the chunk M2 + 32 * the chunk
+  // means' sum of squared deviations, taken about the first chunk's mean (shifted, one pass, so
+  // every load is in flight at once; parts is even: E % 64 == 0, 16-byte loads, fixed order)
+  const float4* st4 = reinterpret_cast<const float4*>(st);
+  const float k0 = __ldcg(&st[0].x);
+  float sm = 0.f, sq = 0.f, sd = 0.f;
+  for (int i0 = 0; i0 < parts / 2; i0 += 10) {
+    float4 b[10];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) b[j] = i0 + j < parts / 2 ? __ldcg(st4 + i0 + j) : make_float4(k0, 0.f, k0, 0.f);
+#pragma unroll
+    for (int j = 0; j < 10; ++j) {
+      sm += b[j].x + b[j].z;
+      sq += b[j].y + b[j].w;
+      const float d0 = b[j].x - k0, d1 = b[j].z - k0;
+      sd = fmaf(d0, d0, fmaf(d1, d1, sd));
+    }
+  }
+  const float n = (float)parts;
+  const float mu = sm / n;
+  const float dm = mu - k0;
+  const float var = (sq + 32.f * fmaxf(sd - n * dm * dm, 0.f)) / (32.f * n);
+  return make_float2(mu, 1.0f / sqrtf(var + 1e-6f));
+}
+
 constexpr int GEMM_THREADS = 384;
 // fp32 residual epilogue through a TMA reduce-add (see RED in gemm_tc_kernel); -DDART_RESID_REDUCE=0
 // builds the load-add-store epilogue instead (A/B)
@@ -403,7 +449,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tmB);
     if (TF > 0) tma_prefetch_desc(&tmB2);
     if (RESID || RED || EPI == EPI_F32) tma_prefetch_desc(&tmC);
-    if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE || EPI == EPI_F32_RESID_LN) tma_prefetch_desc(&tmD);
+    if (EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE || EPI == EPI_F32_RESID_LN || EPI == EPI_F32_RESID_X16)
+      tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -518,6 +565,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const float* const bias = epi.bias;  // hoisted kernel parameters (see the producer)
+    [[maybe_unused]] const float2* const ln_stats = epi.ln_stats;
+    [[maybe_unused]] const float* const ln_colsum = epi.ln_colsum;
+    [[maybe_unused]] float2* const ln_stats_out = epi.ln_stats_out;
+    [[maybe_unused]] const int ln_parts = epi.ln_parts;
     const int rope_cols = epi.rope_cols, rope_hd = epi.rope_hd;
     constexpr int NBUF = L::NBUF;
     constexpr int BUF_F = L::BUF_BYTES / 4;  // staging buffer size in floats
@@ -555,6 +606,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = (tile / num_n) * BM * CG + rank * BM;
       const int n0 = (tile % num_n) * BN + (nh >= 0 ? nh * (BN / 2) : 0);
       const int row0 = m0 + quarter * 32;
+      // LN fold consumer: this row's (mean, rstd), finalised by the producer; loaded while the
+      // unit's main loop still runs
+      [[maybe_unused]] float2 lnrs = make_float2(0.f, 1.f);
+      if constexpr (EPI == EPI_QKV_ROPE || EPI == EPI_F16_RELU) {
+        if (ln_stats != nullptr && row0 + lane < M) lnrs = __ldcg(ln_stats + row0 + lane);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       if (it == 0 && warp == 4 && lane == 0) GEMM_STAMP(4);
       if (warp == 4 && lane == 0) GEMM_STAMP_U(it, 1);  // accumulator ready
@@ -669,11 +726,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+        if constexpr (EPI == EPI_QKV_ROPE || EPI == EPI_F16_RELU) {
+          if (ln_stats != nullptr) {  // LN fold: rstd * (x W' - mu * colsum(W'))
+            const float4* cs4 = reinterpret_cast<const float4*>(ln_colsum + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 cs = __ldg(cs4 + q);
+              v[4 * q] = fmaf(-lnrs.x, cs.x, v[4 * q]) * lnrs.y;
+              v[4 * q + 1] = fmaf(-lnrs.x, cs.y, v[4 * q + 1]) * lnrs.y;
+              v[4 * q + 2] = fmaf(-lnrs.x, cs.z, v[4 * q + 2]) * lnrs.y;
+              v[4 * q + 3] = fmaf(-lnrs.x, cs.w, v[4 * q + 3]) * lnrs.y;
+            }
+          }
+        }
         epilogue_bias_act<EPI>(v, n0 + c, bias);
         if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) rope_chunk(v, n0 + c, rope_hd, rt, ct);
         if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = (EPI == EPI_F32 || EPI == EPI_F32_F16) ? round_f16(v[j]) : sat_f16(v[j]);
+        }
+        if constexpr (EPI == EPI_F32_F16) {
+          if (ln_stats_out != nullptr && row < M)
+            __stcg(ln_stats_out + (size_t)row * ln_parts + ((n0 + c) >> 5), chunk_ln_stats(v));
         }
         if ((EPI == EPI_F32 && epi.wm_scatter) || EPI == EPI_F32_F16) {  // row scatter / 2 outputs: plain stores
           chunk_store_f32(buf, v, reinterpret_cast<float*>(epi.out), epi.ldo, row0, n0 + c, M, epi);
@@ -697,11 +771,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             x.w += v[4 * q + 3];
             if ((PREC && epi.round_f16)) x = make_float4(round_f16(x.x), round_f16(x.y), round_f16(x.z), round_f16(x.w));
             *sp = x;
-            if constexpr (L::LNO) {
+            if constexpr (L::LNO || L::X16) {
               v[4 * q] = x.x;
               v[4 * q + 1] = x.y;
               v[4 * q + 2] = x.z;
               v[4 * q + 3] = x.w;
+            }
+          }
+          if constexpr (L::X16) {  // fp16 copy of the new rows + their LN chunk statistics
+            if (row < M) __stcg(ln_stats_out + (size_t)row * ln_parts + ((n0 + c) >> 5), chunk_ln_stats(v));
+            float* hb = reinterpret_cast<float*>(smem + L::LN_OFF) + (warp - 4) * 512;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 u;
+              u.x = pack_half2(v[8 * q + 0], v[8 * q + 1]);
+              u.y = pack_half2(v[8 * q + 2], v[8 * q + 3]);
+              u.z = pack_half2(v[8 * q + 4], v[8 * q + 5]);
+              u.w = pack_half2(v[8 * q + 6], v[8 * q + 7]);
+              *slot16_sw64(hb, lane, q) = u;
             }
           }
           if constexpr (L::LNO) {  // the new residual row values stay in TMEM for the LN passes
@@ -728,12 +815,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA (async proxy) store
         __syncwarp();
         if (lane == 0) {
-          if (RED)
+          if (RED) {
             tma_reduce_add_2d(&tmC, buf, n0 + c, row0);
-          else if (RESID || EPI == EPI_F32 || EPI == EPI_F32_F16)
+          } else if (RESID || EPI == EPI_F32 || EPI == EPI_F32_F16) {
             tma_store_2d(&tmC, buf, n0 + c, row0);
-          else
+            if constexpr (L::X16)  // same bulk group: the next chunk's wait_read0 covers both buffers
+              tma_store_2d(&tmD, reinterpret_cast<float*>(smem + L::LN_OFF) + (warp - 4) * 512, n0 + c, row0);
+          } else {
             tma_store_2d(&tmD, buf, n0 + c, row0);
+          }
           tma_store_commit();
         }
       }
@@ -748,6 +838,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_arrive(&tempty[acc]);
           } else {
             mbar_arrive_leader(&tempty[acc]);
+          }
+        }
+      }
+      if constexpr (L::X16 || EPI == EPI_F32_F16) {
+        if (ln_stats_out != nullptr) {  // LN statistics: the warp completing a 32-row group finalises it
+          const int nch = (bn_eff - half * 32 + 63) / 64;  // chunks this warp wrote for its 32 rows
+          __threadfence();
+          __syncwarp();
+          int old = 0;
+          if (lane == 0) old = atomicAdd(epi.ln_cnt + (row0 >> 5), nch);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old + nch == ln_parts) {
+            __threadfence();
+            if (row < M) __stcg(epi.ln_final + row, ln_row_stats(ln_stats_out + (size_t)row * ln_parts, ln_parts));
+            if (lane == 0) epi.ln_cnt[row0 >> 5] = 0;
           }
         }
       }
@@ -1107,7 +1212,8 @@ constexpr int stages_for() {
   constexpr int stage = BM * BK * 2 + (BN / CG) * BK * 2;
   constexpr int fixed = 8 * 2 * ((EPI == EPI_F16 || EPI == EPI_F16_RELU || EPI == EPI_QKV_ROPE) ? 2048 : 4096) +
                         (EPI == EPI_QKV_ROPE ? 2 * ROPE_MAX_GRID * ROPE_PAD * 8 : 0) +
-                        (EPI == EPI_F32_RESID_LN ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : 0) + 512 + 1024;
+                        (EPI == EPI_F32_RESID_LN ? 8 * 2 * 2048 + 4 * 2 * 32 * 4 : 0) +
+                        (EPI == EPI_F32_RESID_X16 ? 8 * 2048 : 0) + 512 + 1024;
   constexpr int n = (227 * 1024 - fixed) / stage;
   return n > 8 ? 8 : n;
 }
@@ -1137,6 +1243,8 @@ int dispatch_epi(int epi_mode, const CUtensorMap& tA, const CUtensorMap& tB, con
     case EPI_F32_RESID: return launch_planned<BN, EPI_F32_RESID, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
     case EPI_QKV_ROPE: return launch_planned<BN, EPI_QKV_ROPE, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
     case EPI_F32_F16: return launch_planned<BN, EPI_F32_F16, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
+    case EPI_F32_RESID_X16:
+      return launch_planned<BN, EPI_F32_RESID_X16, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
     case EPI_F32_RESID_LN:
       if constexpr (BN == 256) return launch_planned<BN, EPI_F32_RESID_LN, CG>(tA, tB, tB2, tC, tD, M, N, K, epi, num_sms, stream);
       return (int)cudaErrorInvalidValue;
@@ -1237,9 +1345,16 @@ int gemm_tc(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap* tB2
                                    epi.rope_grid * epi.rope_grid != epi.rope_T || epi.rope_hd % 4 != 0 ||
                                    epi.rope_hd / 4 > ROPE_MAX_Q))
     return (int)cudaErrorInvalidValue;
-  const bool f32_out = epi_mode == EPI_F32_RESID || epi_mode == EPI_F32_RESID_LN || (epi_mode == EPI_F32 && !epi.wm_scatter);
+  const bool f32_out = epi_mode == EPI_F32_RESID || epi_mode == EPI_F32_RESID_LN || epi_mode == EPI_F32_RESID_X16 ||
+                       (epi_mode == EPI_F32 && !epi.wm_scatter);
   const bool f16_out = epi_mode == EPI_F16 || epi_mode == EPI_F16_RELU || epi_mode == EPI_QKV_ROPE ||
-                       epi_mode == EPI_F32_RESID_LN;
+                       epi_mode == EPI_F32_RESID_LN || epi_mode == EPI_F32_RESID_X16;
+  // LN fold: statistics per 32-column chunk, full chunks only; the fp16 copy rides on tD
+  if ((epi_mode == EPI_F32_RESID_X16 || epi.ln_stats_out) &&
+      (!epi.ln_stats_out || !epi.ln_cnt || !epi.ln_final || epi.ln_parts * 32 != N || epi.ln_parts % 2))
+    return (int)cudaErrorInvalidValue;
+  if (epi.ln_stats && (!epi.ln_colsum || (epi_mode != EPI_QKV_ROPE && epi_mode != EPI_F16_RELU)))
+    return (int)cudaErrorInvalidValue;
   if (epi_mode == EPI_F32_RESID_LN && (N != BN || BN != 256 || !epi.ln_g || !epi.ln_b)) return (int)cudaErrorInvalidValue;
   if ((f32_out && !tC) || (f16_out && !tD)) return (int)cudaErrorInvalidValue;
   const CUtensorMap& c = tC ? *tC : tA;

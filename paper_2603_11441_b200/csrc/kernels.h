@@ -17,6 +17,9 @@ enum EpiMode {
   // out32 += acc + bias, then out2_16 = LayerNorm(out32) * ln_g + ln_b over each full row
   // (N == BN: the enc-dec's d = 256 rows sit in one tile; fuses the NEXT sub-block's LN)
   EPI_F32_RESID_LN = 6,
+  // out32 += acc + bias, out2_16 = fp16(out32), and LayerNorm row statistics of out32 per 32-column
+  // chunk into ln_stats_out (see GemmEpi): the producer half of the LN fold (backbone blocks)
+  EPI_F32_RESID_X16 = 7,
 };
 
 struct GemmEpi {
@@ -63,6 +66,22 @@ struct GemmEpi {
   // receive the fp16 normalised rows)
   const float* ln_g = nullptr;
   const float* ln_b = nullptr;
+  // LayerNorm folded into the consuming GEMM (backbone LN1 -> QKV, LN2 -> fc1):
+  //   LN(x) W + b = rstd * (x W' - mu * colsum(W')) + (b + beta W),  W' = diag(gamma) W
+  // Producer (EPI_F32_RESID_X16, or EPI_F32_F16 with ln_stats_out set): writes fp16(x) as the
+  // consumer's A operand and, per row and 32-column chunk, the chunk's (mean, M2) as a float2 at
+  // ln_stats_out[row * ln_parts + col / 32] (two-pass within the chunk).  Each epilogue warp then
+  // adds its chunk count to ln_cnt[row / 32]; the warp that completes a 32-row group (count ==
+  // ln_parts) combines the rows' chunks in order (Chan et al.) into ln_final[row] = (mean, rstd)
+  // and resets the counter (zero before the first launch).  Consumer (EPI_QKV_ROPE /
+  // EPI_F16_RELU with ln_stats = ln_final): v = rstd * (acc - mu * ln_colsum[n]) before bias /
+  // RoPE / ReLU.
+  float2* ln_stats_out = nullptr;
+  int* ln_cnt = nullptr;
+  float2* ln_final = nullptr;
+  const float2* ln_stats = nullptr;
+  const float* ln_colsum = nullptr;
+  int ln_parts = 0;  // 32-column chunks per row (E / 32)
 };
 
 // window-major row index <-> token index within one image

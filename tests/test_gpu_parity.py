@@ -276,15 +276,35 @@ def test_batch_independence_and_chunking():
     assert D.run_shared(model, image, names, cfg) == ref
 
 
+@pytest.mark.parametrize("fold", [3, 1, 0])
 @pytest.mark.parametrize("name", ["B", "C"])
-def test_full_width_parity(name):
+def test_full_width_parity(name, fold):
     """Full-size kernels (hd 80, window 24, T 5184, d 256, hd 16, Q 200) against the reference.
-    B: 4 blocks + 6+6 enc-dec, 3 classes; C: full ViT-H/14, 4 classes."""
+    B: 4 blocks + 6+6 enc-dec, 3 classes; C: full ViT-H/14, 4 classes.  fold 0: the standalone
+    backbone LayerNorm passes (production); fold 3 / 1: both / LN1 only folded into the consuming
+    GEMMs (dart_set_ln_fold, an A/B option measured slower)."""
+    from paper_2603_11441_b200 import _native
+
     g = load_golden(name)
     model = model_for(g)
     image = scene_for(name, model.config)
     assert hashlib_image(image) == str(g["image_checksum"])
-    fpn = D.backbone_forward(model, image)
+    lib = _native.load()
+    lib.dart_set_ln_fold(fold)  # before the model's handle exists: it builds the folded weights
+    try:
+        fpn = D.backbone_forward(model, image)
+        h = D.model.native_handle(model, torch.device("cuda", 0))
+        counts = []
+        for f in (fold, 0):  # the same handle, folded and not: the fold removes the LN launches
+            lib.dart_set_ln_fold(f)
+            lib.dart_reset_launch_count(h.ptr)
+            D.backbone_forward(model, image)
+            counts.append(int(lib.dart_launch_count(h.ptr)))
+    finally:
+        lib.dart_set_ln_fold(0)
+    nb = model.config.num_blocks
+    # LN1 folds remove nb LN launches (and the FPN cast: fc2 leaves fp16 x), LN2 folds nb more
+    assert counts[1] - counts[0] == {3: 2 * nb + 1, 1: nb + 1, 0: 0}[fold], counts
     rows = g["rows"]
     l0 = fpn.levels[0][rows]
     c0 = cosine(l0, g["L0"])
@@ -293,8 +313,8 @@ def test_full_width_parity(name):
     raw = D.encdec_forward(model, fpn, D.text_encode(model, names).stack(names))
     err_b, err_s, err_p = raw_errors(g, raw)
     frac = check_decisions(g, raw, err_s, err_p, err_b)
-    print(f"{name}: L0 cos {c0:.6f} rel {e0:.2e}; box {err_b:.2e} score {err_s:.2e} presence {err_p:.2e}; "
-          f"decided {frac:.2f}")
+    print(f"{name} fold {fold}: L0 cos {c0:.6f} rel {e0:.2e}; box {err_b:.2e} score {err_s:.2e} "
+          f"presence {err_p:.2e}; decided {frac:.2f}")
     te, tb, ts, tp = TOL[name]
     assert c0 > 0.99999 and e0 < te
     assert err_b < tb and err_s < ts and err_p < tp
