@@ -52,27 +52,32 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t addr, uint32_t lbo_bytes,
   return d;
 }
 
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT>
+// QT: query tiles per CTA (independent S -> P -> P.V chains sharing each K / V stage; chain t
+// owns TMEM columns [t * CHAIN, (t + 1) * CHAIN) and softmax warps 2 + 4t .. 5 + 4t)
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int QT = 1>
 struct FaCfg {
   static constexpr int NB = HD / 16;                 // 16-dim column blocks
   static constexpr int ON = HD + 16;                 // O columns (values + row-sum block)
-  static constexpr int OCOL = NS * BKV;              // TMEM column of O
-  static constexpr int TMEM_NEED = NS * BKV + ON;
+  static constexpr int OCOL = NS * BKV;              // TMEM column of O (within a chain)
+  static constexpr int CHAIN = NS * BKV + ON;        // TMEM columns per chain
+  static constexpr int TMEM_NEED = QT * CHAIN;
   static constexpr int TMEM = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128
                               : TMEM_NEED <= 256 ? 256 : 512;
   static_assert(TMEM_NEED <= 512 && TMEM * CTAS <= 512, "TMEM budget");
   static_assert(BKV % (8 * SPLIT) == 0 && (BKV / SPLIT) % 8 == 0, "S tile split into 8-column pieces");
-  static constexpr int THREADS = 64 + 128 * SPLIT;  // TMA/alloc warp, MMA warp, 4*SPLIT softmax warps
+  static_assert(QT == 1 || SPLIT == 1, "query-tile chains use whole-row softmax warps");
+  static constexpr int THREADS = 64 + 128 * SPLIT * QT;  // TMA/alloc warp, MMA warp, 4*SPLIT*QT softmax warps
   static constexpr int COLS = BKV / SPLIT;           // S columns per softmax warp
   static constexpr int Q_BLOCK = BQ * 32;            // bytes per Q column block
   static constexpr int KV_BLOCK = BKV * 32;          // bytes per K/V column block
-  static constexpr int Q_BYTES = NB * Q_BLOCK;
+  static constexpr int Q_TILE_BYTES = NB * Q_BLOCK;
+  static constexpr int Q_BYTES = QT * Q_TILE_BYTES;  // one Q buffer (QT tiles)
   static constexpr int K_BYTES = NB * KV_BLOCK;
   static constexpr int V_BYTES = (NB + 1) * KV_BLOCK;  // + ones block
   static constexpr int OFF_K = 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
   static constexpr int OFF_BAR = OFF_V + STAGES * V_BYTES;
-  static constexpr int NBARS = 4 + 4 * STAGES + 3 * NS + 1;
+  static constexpr int NBARS = 4 + 4 * STAGES + QT * (3 * NS + 1);
   static constexpr int OFF_OVF = OFF_BAR + NBARS * 8 + 16;         // overflow bitmask of local items
   static constexpr int OVF_WORDS = ATTN_TC_MAX_LOCAL_ITEMS / 32;
   static constexpr int OFF_RED = OFF_OVF + OVF_WORDS * 4;          // [2][SPLIT][128] partial row maxima
@@ -102,8 +107,11 @@ __device__ __forceinline__ void wait_sel(uint64_t* bar, uint32_t parity, int tag
     mbar_wait_dbg(bar, parity, tag, dbg);
 }
 
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK>
-__global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREADS, CTAS)
+// KSPL: split-KV instantiation (AttnTcArgs::kv_split, partial outputs); without it the key range is
+// whole and the split bookkeeping compiles out (register pressure of the hd-16 kernel is at its cap)
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK, int QT = 1,
+          bool KSPL = false>
+__global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT, QT>::THREADS, CTAS)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV, AttnTcArgs a) {
   // SPIN bit 4 (PROD): the debug / trace / microbenchmark hooks compiled out -- every kernel
   // parameter read after an asm "memory" clobber is a constant-bank reload in the serial
@@ -112,7 +120,8 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   int* const dbg = PROD ? nullptr : a.dbg;
   long long* const trace = PROD ? nullptr : a.trace;
   const int sm_only = PROD ? 0 : a.softmax_only;
-  using L = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
+  using L = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT, QT>;
+  static_assert(QT == 1 || !LEAN, "query-tile chains use the commit-per-tile protocol");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
@@ -122,11 +131,11 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
   uint64_t* k_empty = k_full + STAGES;     // STAGES
   uint64_t* v_full = k_empty + STAGES;     // STAGES
   uint64_t* v_empty = v_full + STAGES;     // STAGES
-  uint64_t* s_full = v_empty + STAGES;     // NS
-  uint64_t* p_full = s_full + NS;          // NS
-  uint64_t* o_done = p_full + NS;          // NS
-  uint64_t* item_done = o_done + NS;       // 1 (LEAN): all P.V of an item complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_done + 1);
+  uint64_t* s_full = v_empty + STAGES;     // [QT][NS]
+  uint64_t* p_full = s_full + QT * NS;     // [QT][NS]
+  uint64_t* o_done = p_full + QT * NS;     // [QT][NS]
+  uint64_t* item_done = o_done + QT * NS;  // [QT] (LEAN): all P.V of an item complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_done + QT);
   uint32_t* ovf = reinterpret_cast<uint32_t*>(smem + L::OFF_OVF);
   // TMEM column (within an S buffer) of the fp16 P pair holding key k: slice k / COLS keeps its
   // P in the first half of its own S columns
@@ -134,10 +143,34 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
 
   const int warp = warp_id(), lane = lane_id();
   const int q_tiles = (a.Lq + BQ - 1) / BQ;
-  const int n_items = q_tiles * a.heads * a.items;
+  const int q_groups = (q_tiles + QT - 1) / QT;  // an item covers QT query tiles (rows past Lq: zeros)
+  const int KS = KSPL ? a.kv_split : 1;
+  const int n_items = q_groups * a.heads * a.items * KS;
   // MASK: Lkv not a multiple of BKV (decoder self-attention over 201 tokens, text cross-attention
   // over 32): the last key tile is partial and its keys >= Lkv are masked to P = 0
-  const int nkv = MASK ? (a.Lkv + BKV - 1) / BKV : a.Lkv / BKV;
+  const int nkv_all = MASK ? (a.Lkv + BKV - 1) / BKV : a.Lkv / BKV;
+  // item -> (q tile, head, key split, item z) and the split's key tiles [j0, j0 + nkv)
+  struct Item {
+    int qt, h, s, z, j0, nkv;
+  };
+  auto item_of = [&](int item) {  // qt: the first query tile of the item's group
+    Item it;
+    it.qt = (item % q_groups) * QT;
+    it.h = (item / q_groups) % a.heads;
+    if constexpr (KSPL) {
+      it.s = (item / (q_groups * a.heads)) % KS;
+      it.z = item / (q_groups * a.heads * KS) + a.z_base;
+      const int base = nkv_all / KS, rem = nkv_all % KS;
+      it.j0 = it.s * base + (it.s < rem ? it.s : rem);
+      it.nkv = base + (it.s < rem ? 1 : 0);
+    } else {
+      it.s = 0;
+      it.z = item / (q_groups * a.heads) + a.z_base;
+      it.j0 = 0;
+      it.nkv = nkv_all;
+    }
+    return it;
+  };
   // TMA and MMA warps (SMSPs 0 / 1).  The tcgen05.mma stream costs its SMSP issue time, which the
   // softmax warp sharing that SMSP loses; the second CTA of an SM (blocks are placed round-robin,
   // so blockIdx >= grid/2) swaps the two roles to put its MMA issue on the other SMSP.
@@ -151,12 +184,12 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < QT * NS; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 4 * SPLIT);
       mbar_init(&o_done[s], 1);
     }
-    mbar_init(item_done, 1);
+    for (int t = 0; t < QT; ++t) mbar_init(&item_done[t], 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -203,17 +236,18 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
           if (!todo(local)) continue;
-          const int qt = item % q_tiles;
-          const int h = (item / q_tiles) % a.heads;
-          const int z = item / (q_tiles * a.heads) + a.z_base;
-          const int row0 = (a.kv_mod > 0 ? z % a.kv_mod : z) * a.Lkv;  // kv_mod: K/V shared per class
+          const Item I = item_of(item);
+          const int qt = I.qt, h = I.h, z = I.z, nkv = I.nkv;
+          // kv_mod: K/V shared per class; the split's first key row
+          const int row0 = (a.kv_mod > 0 ? z % a.kv_mod : z) * a.Lkv + I.j0 * BKV;
           if (do_qk) {
             const int qb = p_it & 1;
             mbar_wait_dbg(&q_empty[qb], ((p_it >> 1) & 1) ^ 1, 1000000 + p_it, dbg);
             mbar_arrive_expect_tx(&q_full[qb], L::Q_BYTES);
-            for (int b = 0; b < L::NB; ++b)
-              tma_load_2d(smem + qb * L::Q_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb], a.q_col + h * HD + b * 16,
-                          z * a.Lq + qt * BQ);
+            for (int t = 0; t < QT; ++t)
+              for (int b = 0; b < L::NB; ++b)
+                tma_load_2d(smem + qb * L::Q_BYTES + t * L::Q_TILE_BYTES + b * L::Q_BLOCK, &tmQ, &q_full[qb],
+                            a.q_col + h * HD + b * 16, z * a.Lq + (qt + t) * BQ);
             ++p_it;
           }
           for (int j = 0; j < nkv; ++j) {
@@ -261,8 +295,10 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           umma_commit_w(&s_full[gg % NS]);
         };
         int local = 0;
+        if constexpr (QT == 1) {
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
           if (!todo(local)) continue;
+          const int nkv = item_of(item).nkv;
           const int qb = m_it & 1;
           const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
           mbar_wait_dbg(&q_full[qb], (m_it >> 1) & 1, 4000000 + m_it, dbg);
@@ -308,6 +344,70 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
           }
           ++m_it;
         }
+        } else {
+        // commit-per-tile protocol, QT chains: per key tile, V(g) and K(g+NS) are awaited once,
+        // then each chain's P.V(g) follows its own P-ready and is chased by its S(g+NS); the K / V
+        // stages are released after the last chain's MMAs read them
+        auto issue_s_chain = [&](int gg, uint32_t sq, int t) {
+          const uint32_t sk = smem_u32(smem + L::OFF_K + (gg % STAGES) * L::K_BYTES);
+#pragma unroll
+          for (int b = 0; b < L::NB; ++b)
+            umma_f16_w(tmem + t * L::CHAIN + (gg % NS) * BKV, desc_sw32(sq + t * L::Q_TILE_BYTES + b * L::Q_BLOCK, 16, 256),
+                       desc_sw32(sk + b * L::KV_BLOCK, 16, 256), idesc_s, b > 0);
+          umma_commit_w(&s_full[t * NS + gg % NS]);
+        };
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+          if (!todo(local)) continue;
+          const int nkv = item_of(item).nkv;
+          const int qb = m_it & 1;
+          const uint32_t sq = smem_u32(smem + qb * L::Q_BYTES);
+          mbar_wait_dbg(&q_full[qb], (m_it >> 1) & 1, 4000000 + m_it, dbg);
+          tc_fence_after();
+          for (int j = 0; j < NS && j < nkv; ++j) {
+            wait_k(m_g + j);
+            tc_fence_after();
+#pragma unroll
+            for (int t = 0; t < QT; ++t) issue_s_chain(m_g + j, sq, t);
+            umma_commit_w(&k_empty[(m_g + j) % STAGES]);
+          }
+          for (int j = 0; j < nkv; ++j, ++m_g) {
+            const int sb = m_g % NS, st = m_g % STAGES;
+            const bool more = j + NS < nkv;
+            const uint32_t sv = smem_u32(smem + L::OFF_V + st * L::V_BYTES);
+            // P-ready first: the K(g+NS) wait sits behind the first P.V, off the P -> P.V path
+#pragma unroll
+            for (int t = 0; t < QT; ++t) {
+              wait_sel<SPIN & 1>(&p_full[t * NS + sb], (m_g / NS) & 1, 5000000 + m_g, dbg);
+              if (t == 0) wait_sel<SPIN & 1>(&v_full[st], (m_g / STAGES) & 1, 6000000 + m_g, dbg);
+              if (t == 0 && trace && blockIdx.x == 0 && lane == 0 && m_g < 256) trace[512 + m_g] = clock64();
+              tc_fence_after();
+              if constexpr (SPLIT == 1) {  // P of key 16*kc at column 8*kc, V rows 16*kc at +512 B
+                umma_f16_ts_seq_w<BKV / 16, 8, 512 / 16>(tmem + t * L::CHAIN + L::OCOL, tmem + t * L::CHAIN + sb * BKV,
+                                                         desc_sw32(sv, L::KV_BLOCK, 256), idesc_pv, j != 0);
+              } else {
+#pragma unroll
+                for (int kc = 0; kc < BKV / 16; ++kc)  // 16 keys per MMA (V rows 16*kc); slice `part`
+                  umma_f16_ts_w(tmem + L::OCOL, tmem + sb * BKV + p_col(kc * 16),
+                                desc_sw32(sv + kc * 512, L::KV_BLOCK, 256), idesc_pv, (j | kc) != 0);
+              }
+              if (t == QT - 1) umma_commit_w(&v_empty[st]);
+              umma_commit_w(&o_done[t * NS + sb]);
+              if (more) {
+                if (t == 0) {
+                  wait_k(m_g + NS);
+                  tc_fence_after();
+                }
+                issue_s_chain(m_g + NS, sq, t);
+                if (t == QT - 1) umma_commit_w(&k_empty[(m_g + NS) % STAGES]);
+              }
+            }
+            if (trace && blockIdx.x == 0 && lane == 0 && m_g < 256) trace[1280 + m_g] = clock64();
+            if (j == nkv - 1) umma_commit_w(&q_empty[qb]);  // every MMA reading this Q buffer issued
+            if (trace && blockIdx.x == 0 && lane == 0 && m_g < 256) trace[768 + m_g] = clock64();
+          }
+          ++m_it;
+        }
+        }
       }
       __syncwarp();
     } else {
@@ -316,9 +416,13 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
       auto softmax_pass = [&](auto pass_c) {
         constexpr int PASS = decltype(pass_c)::value;
         // softmax warp: TMEM lane quarter (warp & 3), column slice `part` of every S tile
-        const int quarter = warp & 3, part = (warp - 2) >> 2;
+        // chain: the query tile of the item this warp's rows belong to (QT > 1: warps 2+4t..5+4t)
+        const int quarter = warp & 3, part = QT > 1 ? 0 : (warp - 2) >> 2, chain = QT > 1 ? (warp - 2) >> 2 : 0;
         const int r = quarter * 32 + lane;
-        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + chain * L::CHAIN;
+        uint64_t* const c_s_full = s_full + chain * NS;
+        uint64_t* const c_p_full = p_full + chain * NS;
+        uint64_t* const c_o_done = o_done + chain * NS;
         [[maybe_unused]] float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [2][SPLIT][BQ]
         const float c = a.scale_log2;
         // row max of the loaded S slice, combined over the SPLIT slices of this row
@@ -344,14 +448,13 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
         int local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
           if (!todo(local)) continue;
-          const int qt = item % q_tiles;
-          const int h = (item / q_tiles) % a.heads;
-          const int z = item / (q_tiles * a.heads) + a.z_base;
+          const Item I = item_of(item);
+          const int qt = I.qt, h = I.h, z = I.z, nkv = I.nkv;
           float m_ref = -INFINITY;
           float nb = 0.f, cr = 0.f, br = 0.f;
           for (int j = 0; j < nkv; ++j, ++s_g) {
             const int sb = s_g % NS;
-            if (sm_only != 1) wait_sel<(SPIN >> 1) & 1>(&s_full[sb], (s_g / NS) & 1, 7000000 + s_g, dbg);
+            if (sm_only != 1) wait_sel<(SPIN >> 1) & 1>(&c_s_full[sb], (s_g / NS) & 1, 7000000 + s_g, dbg);
             if (trace && blockIdx.x == 0 && warp == 2 && lane == 0 && s_g < 256) trace[s_g] = clock64();
             if (LEAN && warp == 2 && lane == 0 && sm_only != 1) {
               mbar_arrive(&k_empty[s_g % STAGES]);                    // S(g) has consumed K(g)
@@ -361,7 +464,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             if (sm_only == 2) {  // microbenchmark: MMA/TMA pipeline alone
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&p_full[sb]);
+              if (lane == 0) mbar_arrive(&c_p_full[sb]);
               continue;
             }
             tc_fence_after();
@@ -370,7 +473,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             tmem_ld_cols<L::COLS>(sbase, v);
             tmem_ld_wait();
             if constexpr (MASK) {  // keys past Lkv in a partial last tile: score -inf -> P = 0
-              const int valid = a.Lkv - j * BKV - part * L::COLS;
+              const int valid = a.Lkv - (I.j0 + j) * BKV - part * L::COLS;
               if (valid < L::COLS) {
   #pragma unroll
                 for (int k = 0; k < L::COLS; ++k)
@@ -406,7 +509,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
                 const float m_new = fmaxf(m_ref, mx);
                 if (j > 0 && part == 0) {
                   const int gp = LEAN ? s_g1 - 1 : s_g - 1;  // previous P.V complete before O is rescaled
-                  mbar_wait_dbg(&o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, dbg);
+                  mbar_wait_dbg(&c_o_done[gp % NS], (gp / NS) & 1, 8000000 + gp, dbg);
                   tc_fence_after();
                   const float f = fast_exp2((m_ref - m_new) * c);
   #pragma unroll 1
@@ -436,7 +539,7 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0 && sm_only != 1) mbar_arrive(&p_full[sb]);
+            if (lane == 0 && sm_only != 1) mbar_arrive(&c_p_full[sb]);
             if (PASS == 1) ++s_g1;
             if (trace && blockIdx.x == 0 && lane == 0 && s_g < 256) {
               if (warp == 2) trace[256 + s_g] = clock64();
@@ -450,17 +553,32 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
             if constexpr (LEAN)
               mbar_wait_dbg(item_done, s_it & 1, 9000000 + s_it, dbg);
             else
-              mbar_wait_dbg(&o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, dbg);
+              mbar_wait_dbg(&c_o_done[gl % NS], (gl / NS) & 1, 9000000 + gl, dbg);
           }
           ++s_it;
           tc_fence_after();
           float lsum[8];
           tmem_ld8(lane_base + L::OCOL + HD, lsum);
           tmem_ld_wait();
-          const int qrow = qt * BQ + r;
+          const int qrow = (qt + chain) * BQ + r;
           if (PASS == 0) {
             const bool bad = qrow < a.Lq && !(fabsf(lsum[0]) < INFINITY);
             if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&ovf[local >> 5], 1u << (local & 31));
+          }
+          if (KSPL) {  // split-KV: unnormalised O, row sum and reference max (log2 units)
+            float4* dp = reinterpret_cast<float4*>(a.part + ((((size_t)z * a.heads + h) * KS + I.s) * a.Lq + qrow) * 20);
+#pragma unroll 1
+            for (int ch = part; ch < HD / 8; ch += SPLIT) {
+              float o[8];
+              tmem_ld8(lane_base + L::OCOL + ch * 8, o);  // warp-collective: every lane loads
+              tmem_ld_wait();
+              if (qrow < a.Lq) {
+                dp[2 * ch] = make_float4(o[0], o[1], o[2], o[3]);
+                dp[2 * ch + 1] = make_float4(o[4], o[5], o[6], o[7]);
+              }
+            }
+            if (part == 0 && qrow < a.Lq) dp[HD / 4] = make_float4(lsum[0], m_ref * c, 0.f, 0.f);
+            continue;
           }
           const float inv = 1.f / lsum[0];
           __half* dst = a.o + ((long long)z * a.Lq + qrow) * a.o_ld + h * HD;
@@ -497,14 +615,16 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>::THREA
 
 // Kernel variants per head dim; variant 0 is the production choice, the others exist for A/B
 // measurement (DART_FA_VARIANT, scripts/bench_attn.py).
-template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK = false>
+template <int HD, int BKV, int STAGES, int CTAS, int NS, int SPLIT, int NPOLY, int SPIN, int LEAN, bool MASK = false,
+          int QT = 1, bool KSPL = false>
 int launch_v(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int num_sms, cudaStream_t stream) {
-  using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT>;
-  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN, MASK>;
+  using Lay = FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT, QT>;
+  auto kern = fa_tc_kernel<HD, BKV, STAGES, CTAS, NS, SPLIT, NPOLY, SPIN, LEAN, MASK, QT, KSPL>;
+  if (!KSPL && a.kv_split != 1) return (int)cudaErrorInvalidValue;
   static std::atomic<uint64_t> smem_set{0};
   if (const cudaError_t e = set_smem_once(smem_set, kern, Lay::TOTAL); e != cudaSuccess) return (int)e;
   // items of one launch: each CTA may own at most ATTN_TC_MAX_LOCAL_ITEMS (overflow bitmask)
-  const long long per_z = (long long)((a.Lq + BQ - 1) / BQ) * a.heads;
+  const long long per_z = (long long)(((a.Lq + BQ - 1) / BQ + QT - 1) / QT) * a.heads * a.kv_split;
   const long long max_grid = (long long)num_sms * CTAS;
   int zchunk = a.items;
   while (zchunk > 1 && (per_z * zchunk + max_grid - 1) / max_grid > ATTN_TC_MAX_LOCAL_ITEMS) zchunk = (zchunk + 1) / 2;
@@ -542,18 +662,21 @@ int fa_variant() {
 }
 
 // Variant tables (HD, BKV, STAGES, CTAS/SM, S buffers, column slices, poly exps per 16, SPIN,
-// LEAN).  Variant 0 is the default, dispatched below to its hook-free production twin.
-#define DART_FA80_VARIANTS(X)      \
-  X(0, 80, 64, 3, 2, 2, 1, 0, 0, 0) \
-  X(1, 80, 64, 3, 2, 2, 1, 0, 0, 1) \
-  X(2, 80, 64, 3, 2, 2, 1, 4, 0, 0)
-#define DART_FA16_VARIANTS(X)      \
-  X(0, 16, 96, 4, 2, 2, 1, 6, 0, 0) \
-  X(1, 16, 96, 4, 2, 2, 1, 6, 0, 1) \
-  X(2, 16, 96, 4, 2, 2, 1, 8, 0, 0) \
-  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 0)   \
-  X(4, 16, 96, 4, 2, 2, 2, 6, 16, 0)  \
-  X(5, 16, 80, 4, 2, 2, 1, 6, 16, 0)
+// LEAN, query-tile chains per CTA).  Variant 0 is the default, dispatched below to its hook-free
+// production twin.
+#define DART_FA80_VARIANTS(X)         \
+  X(0, 80, 64, 3, 2, 2, 1, 0, 0, 0, 1) \
+  X(1, 80, 64, 3, 2, 2, 1, 0, 0, 1, 1) \
+  X(2, 80, 64, 3, 2, 2, 1, 4, 0, 0, 1)
+#define DART_FA16_VARIANTS(X)           \
+  X(0, 16, 96, 4, 2, 2, 1, 6, 0, 0, 1)   \
+  X(1, 16, 96, 4, 2, 2, 1, 6, 0, 1, 1)   \
+  X(2, 16, 96, 4, 2, 2, 1, 8, 0, 0, 1)   \
+  X(3, 16, 96, 4, 2, 2, 1, 4, 0, 0, 1)   \
+  X(4, 16, 96, 4, 2, 2, 2, 6, 16, 0, 1)  \
+  X(5, 16, 80, 4, 2, 2, 1, 6, 16, 0, 1)  \
+  X(7, 16, 64, 4, 1, 1, 1, 6, 16, 0, 4)  \
+  X(8, 16, 96, 4, 1, 1, 1, 6, 16, 0, 3)
 // Variant 0 issues MMAs from the converged warp 1 (warp-collective umma_*_w, one elected lane):
 // the per-MMA issue path shrank from ~77 to ~40 clk (no per-lane R2UR waterfall), which took hd 80
 // global attention 217 -> 193 us and windowed 36.5 -> 33.2 us (scripts/ab_attn.py); with it the
@@ -566,12 +689,18 @@ int fa_variant() {
 // commit ~44 clk and each mbarrier wait ~40 clk of the issuer's tensor stream
 // (scripts/probes/mma_rate.cu), so the 6 P.V steps of a 96-key tile plus S, commits and waits
 // make a ~600-clk per-tile MMA chain (scripts/trace_attn.py timelines) that S(g+2) sits behind.
+// Query-tile chains (QT tiles per CTA, one CTA per SM, each chain its own S buffers / O / softmax
+// warp group, K / V stages shared; profiles/r02/attn_hd16_chains.log), enc self N=20: production
+// 1987 us; QT 3 x (2 x 64-key S) 2311, QT 4 x (1 x 64) 2097 (variant 7), QT 3 x (1 x 96) 2202
+// (variant 8), QT 2 x (2 x 96) 2299, QT 3 x 64 NPOLY 8 2420 us -- the register file (64 K per SM)
+// caps 12-16 softmax warps at 96-128 registers, below one S tile plus its P, so the extra chains
+// spill; the one-chain-per-CTA code path is kept as it was for QT = 1.
 // Staging P in shared memory or in separate TMEM buffers (S released at load time) was slower
 // (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.  A decoupled
 // variant at 96-key tiles (2 S buffers | one P buffer | O without the ones block, row sums in
 // registers; git history "fa_dec_kernel") was correct but also slower: N=20 2.67-2.78 vs 2.41 ms.
 int kv_tile_of(int hd, int var) {
-#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN, QT) \
   if (hd == HD && var == V) return BKV;
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
@@ -581,7 +710,65 @@ int kv_tile_of(int hd, int var) {
   return 0;
 }
 
+// One thread per (item, head, query row): w_s = 2^(m_s - max m), o = sum w_s O_s / sum w_s l_s.
+template <int HD>
+__global__ void split_combine_kernel(const float* __restrict__ part, __half* __restrict__ o, int o_ld, int items,
+                                     int heads, int Lq, int KS) {
+  pdl_wait();
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)items * heads * Lq) return;
+  const int row = (int)(t % Lq);
+  const int h = (int)((t / Lq) % heads);
+  const int z = (int)(t / ((long long)Lq * heads));
+  const float4* p0 = reinterpret_cast<const float4*>(part) + (((size_t)z * heads + h) * KS * Lq + row) * 5;
+  const size_t sstride = (size_t)Lq * 5;  // float4s between splits
+  float mx = -INFINITY;
+  for (int s = 0; s < KS; ++s) mx = fmaxf(mx, p0[s * sstride + HD / 4].y);
+  float acc[HD], l = 0.f;
+#pragma unroll
+  for (int k = 0; k < HD; ++k) acc[k] = 0.f;
+  for (int s = 0; s < KS; ++s) {
+    const float4* ps = p0 + s * sstride;
+    const float4 lm = ps[HD / 4];
+    const float w = exp2f(lm.y - mx);
+    l = fmaf(w, lm.x, l);
+#pragma unroll
+    for (int k = 0; k < HD / 4; ++k) {
+      const float4 v = ps[k];
+      acc[4 * k] = fmaf(w, v.x, acc[4 * k]);
+      acc[4 * k + 1] = fmaf(w, v.y, acc[4 * k + 1]);
+      acc[4 * k + 2] = fmaf(w, v.z, acc[4 * k + 2]);
+      acc[4 * k + 3] = fmaf(w, v.w, acc[4 * k + 3]);
+    }
+  }
+  const float inv = 1.f / l;
+  uint4* dst = reinterpret_cast<uint4*>(o + ((long long)z * Lq + row) * o_ld + h * HD);
+#pragma unroll
+  for (int k = 0; k < HD / 8; ++k)
+    dst[k] = make_uint4(pack_half2(acc[8 * k] * inv, acc[8 * k + 1] * inv), pack_half2(acc[8 * k + 2] * inv, acc[8 * k + 3] * inv),
+                        pack_half2(acc[8 * k + 4] * inv, acc[8 * k + 5] * inv), pack_half2(acc[8 * k + 6] * inv, acc[8 * k + 7] * inv));
+  pdl_launch_dependents();
+}
+
 }  // namespace
+
+int attention_split_combine(const float* part, __half* o, int o_ld, int items, int heads, int Lq, int kv_split,
+                            int hd, cudaStream_t stream) {
+  if (hd != 16) return (int)cudaErrorInvalidValue;
+  const long long n = (long long)items * heads * Lq;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((n + 127) / 128));
+  cfg.blockDim = dim3(128);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (pdl_enabled()) {
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, split_combine_kernel<16>, part, o, o_ld, items, heads, Lq, kv_split);
+  return (int)cudaGetLastError();
+}
 
 void attention_tc_set_variant(int v) { g_fa_variant = v < 0 ? 0 : v; }
 
@@ -602,10 +789,10 @@ bool attention_tc_supported(int head_dim, int Lkv) {
 int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcArgs& a, int head_dim, int num_sms,
                  cudaStream_t stream) {
   const int var = fa_variant();
-#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN) \
-  if (V != 0 && head_dim == HD && var == V)                                                  \
-    return a.Lkv % BKV ? launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN, true>(tmQ, tmKV, a, num_sms, stream) \
-                       : launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN>(tmQ, tmKV, a, num_sms, stream);
+#define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN, QT) \
+  if (V != 0 && head_dim == HD && var == V && a.kv_split == 1)                               \
+    return a.Lkv % BKV ? launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN, true, QT>(tmQ, tmKV, a, num_sms, stream) \
+                       : launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN, false, QT>(tmQ, tmKV, a, num_sms, stream);
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
 #undef X
@@ -621,6 +808,9 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
     if (a.Lkv <= SHORT_KV)  // text cross-attention: one (possibly partial) 32-key tile per item
       return a.Lkv == SHORT_KV ? launch_v<16, SHORT_KV, 2, 4, 2, 1, 0, 16, 0>(tmQ, tmKV, a, num_sms, stream)
                                : launch_v<16, SHORT_KV, 2, 4, 2, 1, 0, 16, 0, true>(tmQ, tmKV, a, num_sms, stream);
+    if (a.kv_split > 1)  // split-KV (decoder cross-attention)
+      return a.Lkv % 96 ? launch_v<16, 96, 4, 2, 2, 1, 6, 16, 0, true, 1, true>(tmQ, tmKV, a, num_sms, stream)
+                        : launch_v<16, 96, 4, 2, 2, 1, 6, 16, 0, false, 1, true>(tmQ, tmKV, a, num_sms, stream);
     if (a.Lkv % 96 != 0)  // decoder self-attention (201 = 2 x 96 + 9 keys)
       return launch_v<16, 96, 4, 2, 2, 1, 6, 16, 0, true>(tmQ, tmKV, a, num_sms, stream);
     return hooks ? launch_v<16, 96, 4, 2, 2, 1, 6, 0, 0>(tmQ, tmKV, a, num_sms, stream)

@@ -115,6 +115,8 @@ int g_splitk_mask = getenv("DART_SPLITK") ? atoi(getenv("DART_SPLITK")) : 0;
 // statistics more than the LayerNorm pass it replaces costs.  The folded weights exist only in
 // handles created while the fold is enabled (DART_LN_FOLD=<mask> or dart_set_ln_fold).
 int g_ln_fold = getenv("DART_LN_FOLD") ? atoi(getenv("DART_LN_FOLD")) : 0;
+// split-KV factor of the decoder cross-attention (xattn); DART_ATTN_SPLIT=<k> overrides, <= 1: off (A/B)
+int g_attn_split = getenv("DART_ATTN_SPLIT") ? atoi(getenv("DART_ATTN_SPLIT")) : 2;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
@@ -125,7 +127,7 @@ long long* g_attn_trace = nullptr;
 // [items*Lkv, kv_ld] (k at k_col, v at v_col), output [items*Lq, o_ld] at column h*hd.
 int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv_ld, int k_col, int v_col, __half* o,
             int o_ld, int items, int heads, int Lq, int Lkv, int hd, int num_sms, cudaStream_t s, int* dbg = nullptr,
-            int kv_mod = 0) {
+            int kv_mod = 0, int kv_split = 1, float* part = nullptr) {
   CUtensorMap tq, tkv;  // maps cover exactly the used column ranges
   const int q_inner = q_col + heads * hd, kv_inner = (k_col > v_col ? k_col : v_col) + heads * hd;
   const int kv_items = kv_mod > 0 ? kv_mod : items;
@@ -148,11 +150,14 @@ int attn_tc(const __half* qbuf, int q_ld, int q_col, const __half* kvbuf, int kv
   a.force_safe = g_attn_force_safe;
   a.trace = g_attn_trace;
   a.kv_mod = kv_mod;
+  a.kv_split = kv_split;
+  a.part = part;
   {
     const char* e = getenv("DART_FA_SOFTMAX_ONLY");  // microbenchmarks: 1 softmax alone, 2 MMA alone
     a.softmax_only = e ? atoi(e) : 0;
   }
   int rc = attention_tc(tq, tkv, a, hd, num_sms, s);
+  if (!rc && kv_split > 1) rc = attention_split_combine(part, o, o_ld, items, heads, Lq, kv_split, hd, s);
   if (rc) return fail(DART_ERR_CUDA, std::string("attention_tc: ") + cudaGetErrorString((cudaError_t)rc));
   return 0;
 }
@@ -286,8 +291,11 @@ struct dart_model {
   long long splitk_cap = 0;  // flags
   float* splitk_ws = nullptr;
   long long splitk_ws_cap = 0;  // floats
+  float* attn_part = nullptr;  // split-KV attention partials (per handle)
+  size_t attn_part_cap = 0;    // floats
 
   ~dart_model() {
+    if (attn_part) cudaFree(attn_part);
     if (splitk_flags) cudaFree(splitk_flags);
     if (splitk_ws) cudaFree(splitk_ws);
     bb_ws.release();
@@ -691,9 +699,27 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
       m->launches++;
       RUN(attn_tc(q, D, 0, kv, 2 * D, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
     } else {
+      // split-KV for the decoder cross-attention (201 queries over T = 5184 keys): at small N its
+      // (q tile, head, class) items leave most CTA slots idle (4 classes: 2 x 16 x 4 = 128 items
+      // for 296 slots, each over 54 key tiles), so every item's key range runs on g_attn_split
+      // CTAs and is merged.  The split does not depend on N, so a class's rows stay bitwise
+      // independent of the batch
+      const int ks = (hd == 16 && Lk >= 1024 && g_attn_split > 1) ? g_attn_split : 1;
+      if (ks > 1) {
+        const size_t need = (size_t)sp.items * H * ks * sp.Lq * 20;
+        if (need > m->attn_part_cap) {
+          if (m->attn_part) cudaFree(m->attn_part);
+          m->attn_part = nullptr;
+          m->attn_part_cap = 0;
+          if (cudaMalloc(&m->attn_part, need * sizeof(float)) != cudaSuccess)
+            return fail(DART_ERR_CUDA, "split-KV workspace allocation failed");
+          m->attn_part_cap = need;
+        }
+        m->launches++;  // the merge kernel
+      }
       m->launches++;
       RUN(attn_tc(q, D, 0, sp.kv16, sp.kv_tok_stride, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s, nullptr,
-                  sp.kv_mod));
+                  sp.kv_mod, ks, m->attn_part));
     }
     return resid_gemm(m, o, rows, D, w.out, x, next, h, s);
   }
@@ -903,6 +929,8 @@ int dart_model_fork(const dart_model* parent, dart_model** out) {
   f->splitk_cap = 0;
   f->splitk_ws = nullptr;
   f->splitk_ws_cap = 0;
+  f->attn_part = nullptr;
+  f->attn_part_cap = 0;
   *out = f;
   return DART_OK;
 }

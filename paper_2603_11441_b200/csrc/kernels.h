@@ -161,7 +161,18 @@ struct AttnTcArgs {
   int softmax_only = 0;        // microbenchmark: softmax warps run on stale S without MMA / TMA
   long long* trace = nullptr;  // microbenchmark: CTA 0 clock64 stamps [7][256] of the first 256 tiles
   int kv_mod = 0;              // > 0: item z reads K/V item z % kv_mod (text K/V shared by a class's images)
+  // Split-KV (flash-decoding): kv_split > 1 runs each (q tile, head, item) as kv_split CTAs over
+  // consecutive ranges of key tiles; each writes its rows' unnormalised O, row sum and reference
+  // max (log2 units) to part[(((z * heads + h) * kv_split + s) * Lq + row) * 20 + {0..15, 16, 17}]
+  // and attention_split_combine merges them into o.  For launches with too few items to fill
+  // the GPU (decoder cross-attention at small N: 201 queries x 5184 keys per class).
+  int kv_split = 1;
+  float* part = nullptr;
 };
+// Merge of the kv_split partial results of attention_tc (hd 16): o row = sum_s w_s O_s / sum_s w_s l_s
+// with w_s = 2^(m_s - max m).
+int attention_split_combine(const float* part, __half* o, int o_ld, int items, int heads, int Lq, int kv_split,
+                            int hd, cudaStream_t stream);
 constexpr int ATTN_TC_MAX_LOCAL_ITEMS = 4096;  // items per CTA per launch (overflow bitmask in smem)
 int attention_tc_kv_tile(int head_dim, int Lkv);  // key tile (64 hd 80, 96 hd 16, 32 hd 16 short), 0 = unsupported
 void attention_tc_set_variant(int v);  // microbenchmarks (DART_FA_VARIANT otherwise)
