@@ -464,6 +464,8 @@ def run_ours(args):
             r["value_serial"] = imgs / (ms / 1000.0)
             r["ms_per_step_serial"] = ms / args.steps
             r["gpu_launches_serial"] = det.launch_count()
+        # where one serial step's device time goes (CUDA events between the stages)
+        r["stage_ms"] = {k: round(v, 4) for k, v in det.stage_times(dev_pool[0], reps=3).items()}
         # inter-frame pipeline (headline value)
         for i in range(args.warmup):
             det.detect_device_pipelined(dev_pool[i % n_imgs])
@@ -557,12 +559,13 @@ def run_ours(args):
             "gpu_launches": r4["gpu_launches"],
             "value_serial": r4.get("value_serial"), "ms_per_step_serial": r4.get("ms_per_step_serial"),
             "gpu_launches_serial": r4.get("gpu_launches_serial"),
+            "stage_ms_serial": r4.get("stage_ms"),
             "value_default_thresholds": r4.get("value_default_thresholds"),
             "kept_detections_last_step": r4["kept_detections_last_step"],
             "detections_e2e_last": r4["detections_e2e_last"],
             "n80": None if r80 is None else {
                 "classes": N80, "value": r80["value"], "unit": "images/s", "ms_per_step": r80["ms_per_step"],
-                "e2e": r80["e2e"], "gpu_launches": r80["gpu_launches"],
+                "e2e": r80["e2e"], "gpu_launches": r80["gpu_launches"], "stage_ms_serial": r80.get("stage_ms"),
                 "kept_detections_last_step": r80["kept_detections_last_step"],
                 "step_roofline_frac": gflops_per_image(cfg, N80) * r80["value"] / world / 1000.0 /
                 pk["bf16_tflops_sustained"],

@@ -22,6 +22,25 @@ from .pipeline import Detection, PipelineConfig, _require_classes
 from .tensors import device_mode, precision_code
 
 
+class _nvtx:
+    """NVTX range around a host-side enqueue (shows the stages on an nsys / ncu --nvtx timeline;
+    a no-op push/pop otherwise)."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        import torch
+
+        torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        import torch
+
+        torch.cuda.nvtx.range_pop()
+        return False
+
+
 def _on_device(fn):
     """Run a Detector method with its GPU as the current device: the C ABI allocates
     workspaces and sets kernel attributes on the CURRENT device."""
@@ -122,6 +141,10 @@ class Detector:
 
     def _enqueue_backbone(self, h, images, b, st: int) -> None:
         """dart_backbone of one batch into slot `b` on stream `st` (the call clears the flags)."""
+        with _nvtx("dart.backbone"):
+            self._enqueue_backbone_impl(h, images, b, st)
+
+    def _enqueue_backbone_impl(self, h, images, b, st: int) -> None:
         B = int(images.shape[0])
         if self._bb_precision:
             _native.check(self.lib.dart_model_set_precision(h.ptr, self._bb_precision))
@@ -135,6 +158,12 @@ class Detector:
     def _enqueue_decode(self, h, b, B: int, st: int, l0_ptr) -> None:
         """Class-batched enc-dec (one pass per n_max chunk) and post-processing of slot `b` on
         stream `st`.  l0_ptr None: the level-0 features still in `h`'s backbone workspace."""
+        with _nvtx("dart.encdec"):
+            self._enqueue_encdec(h, b, B, st, l0_ptr)
+        with _nvtx("dart.postprocess"):
+            self._enqueue_postprocess(h, b, B, st)
+
+    def _enqueue_encdec(self, h, b, B: int, st: int, l0_ptr) -> None:
         import torch
 
         lib = self.lib
@@ -156,6 +185,10 @@ class Detector:
                     b["scores"][:, off: off + n].copy_(sc)
                     b["presence"][:, off: off + n].copy_(pr)
             off += n
+
+    def _enqueue_postprocess(self, h, b, B: int, st: int) -> None:
+        lib = self.lib
+        N, Q = len(self.class_names), self.model.config.num_queries
         c = self.cfg
         xc = int(c.cross_class_nms)
         if xc and B > 1:
@@ -183,6 +216,38 @@ class Detector:
         self._enqueue_backbone(self.handle, images, b, st)
         self._enqueue_decode(self.handle, b, B, st, None)
         return b
+
+    @_on_device
+    def stage_times(self, images, reps: int = 5) -> dict:
+        """Per-stage device time of `detect_device` on the current stream (CUDA events between the
+        stages; one untimed warm-up): {"backbone", "encdec", "postprocess", "total"} in ms, the
+        mean over `reps` runs.  images: device float32 [B, S, S, 3]."""
+        import torch
+
+        B = int(images.shape[0])
+        b = self._buffers(B)
+        cur = torch.cuda.current_stream(self.device)
+        st = cur.cuda_stream
+        names = ["backbone", "encdec", "postprocess"]
+        acc = dict.fromkeys(names + ["total"], 0.0)
+        for r in range(reps + 1):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(cur)
+            self._enqueue_backbone(self.handle, images, b, st)
+            ev[1].record(cur)
+            with _nvtx("dart.encdec"):
+                self._enqueue_encdec(self.handle, b, B, st, None)
+            ev[2].record(cur)
+            with _nvtx("dart.postprocess"):
+                self._enqueue_postprocess(self.handle, b, B, st)
+            ev[3].record(cur)
+            ev[3].synchronize()
+            if r == 0:
+                continue
+            for i, n in enumerate(names):
+                acc[n] += ev[i].elapsed_time(ev[i + 1]) / reps
+            acc["total"] += ev[0].elapsed_time(ev[3]) / reps
+        return acc
 
     # ------------------------------------------------------------------ inter-frame pipelining
     def _pipeline(self, B: int):

@@ -87,3 +87,18 @@ def test_graph_pipeline_matches_detect():
             assert torch.equal(g[k], ref[k]), k
         for it, n in enumerate(ref["kc"].tolist()):
             assert torch.equal(g["kq"][it, :n], ref["kq"][it, :n])
+
+
+def test_stage_times_cover_the_step():
+    """Detector.stage_times (CUDA events between backbone / enc-dec / post-processing, SURVEY section 5
+    tracing): every stage is timed, the stages add up to the step, and the step still produces the
+    same detections as detect()."""
+    model, names, cfg, imgs = _setup(1)
+    img = imgs[0]
+    det = Detector(model, names, cfg)
+    dimg = torch.from_numpy(img[None]).cuda()
+    t = det.stage_times(dimg, reps=3)
+    assert set(t) == {"backbone", "encdec", "postprocess", "total"}
+    assert all(v > 0 for v in t.values())
+    assert abs(t["backbone"] + t["encdec"] + t["postprocess"] - t["total"]) < 0.05 * t["total"] + 0.05
+    assert det.detect(img) == det.detect(img)
