@@ -136,6 +136,12 @@ int dart_nccl_available(void);
 int dart_nccl_unique_id(uint8_t* id /* [DART_NCCL_ID_BYTES], host */);
 int dart_nccl_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, dart_comm** out);
 void dart_nccl_comm_destroy(dart_comm* c);
+/* Failure detection: 0 while the communicator is healthy, else the asynchronous NCCL error (a
+ * dead peer, a broken link) as a status + dart_last_error; never blocks.  dart_nccl_comm_abort
+ * aborts the communicator (ncclCommAbort) so that no rank stays blocked in a collective; later
+ * calls on it fail.  The timeout policy is the caller's (Python: distributed.NcclComm.wait). */
+int dart_nccl_comm_check(dart_comm* c);
+int dart_nccl_comm_abort(dart_comm* c);
 int32_t dart_nccl_comm_size(const dart_comm* c);
 int32_t dart_nccl_comm_rank(const dart_comm* c);
 /* recv [nranks * bytes_per_rank] <- send [bytes_per_rank] of every rank, in rank order */

@@ -41,6 +41,8 @@ EXPORTS = (
     "dart_nccl_unique_id",
     "dart_nccl_comm_create",
     "dart_nccl_comm_destroy",
+    "dart_nccl_comm_check",
+    "dart_nccl_comm_abort",
     "dart_nccl_comm_size",
     "dart_nccl_comm_rank",
     "dart_nccl_all_gather",
@@ -175,6 +177,10 @@ def load() -> ctypes.CDLL:
     lib.dart_nccl_comm_create.restype = ctypes.c_int
     lib.dart_nccl_comm_destroy.argtypes = [P]
     lib.dart_nccl_comm_destroy.restype = None
+    lib.dart_nccl_comm_check.argtypes = [P]
+    lib.dart_nccl_comm_check.restype = ctypes.c_int
+    lib.dart_nccl_comm_abort.argtypes = [P]
+    lib.dart_nccl_comm_abort.restype = ctypes.c_int
     lib.dart_nccl_comm_size.argtypes = [P]
     lib.dart_nccl_comm_size.restype = I32
     lib.dart_nccl_comm_rank.argtypes = [P]

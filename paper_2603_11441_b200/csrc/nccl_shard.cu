@@ -37,6 +37,8 @@ struct NcclApi {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;  // optional
+  ncclResult_t (*comm_abort)(ncclComm_t) = nullptr;                       // optional
   std::string why;
   bool ok = false;
 };
@@ -58,6 +60,8 @@ NcclApi& nccl() {
     api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+    api.get_async_error = reinterpret_cast<decltype(api.get_async_error)>(sym("ncclCommGetAsyncError"));
+    api.comm_abort = reinterpret_cast<decltype(api.comm_abort)>(sym("ncclCommAbort"));
     api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_gather && api.all_reduce &&
              api.error_string;
     if (!api.ok) api.why = "libnccl.so.2 lacks an expected symbol";
@@ -179,17 +183,41 @@ int dart_nccl_comm_create(const uint8_t* id, int32_t nranks, int32_t rank, dart_
 
 void dart_nccl_comm_destroy(dart_comm* c) { delete c; }
 
+// Failure detection: a peer that died or a broken link surfaces as an
+// asynchronous communicator error; dart_nccl_comm_check reports it without blocking, and
+// dart_nccl_comm_abort releases the communicator so that no rank stays blocked in a collective
+// (the caller's timeout policy decides when: distributed.NcclComm.wait).
+int dart_nccl_comm_check(dart_comm* c) {
+  if (!c) return dart::set_error(DART_ERR_INVALID, "dart_nccl_comm_check: null communicator");
+  if (!c->comm) return dart::set_error(DART_ERR_CUDA, "NCCL communicator was aborted");
+  if (!nccl().get_async_error) return DART_OK;
+  ncclResult_t async = ncclSuccess;
+  if (ncclResult_t r = nccl().get_async_error(c->comm, &async); r != ncclSuccess)
+    return nccl_fail("ncclCommGetAsyncError", r);
+  return async == ncclSuccess || async == ncclInProgress ? DART_OK : nccl_fail("NCCL asynchronous error", async);
+}
+
+int dart_nccl_comm_abort(dart_comm* c) {
+  if (!c) return dart::set_error(DART_ERR_INVALID, "dart_nccl_comm_abort: null communicator");
+  if (!c->comm) return DART_OK;
+  ncclResult_t r = nccl().comm_abort ? nccl().comm_abort(c->comm) : nccl().comm_destroy(c->comm);
+  c->comm = nullptr;  // the destructor must not destroy it again
+  return r == ncclSuccess ? DART_OK : nccl_fail("ncclCommAbort", r);
+}
+
 int32_t dart_nccl_comm_size(const dart_comm* c) { return c ? c->nranks : 0; }
 int32_t dart_nccl_comm_rank(const dart_comm* c) { return c ? c->rank : -1; }
 
 int dart_nccl_all_gather(dart_comm* c, const void* send, void* recv, int64_t bytes_per_rank, void* stream) {
   if (!c || !send || !recv || bytes_per_rank < 0) return dart::set_error(DART_ERR_INVALID, "dart_nccl_all_gather: bad args");
+  if (!c->comm) return dart::set_error(DART_ERR_CUDA, "NCCL communicator was aborted");
   ncclResult_t r = nccl().all_gather(send, recv, (size_t)bytes_per_rank, ncclUint8, c->comm, (cudaStream_t)stream);
   return r == ncclSuccess ? DART_OK : nccl_fail("ncclAllGather", r);
 }
 
 int dart_nccl_all_reduce_max_i32(dart_comm* c, int32_t* buf, int64_t count, void* stream) {
   if (!c || !buf || count < 0) return dart::set_error(DART_ERR_INVALID, "dart_nccl_all_reduce_max_i32: bad args");
+  if (!c->comm) return dart::set_error(DART_ERR_CUDA, "NCCL communicator was aborted");
   ncclResult_t r = nccl().all_reduce(buf, buf, (size_t)count, ncclInt32, ncclMax, c->comm, (cudaStream_t)stream);
   return r == ncclSuccess ? DART_OK : nccl_fail("ncclAllReduce", r);
 }
@@ -198,6 +226,7 @@ int dart_class_sharded(dart_model* m, dart_comm* c, const float* images, int32_t
                        double* boxes, double* score_logits, double* presence_logits, int32_t* flags, void* stream) {
   if (!m || !c || !images || B <= 0 || !text || N <= 0 || !boxes || !score_logits || !presence_logits || !flags)
     return dart::set_error(DART_ERR_INVALID, "dart_class_sharded: bad args");
+  if (!c->comm) return dart::set_error(DART_ERR_CUDA, "NCCL communicator was aborted");
   const dart_model_desc* d = dart_model_get_desc(m);
   const int g = d->image_size / d->patch_size, T = g * g, D = d->text_dim, Q = d->num_queries, Lt = d->text_tokens;
   const int W = c->nranks, R = c->rank;

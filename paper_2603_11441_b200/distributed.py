@@ -252,6 +252,36 @@ class NcclComm:
         self.ptr = out.value
         self.world, self.rank = world, rank
 
+    def check(self) -> None:
+        """Raise if the communicator has an asynchronous error (dead peer, broken link); never blocks."""
+        from . import _native
+
+        _native.check(self.lib.dart_nccl_comm_check(self.ptr))
+
+    def abort(self) -> None:
+        """ncclCommAbort: release every collective this rank is blocked in; later calls fail."""
+        if self.ptr:
+            self.lib.dart_nccl_comm_abort(self.ptr)
+
+    def wait(self, event, timeout_s: float = 60.0, poll_s: float = 1e-3) -> None:
+        """Block until `event` (a torch.cuda.Event recorded after a round) completes, polling the
+        communicator's asynchronous error; on an error or after `timeout_s` the communicator is
+        aborted (so no rank stays blocked in a collective) and RuntimeError is raised."""
+        import time
+
+        deadline = time.monotonic() + timeout_s
+        while not event.query():
+            try:
+                self.check()
+            except Exception as e:
+                self.abort()
+                raise RuntimeError(f"class-sharded round failed: {e}") from e
+            if time.monotonic() > deadline:
+                self.abort()
+                raise RuntimeError(f"class-sharded round timed out after {timeout_s:.1f} s (communicator aborted)")
+            time.sleep(poll_s)
+        self.check()
+
     def close(self):
         if self.ptr:
             self.lib.dart_nccl_comm_destroy(self.ptr)
@@ -264,11 +294,13 @@ class NcclComm:
             pass
 
 
-def class_sharded_raw_native(engine, comm: NcclComm, images, class_names):
+def class_sharded_raw_native(engine, comm: NcclComm, images, class_names, timeout_s: float | None = None):
     """`class_sharded_raw` through the C ABI (dart_class_sharded): one call per round, all
     collectives inside the library.  images [B, S, S, 3] (this rank's); returns boxes [B, N, Q, 4],
     score logits [B, N, Q], presence logits [B, N] (float64, device) of this rank's images over
-    all N classes, and the rank-reduced flags (int32 [1]).  Asynchronous on the current stream."""
+    all N classes, and the rank-reduced flags (int32 [1]).  Asynchronous on the current stream,
+    unless `timeout_s` is given: then the round is awaited with NcclComm.wait (asynchronous NCCL
+    errors and the timeout abort the communicator and raise)."""
     import torch
 
     from . import _native
@@ -286,4 +318,8 @@ def class_sharded_raw_native(engine, comm: NcclComm, images, class_names):
         _native.check(engine.lib.dart_class_sharded(engine.handle.ptr, comm.ptr, imgs.data_ptr(), B, text.data_ptr(), N,
                                                     boxes.data_ptr(), scores.data_ptr(), pres.data_ptr(),
                                                     flags.data_ptr(), _stream_ptr(engine.device)))
+        if timeout_s is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(engine.device))
+            comm.wait(ev, timeout_s)
     return boxes, scores, pres, flags

@@ -75,3 +75,26 @@ def test_native_nccl_bad_image_flag():
     with pytest.raises(ValueError):
         eng.check_flags(int(flags.item()))
     comm.close()
+
+
+def test_native_nccl_failure_detection_and_abort():
+    """SURVEY section 5 failure detection: a healthy communicator checks clean and a round awaited
+    with a timeout completes; an aborted communicator reports the failure on every later call
+    instead of blocking (no rank stays stuck in a collective)."""
+    from paper_2603_11441_b200 import _native
+    from paper_2603_11441_b200.distributed import NcclComm, class_sharded_raw_native
+
+    model = D.build_model(D.toy_config(seed=0), with_mask_head=False)
+    image, _ = D.generate_scene(D.SceneSpec(seed=1, num_classes=3))
+    x = torch.from_numpy(image.astype(np.float32))[None].cuda()
+    eng = NativeEngine(model)
+    comm = NcclComm(1, 0)
+    comm.check()
+    b0, s0, p0, f0 = class_sharded_raw_native(eng, comm, x, ["car", "dog"], timeout_s=60.0)
+    assert int(f0.item()) == 0
+    comm.abort()
+    with pytest.raises(_native.NativeError):
+        comm.check()
+    with pytest.raises(_native.NativeError):
+        class_sharded_raw_native(eng, comm, x, ["car", "dog"])
+    comm.close()
