@@ -261,6 +261,12 @@ void dart_set_pdl(int32_t mode);
  * non-zero.  Process wide; tests and A/B measurement. */
 void dart_set_ln_fold(int32_t mask);
 
+/* Split-KV factor (1..8) of the enc-dec decoder cross-attention: each (query tile, head, class) item
+ * over the T image keys runs as k CTAs over consecutive key ranges, merged by a small kernel.
+ * 1 = off (the default: it helps only small N, DART_ATTN_SPLIT sets the process default).
+ * Process wide; tests and A/B measurement. */
+void dart_attention_kv_split(int32_t k);
+
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */
 int64_t dart_launch_count(const dart_model* m);

@@ -61,6 +61,7 @@ EXPORTS = (
     "dart_gemm_force_splitk",
     "dart_set_pdl",
     "dart_set_ln_fold",
+    "dart_attention_kv_split",
     "dart_gemm_force_precision",
     "dart_attention_force_safe",
     "dart_attention_trace",
@@ -217,6 +218,8 @@ def load() -> ctypes.CDLL:
     lib.dart_set_pdl.restype = None
     lib.dart_set_ln_fold.argtypes = [I32]
     lib.dart_set_ln_fold.restype = None
+    lib.dart_attention_kv_split.argtypes = [I32]
+    lib.dart_attention_kv_split.restype = None
     lib.dart_gemm_force_precision.argtypes = [I32]
     lib.dart_gemm_force_precision.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,

@@ -115,8 +115,11 @@ int g_splitk_mask = getenv("DART_SPLITK") ? atoi(getenv("DART_SPLITK")) : 0;
 // statistics more than the LayerNorm pass it replaces costs.  The folded weights exist only in
 // handles created while the fold is enabled (DART_LN_FOLD=<mask> or dart_set_ln_fold).
 int g_ln_fold = getenv("DART_LN_FOLD") ? atoi(getenv("DART_LN_FOLD")) : 0;
-// split-KV factor of the decoder cross-attention (xattn); DART_ATTN_SPLIT=<k> overrides, <= 1: off (A/B)
-int g_attn_split = getenv("DART_ATTN_SPLIT") ? atoi(getenv("DART_ATTN_SPLIT")) : 2;
+// split-KV factor of the decoder cross-attention (xattn); DART_ATTN_SPLIT=<k>, <= 1: off.  Off by
+// default: 2-way saves 40 us per N=4 step (128 items for 296 CTA slots) but costs ~0.5 ms per N=80
+// step (partials + merge where the items already fill the GPU), and a split that depended on N
+// would break the bitwise batch invariance of a class's rows (profiles/r02/attn_hd16_chains.log).
+int g_attn_split = getenv("DART_ATTN_SPLIT") ? atoi(getenv("DART_ATTN_SPLIT")) : 1;
 int g_gemm_splitk = 1;  // dart_gemm_force_splitk (kernel-level tests)
 int g_gemm_precision = 0;  // dart_gemm_force_precision (kernel-level tests)
 int g_fused_mlp = getenv("DART_NO_FUSED_MLP") == nullptr;  // enc-dec MLP on the fused kernel
@@ -699,11 +702,11 @@ int xattn(dart_model* m, float* x, const LNW& ln, const AttnW& w, const XAttnSpe
       m->launches++;
       RUN(attn_tc(q, D, 0, kv, 2 * D, 0, D, o, D, sp.items, H, sp.Lq, Lk, hd, m->num_sms, s));
     } else {
-      // split-KV for the decoder cross-attention (201 queries over T = 5184 keys): at small N its
-      // (q tile, head, class) items leave most CTA slots idle (4 classes: 2 x 16 x 4 = 128 items
-      // for 296 slots, each over 54 key tiles), so every item's key range runs on g_attn_split
-      // CTAs and is merged.  The split does not depend on N, so a class's rows stay bitwise
-      // independent of the batch
+      // split-KV for the decoder cross-attention (201 queries over T = 5184 keys; g_attn_split,
+      // off by default): at small N its (q tile, head, class) items leave most CTA slots idle
+      // (4 classes: 2 x 16 x 4 = 128 items for 296 slots, each over 54 key tiles); when enabled
+      // every item's key range runs on g_attn_split CTAs and is merged.  The factor does not
+      // depend on N, so a class's rows stay bitwise independent of the batch
       const int ks = (hd == 16 && Lk >= 1024 && g_attn_split > 1) ? g_attn_split : 1;
       if (ks > 1) {
         const size_t need = (size_t)sp.items * H * ks * sp.Lq * 20;
@@ -1392,6 +1395,7 @@ int dart_layernorm(const float* x, const float* gamma, const float* beta, void* 
 void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 void dart_set_pdl(int32_t mode) { pdl_set_thread(mode); }
 void dart_set_ln_fold(int32_t on) { g_ln_fold = on & 3; }
+void dart_attention_kv_split(int32_t k) { g_attn_split = k < 1 ? 1 : k > 8 ? 8 : k; }
 void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
 int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,

@@ -12,12 +12,14 @@ from paper_2603_11441_b200 import _native
 lib = _native.load()
 st = torch.cuda.current_stream()
 ev = ["mma issued", "acc ready", "part stored", "published", "comb wait0", "part visible", "epi done"]
-for label, M, N, K, epi in (("attn.out", 5184, 1280, 1280, 3), ("mlp.fc2", 5184, 1280, 5120, 3)):
+SPLITS = [int(a) for a in sys.argv[1:]] or [1, 2]
+for label, M, N, K, epi in (("attn.out", 5184, 1280, 1280, 3), ("mlp.fc2", 5184, 1280, 5120, 3),
+                            ("mlp.fc1", 5184, 5120, 1280, 1), ("epi-only K=64", 5184 * 4, 1280, 64, 0)):
     A = torch.randn(M, K, device="cuda").half()
     W = (torch.randn(N, K, device="cuda") / K ** 0.5).half()
     bias = torch.zeros(N, device="cuda")
-    out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-    for sk in (1, 2):
+    out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi == 3 else torch.float16)
+    for sk in SPLITS:
         lib.dart_gemm_force_splitk(sk)
         tr = torch.zeros(148 * 8 + 148 * 64, dtype=torch.int64, device="cuda")
         f = lambda: _native.check(lib.dart_gemm(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), None, M, N,

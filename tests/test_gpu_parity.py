@@ -321,6 +321,34 @@ def test_full_width_parity(name, fold):
     assert frac == 1.0  # every decision of B and C is decidable at the measured error levels
 
 
+@pytest.mark.parametrize("ks", [2, 3])
+def test_decoder_cross_attention_split_kv(ks):
+    """Split-KV decoder cross-attention (dart_attention_kv_split: each item's 5184 keys on ks CTAs,
+    partial O / row sum / reference max merged): golden B's raw outputs stay within B's gates and
+    within fp16-rounding distance of the unsplit path, with every decision identical."""
+    from paper_2603_11441_b200 import _native
+
+    g = load_golden("B")
+    model = model_for(g)
+    image = scene_for("B", model.config)
+    names = [str(n) for n in g["names"]]
+    fpn = D.backbone_forward(model, image)
+    text = D.text_encode(model, names).stack(names)
+    lib = _native.load()
+    raw0 = D.encdec_forward(model, fpn, text)
+    lib.dart_attention_kv_split(ks)
+    try:
+        raw = D.encdec_forward(model, fpn, text)
+    finally:
+        lib.dart_attention_kv_split(1)
+    err_b, err_s, err_p = raw_errors(g, raw)
+    te, tb, ts, tp = TOL["B"]
+    assert err_b < tb and err_s < ts and err_p < tp
+    assert check_decisions(g, raw, err_s, err_p, err_b) == 1.0
+    assert np.abs(raw.score_logits - raw0.score_logits).max() < 1e-3
+    assert not np.array_equal(raw.score_logits, raw0.score_logits)  # the split path actually ran
+
+
 def hashlib_image(img):
     import hashlib
 
