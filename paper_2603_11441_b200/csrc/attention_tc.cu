@@ -492,7 +492,9 @@ __global__ void __launch_bounds__(FaCfg<HD, BKV, STAGES, CTAS, NS, SPLIT, QT>::T
   #pragma unroll
               for (int i = 0; i < L::COLS / 2; ++i) {
                 float x0, x1;
-                if ((i & 7) < NPOLY / 2) {  // NPOLY of every 16 exponentials on the FMA pipe
+                // NPOLY of every 16 exponentials on the FMA pipe (the first NPOLY / 2 pairs of every 8);
+                // NPOLY >= 256 (placement search, attention_search.inc): pair i iff bit (i & 7) of NPOLY - 256
+                if (NPOLY >= 256 ? ((NPOLY - 256) >> (i & 7)) & 1 : (i & 7) < NPOLY / 2) {
                   exp2_poly2_sat(v[2 * i], v[2 * i + 1], cr, br, x0, x1);
                 } else {
                   f2_unpack(ffma2(f2_pack(v[2 * i], v[2 * i + 1]), c2, nb2), x0, x1);
@@ -699,11 +701,18 @@ int fa_variant() {
 // (11.4 / 14.0 ms): the extra per-tile softmax work outweighed the decoupling.  A decoupled
 // variant at 96-key tiles (2 S buffers | one P buffer | O without the ones block, row sums in
 // registers; git history "fa_dec_kernel") was correct but also slower: N=20 2.67-2.78 vs 2.41 ms.
+#ifdef DART_FA_SEARCH
+#include "attention_search.inc"
+#else
+#define DART_FA16_SEARCH_VARIANTS(X)
+#endif
+
 int kv_tile_of(int hd, int var) {
 #define X(V, HD, BKV, ST, CT, NS, SP, NP, SN, LN, QT) \
   if (hd == HD && var == V) return BKV;
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
+  DART_FA16_SEARCH_VARIANTS(X)
 #undef X
   if (hd == 80) return 64;
   if (hd == 16) return 96;
@@ -795,6 +804,7 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
                        : launch_v<HD, BKV, ST, CT, NS, SP, NP, SN, LN, false, QT>(tmQ, tmKV, a, num_sms, stream);
   DART_FA80_VARIANTS(X)
   DART_FA16_VARIANTS(X)
+  DART_FA16_SEARCH_VARIANTS(X)
 #undef X
   // the production instantiations (SPIN bit 4) carry no debug / trace / microbenchmark hooks;
   // a launch that asks for one of them runs the hooked twin (identical arithmetic)
