@@ -170,3 +170,58 @@ def test_native_unpack_owner_arithmetic_matches_plan():
                 start = owner * base + min(owner, extra)
                 s, e = plan.bounds(owner)
                 assert s == start and s <= cls < e and cls - start < plan.width
+
+
+class _FakeEvent:
+    def __init__(self, done_after):
+        self.n, self.done_after = 0, done_after
+
+    def query(self):
+        self.n += 1
+        return self.n > self.done_after
+
+
+class _FakeLib:
+    """dart_nccl_comm_check / _abort stand-ins: the communicator fails after `fail_after` checks."""
+
+    def __init__(self, fail_after=None):
+        self.checks, self.aborted, self.fail_after = 0, False, fail_after
+
+    def dart_nccl_comm_check(self, ptr):
+        self.checks += 1
+        return 2 if self.aborted or (self.fail_after is not None and self.checks > self.fail_after) else 0
+
+    def dart_nccl_comm_abort(self, ptr):
+        self.aborted = True
+        return 0
+
+    def dart_last_error(self):
+        return b"NCCL asynchronous error: remote process exited"
+
+
+def _comm(lib):
+    from paper_2603_11441_b200.distributed import NcclComm
+
+    c = NcclComm.__new__(NcclComm)
+    c.lib, c.ptr, c.world, c.rank = lib, 1, 2, 0
+    return c
+
+
+def test_nccl_wait_completes_aborts_on_error_and_times_out(monkeypatch):
+    """NcclComm.wait (SURVEY section 5 failure detection): returns once the round's event completes
+    while the communicator stays healthy; an asynchronous NCCL error or the timeout aborts the
+    communicator (releasing ranks blocked in collectives) and raises RuntimeError."""
+    from paper_2603_11441_b200 import _native
+
+    monkeypatch.setattr(_native, "load", lambda: _FakeLib())
+    ok = _FakeLib()
+    _comm(ok).wait(_FakeEvent(3), timeout_s=10.0, poll_s=0.0)
+    assert not ok.aborted and ok.checks >= 3
+    bad = _FakeLib(fail_after=2)
+    with pytest.raises(RuntimeError, match="failed"):
+        _comm(bad).wait(_FakeEvent(10 ** 9), timeout_s=10.0, poll_s=0.0)
+    assert bad.aborted
+    slow = _FakeLib()
+    with pytest.raises(RuntimeError, match="timed out"):
+        _comm(slow).wait(_FakeEvent(10 ** 9), timeout_s=0.05, poll_s=0.001)
+    assert slow.aborted
