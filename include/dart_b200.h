@@ -267,6 +267,12 @@ void dart_set_ln_fold(int32_t mask);
  * Process wide; tests and A/B measurement. */
 void dart_attention_kv_split(int32_t k);
 
+/* Row-block dependency chain inside dart_backbone (fc1 -> fc2 -> next LN1 -> QKV start on the row
+ * blocks their producer finished, in its last wave): 1 = on, 0 = off (the default: measured no
+ * faster; DART_CHAIN sets the process default).  Results are bitwise identical either way.
+ * Process wide; tests and A/B measurement. */
+void dart_set_chain(int32_t on);
+
 /* Kernel launches issued by the last dart_backbone + dart_encdec + dart_postprocess calls
  * on this handle (for the bench's gpu_launches evidence). */
 int64_t dart_launch_count(const dart_model* m);

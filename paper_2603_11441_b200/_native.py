@@ -62,6 +62,7 @@ EXPORTS = (
     "dart_set_pdl",
     "dart_set_ln_fold",
     "dart_attention_kv_split",
+    "dart_set_chain",
     "dart_gemm_force_precision",
     "dart_attention_force_safe",
     "dart_attention_trace",
@@ -220,6 +221,8 @@ def load() -> ctypes.CDLL:
     lib.dart_set_ln_fold.restype = None
     lib.dart_attention_kv_split.argtypes = [I32]
     lib.dart_attention_kv_split.restype = None
+    lib.dart_set_chain.argtypes = [I32]
+    lib.dart_set_chain.restype = None
     lib.dart_gemm_force_precision.argtypes = [I32]
     lib.dart_gemm_force_precision.restype = None
     lib.dart_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, ctypes.c_int64,

@@ -115,6 +115,13 @@ int g_splitk_mask = getenv("DART_SPLITK") ? atoi(getenv("DART_SPLITK")) : 0;
 // statistics more than the LayerNorm pass it replaces costs.  The folded weights exist only in
 // handles created while the fold is enabled (DART_LN_FOLD=<mask> or dart_set_ln_fold).
 int g_ln_fold = getenv("DART_LN_FOLD") ? atoi(getenv("DART_LN_FOLD")) : 0;
+// Row-block dependency chain fc1 -> fc2 -> LN1(next block) -> QKV inside the backbone (GemmEpi::dep_*):
+// each consumer starts on the 128-row blocks its producer has finished, in the SMs the producer's
+// last wave leaves idle.  Correct (parity B / C, batch invariance) but not faster: serial step
+// -0.5%, inter-frame pipeline -1 to -2% (the store-completion waits behind each signal and the
+// chain LayerNorm's fences cost what the overlap saves; profiles/r02/chain_ab.log).  Off by default;
+// DART_CHAIN=1 turns it on (A/B).
+int g_chain = getenv("DART_CHAIN") ? atoi(getenv("DART_CHAIN")) : 0;
 // split-KV factor of the decoder cross-attention (xattn); DART_ATTN_SPLIT=<k>, <= 1: off.  Off by
 // default: 2-way saves 40 us per N=4 step (128 items for 296 CTA slots) but costs ~0.5 ms per N=80
 // step (partials + merge where the items already fill the GPU), and a split that depended on N
@@ -278,6 +285,7 @@ struct dart_model {
     float2* lnst;  // LN fold: per-row chunk statistics of x [rows, E / 32] (h holds fp16(x))
     float2* lnfin;  // LN fold: per-row (mean, rstd) of x [rows]
     int* lncnt;     // LN fold: chunk counters per 32-row group [rows / 32] (zeroed at allocation)
+    int* chain;     // row-block dependency chain counters [3][rows / 128 + 1]: fc1, fc2, LN1 (zeroed)
   } bb{};
   struct {
     float *e1, *e, *qd, *qd0, *qf;
@@ -289,6 +297,10 @@ struct dart_model {
   int precision = 0;
   bool in_backbone = false;  // set while a backbone stage issues its GEMMs
   bool x16_valid = false;    // LN fold: bb.h holds fp16 of the backbone residual stream (last producer)
+  // row-block dependency chain (bb_blocks): rows the counters were last used for, and the number of
+  // completed signalling launches per counter array (the cumulative targets)
+  int chain_rows = -1;
+  int chain_epoch[3] = {0, 0, 0};
   // split-K claim flags and partial accumulators, per handle (a fork gets its own)
   int* splitk_flags = nullptr;
   long long splitk_cap = 0;  // flags
@@ -583,9 +595,12 @@ int ensure_backbone_ws(dart_model* m, int B) {
   m->bb.lnst = (float2*)w.get(rows * (E / 32) * sizeof(float2));
   m->bb.lnfin = (float2*)w.get(rows * sizeof(float2));
   m->bb.lncnt = (int*)w.get((rows / 32 + 1) * sizeof(int));
+  m->bb.chain = (int*)w.get(3 * (rows / 128 + 1) * sizeof(int));
+  m->chain_rows = -1;  // counters zeroed below; the first chained call starts the epochs
   if (!m->bb.patches || !m->bb.x || !m->bb.h || !m->bb.qkv || !m->bb.ao || !m->bb.hid || !m->bb.pool1 ||
-      !m->bb.pool2 || !m->bb.l0h || !m->bb.lnst || !m->bb.lnfin || !m->bb.lncnt ||
+      !m->bb.pool2 || !m->bb.l0h || !m->bb.lnst || !m->bb.lnfin || !m->bb.lncnt || !m->bb.chain ||
       cudaMemset(m->bb.lncnt, 0, (rows / 32 + 1) * sizeof(int)) != cudaSuccess ||
+      cudaMemset(m->bb.chain, 0, 3 * (rows / 128 + 1) * sizeof(int)) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess) {  // counters zero before any stream uses them
     m->bb_ws.release();
     m->bb_cap = 0;
@@ -1022,11 +1037,38 @@ int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* att
     e.ln_stats = w.lnfin;
     e.ln_colsum = Wf.colsum;
   };
+  // row-block dependency chain (g_chain): fc1 -> fc2 -> LN1 of the next block -> its QKV, for blocks
+  // that run both sub-blocks on the model's own enable flags in the detection discipline
+  const bool chain = g_chain && !fold && m->precision == 0 && E == 1280 && !attn_on && !mlp_on && x == w.x;
+  const int nblk = rows / 128 + 1;
+  int* const c_fc1 = w.chain;
+  int* const c_fc2 = w.chain + nblk;
+  int* const c_ln = w.chain + 2 * nblk;
+  int* const ep = m->chain_epoch;
+  if (chain && m->chain_rows != rows) {  // counters are cumulative per row-block layout
+    if (cudaMemsetAsync(w.chain, 0, 3 * nblk * sizeof(int), s) != cudaSuccess) return fail(DART_ERR_CUDA, "chain reset");
+    m->chain_rows = rows;
+    ep[0] = ep[1] = ep[2] = 0;
+  }
+  auto chained = [&](int blk) { return chain && m->d.attn_enabled[blk] && m->d.mlp_enabled[blk]; };
+  bool fc2_signalled = false;  // the previous block's fc2 counts its row blocks into c_fc2
   for (int b = b0; b < b1; ++b) {
     const BlockW& bw = m->blocks[b];
     if (attn_on ? attn_on[b] : m->d.attn_enabled[b]) {
-      if (!(fold & 1)) LAUNCH(layernorm_f32_to_f16(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
       GemmEpi e = epi_out(w.qkv, 3 * E);
+      if (chained(b)) {  // LN1 row by row as fc2 finishes its rows; QKV block by block as LN1 does
+        LAUNCH(layernorm_f32_to_f16_chain(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, fc2_signalled ? c_fc2 : nullptr,
+                                          ep[1] * (E / 8), c_ln, s));
+        ++ep[2];
+        e.dep_wait = c_ln;
+        e.dep_mult = ep[2];
+        e.dep_per_row = 1;
+        e.skip_pdl_wait = 1;
+        e.force_pdl = 1;
+      } else if (!(fold & 1)) {
+        LAUNCH(layernorm_f32_to_f16(x, bw.ln1.g, bw.ln1.b, w.h, rows, E, E, E, s));
+      }
+      fc2_signalled = false;
       if (fold & 1) folded_in(e, bw.qkv_f);
       e.rope_cos = m->rope_cos;
       e.rope_sin = m->rope_sin;
@@ -1069,8 +1111,30 @@ int bb_blocks(dart_model* m, float* x, int B, int b0, int b1, const int32_t* att
         folded_in(e, bw.fc1_f);
       else
         LAUNCH(layernorm_f32_to_f16(x, bw.ln2.g, bw.ln2.b, w.h, rows, E, E, E, s));
-      RUN(gemm(m, w.h, rows, E, (fold & 2) ? bw.fc1_f : bw.fc1, EPI_F16_RELU, e, s));
-      RUN(resid(w.hid, 4 * E, bw.fc2, 1));
+      fc2_signalled = false;
+      if (chained(b)) {  // fc1 counts its finished row blocks; fc2 starts on them in fc1's last wave
+        e.dep_signal = c_fc1;
+        e.early_trigger = 1;
+        RUN(gemm(m, w.h, rows, E, bw.fc1, EPI_F16_RELU, e, s));
+        ++ep[0];
+        GemmEpi e2 = epi_out(x, E);
+        e2.dep_wait = c_fc1;
+        e2.dep_mult = ep[0] * (4 * E / 8);
+        e2.skip_pdl_wait = 1;
+        e2.force_pdl = 1;
+        if (b + 1 < b1 && chained(b + 1)) {  // the next block's LN1 starts on fc2's finished rows
+          e2.dep_signal = c_fc2;
+          e2.early_trigger = 1;
+        }
+        RUN(gemm(m, w.hid, rows, 4 * E, bw.fc2, EPI_F32_RESID, e2, s));
+        if (e2.dep_signal) {
+          ++ep[1];
+          fc2_signalled = true;
+        }
+      } else {
+        RUN(gemm(m, w.h, rows, E, (fold & 2) ? bw.fc1_f : bw.fc1, EPI_F16_RELU, e, s));
+        RUN(resid(w.hid, 4 * E, bw.fc2, 1));
+      }
     }
   }
   return DART_OK;
@@ -1396,6 +1460,7 @@ void dart_gemm_force_splitk(int32_t s) { g_gemm_splitk = s == 2 ? 2 : 1; }
 void dart_set_pdl(int32_t mode) { pdl_set_thread(mode); }
 void dart_set_ln_fold(int32_t on) { g_ln_fold = on & 3; }
 void dart_attention_kv_split(int32_t k) { g_attn_split = k < 1 ? 1 : k > 8 ? 8 : k; }
+void dart_set_chain(int32_t on) { g_chain = on != 0; }
 void dart_gemm_force_precision(int32_t p) { g_gemm_precision = p >= 0 && p <= 2 ? p : 0; }
 
 int dart_mlp_fused_ln(const void* h, const void* w1, const float* b1, const void* w2, const float* b2, float* x,

@@ -469,7 +469,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) GEMM_STAMP(0);
-  pdl_wait();  // the previous kernel's outputs (our A / residual) are complete from here on
+  // the previous kernel's outputs (our A / residual) are complete from here on -- or, in a
+  // row-block dependency chain (GemmEpi::dep_wait), per 128-row block as the producer sees them
+  if (!epi.skip_pdl_wait) pdl_wait();
+  if (epi.early_trigger) pdl_launch_dependents();
   if (threadIdx.x == 0) GEMM_STAMP(1);
 
   if (warp == 0) {
@@ -477,6 +480,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // kernel parameters read inside the loops are hoisted: after every asm "memory" clobber
       // (barrier waits, TMA) a parameter is otherwise re-loaded from the constant bank
       const bool noload = epi.dbg_noload != 0;
+      const int* const dep_wait = epi.dep_wait;
+      const int dep_mult = epi.dep_mult, dep_per_row = epi.dep_per_row;
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = cl; unit < num_units; unit += ncl) {
@@ -485,6 +490,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int kb0 = kh * nk;
         const bool hu = nh >= 0;
         const int m0 = (tile / num_n) * BM * CG + rank * BM;
+        if (dep_wait != nullptr && m0 < M) {  // dependency chain: this CTA's 128 A rows are complete
+          const int rows_blk = M - m0 < BM ? M - m0 : BM;
+          const int target = dep_mult * (dep_per_row ? rows_blk : 1);
+          long long spins = 0;
+          while (*reinterpret_cast<const volatile int*>(dep_wait + (m0 >> 7)) < target) {
+            __nanosleep(256);
+            if (++spins > (1ll << 25)) __trap();  // a broken chain fails loudly instead of hanging
+          }
+          __threadfence();
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA reads below see the rows
+        }
         const int n0 = (tile % num_n) * BN + (hu ? nh * (BN / 2) + rank * (L::B_ROWS / 2) : rank * L::B_ROWS);
         const CUtensorMap* mb = hu ? &tmB2 : &tmB;
         const uint32_t bytes = hu ? L::A_BYTES + L::B_BYTES / 2 : L::STAGE_BYTES;
@@ -840,6 +856,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_arrive_leader(&tempty[acc]);
           }
         }
+      }
+      // dependency chain: this warp's rows of the unit are stored (CTAs wholly past M -- the second
+      // CTA of a pair tile over the last, partial row block -- have no rows to announce)
+      if (epi.dep_signal != nullptr && (row0 & ~127) < M) {
+        if (lane == 0) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(epi.dep_signal + (row0 >> 7), (bn_eff - half * 32 + 63) / 64);
+        }
+        __syncwarp();
       }
       if constexpr (L::X16 || EPI == EPI_F32_F16) {
         if (ln_stats_out != nullptr) {  // LN statistics: the warp completing a 32-row group finalises it
@@ -1198,7 +1225,7 @@ int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap&
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (pdl_enabled()) pdl_attr(attr[na++]);
+  if (pdl_enabled() || epi.force_pdl) pdl_attr(attr[na++]);
   cfg.attrs = attr;
   cfg.numAttrs = na;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tA, tB, tB2, tC, tD, M, N, K, epi);

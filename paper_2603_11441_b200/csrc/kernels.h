@@ -82,6 +82,26 @@ struct GemmEpi {
   const float2* ln_stats = nullptr;
   const float* ln_colsum = nullptr;
   int ln_parts = 0;  // 32-column chunks per row (E / 32)
+  // Row-block dependency chain across kernel boundaries (backbone fc1 -> fc2 -> LN1 -> QKV): instead
+  // of waiting for the whole previous grid (griddepcontrol.wait), a consumer starts on the rows
+  // whose producer tiles are done, so it fills the SMs the producer's last wave leaves idle.
+  //   dep_signal: after a unit's stores complete, each epilogue warp adds the number of 32-column
+  //     chunks it wrote to dep_signal[row / 128] (a 128-row block is complete when its counter
+  //     gains N / 8).
+  //   dep_wait: before loading the A rows [m0, m0 + 128) of a unit the producer waits until
+  //     dep_wait[m0 / 128] >= dep_mult * (dep_per_row ? rows of that block in [0, M) : 1).
+  //   early_trigger: griddepcontrol.launch_dependents right after this kernel's own wait, so the
+  //     next kernel's CTAs take the SMs this grid's CTAs free.  skip_pdl_wait: no griddepcontrol
+  //     .wait (every input other than the dep_wait rows is complete before the launch);
+  //     force_pdl: launched with programmatic stream serialization whatever dart_set_pdl says.
+  // Counters are cumulative (dep_mult grows by one chain epoch per use), so nothing resets them.
+  int* dep_signal = nullptr;
+  const int* dep_wait = nullptr;
+  int dep_mult = 0;
+  int dep_per_row = 0;
+  int early_trigger = 0;
+  int skip_pdl_wait = 0;
+  int force_pdl = 0;
 };
 
 // window-major row index <-> token index within one image
@@ -183,6 +203,11 @@ int attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const AttnTcAr
                  cudaStream_t stream);
 
 // Row kernels.
+// LayerNorm in a row-block dependency chain (see GemmEpi::dep_*): wait_cnt == nullptr: full wait on the
+// previous grid; else row r waits until wait_cnt[r / 128] >= wait_target.  Each finished row adds 1 to
+// sig_cnt[r / 128]; the kernel triggers its dependents as soon as it starts.
+int layernorm_f32_to_f16_chain(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
+                               const int* wait_cnt, int wait_target, int* sig_cnt, cudaStream_t stream);
 int layernorm_f32_to_f16(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
                          int ld_in, int ld_out, cudaStream_t stream);
 int layernorm_f32_to_f32(const float* x, const float* gamma, const float* beta, float* y, int rows, int dim,

@@ -83,6 +83,77 @@ __global__ void layernorm_vec_kernel(const float* __restrict__ x, const float* _
   }
 }
 
+// One warp per row of a row-block dependency chain (GemmEpi::dep_*): the row's 128-row block must
+// be complete in wait_cnt before x is read; the finished row is counted in sig_cnt.
+template <int VPL>
+__device__ __forceinline__ void layernorm_chain_rows(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, __half* __restrict__ y,
+                                                     int rows, const int* wait_cnt, int wait_target) {
+  if (wait_cnt == nullptr) pdl_wait();
+  pdl_launch_dependents();  // the consumer (QKV) may take SMs as this grid's CTAs free them
+  constexpr int V4 = VPL / 4, DIM = 32 * VPL;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wait_cnt != nullptr) {  // one poller per CTA: its rows (a multiple of 8 apart) share a 128-row block
+    if (threadIdx.x == 0) {
+      const int blk = (blockIdx.x * (blockDim.x >> 5)) >> 7;
+      long long spins = 0;
+      while (*reinterpret_cast<const volatile int*>(wait_cnt + blk) < wait_target) {
+        __nanosleep(512);
+        if (++spins > (1ll << 24)) __trap();  // a broken chain fails loudly instead of hanging
+      }
+    }
+    __syncthreads();
+    __threadfence();
+  }
+  if (row >= rows) return;  // (no barrier follows inside: the caller's __syncthreads sees every warp)
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * DIM);
+  float4 v[V4];
+#pragma unroll
+  for (int i = 0; i < V4; ++i) v[i] = __ldcg(xr + 32 * i + lane);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  const float mu = s * (1.0f / DIM);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
+    q += (a * a + b * b) + (c * c + d * d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  const float rstd = 1.0f / sqrtf(q * (1.0f / DIM) + LN_EPS);
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float4* b4 = reinterpret_cast<const float4*>(beta);
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const float4 g = __ldg(g4 + 32 * i + lane), b = __ldg(b4 + 32 * i + lane);
+    const float4 w = v[i];
+    const float r0 = (w.x - mu) * rstd * g.x + b.x, r1 = (w.y - mu) * rstd * g.y + b.y;
+    const float r2 = (w.z - mu) * rstd * g.z + b.z, r3 = (w.w - mu) * rstd * g.w + b.w;
+    reinterpret_cast<uint2*>(y + (size_t)row * DIM)[32 * i + lane] = make_uint2(pack_half2(r0, r1), pack_half2(r2, r3));
+  }
+}
+
+// the CTA's rows are announced together: barrier, then one device-scope fence + atomic (the
+// grid-sync pattern: the barrier orders every warp's stores before thread 0's fence)
+template <int VPL>
+__global__ void layernorm_chain_kernel_cta(const float* __restrict__ x, const float* __restrict__ gamma,
+                                           const float* __restrict__ beta, __half* __restrict__ y, int rows,
+                                           const int* wait_cnt, int wait_target, int* sig_cnt) {
+  layernorm_chain_rows<VPL>(x, gamma, beta, y, rows, wait_cnt, wait_target);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int row0 = blockIdx.x * (blockDim.x >> 5);
+    const int n = rows - row0 < (int)(blockDim.x >> 5) ? rows - row0 : (int)(blockDim.x >> 5);
+    __threadfence();
+    if (n > 0) atomicAdd(sig_cnt + (row0 >> 7), n);
+  }
+}
+
 template <int VPL, typename OutT>
 __global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                  const float* __restrict__ beta, OutT* __restrict__ y, int rows, int ld_in,
@@ -302,6 +373,23 @@ inline int grid_for(long long n, int threads = 256) {
 }
 
 }  // namespace
+
+int layernorm_f32_to_f16_chain(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
+                               const int* wait_cnt, int wait_target, int* sig_cnt, cudaStream_t stream) {
+  if (rows <= 0) return 0;
+  if (dim != 1280 || sig_cnt == nullptr) return (int)cudaErrorInvalidValue;
+  constexpr int warps = 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((rows + warps - 1) / warps);
+  cfg.blockDim = dim3(warps * 32);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  pdl_attr(attr[0]);  // always: the chain relies on launching into the producer's tail
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, layernorm_chain_kernel_cta<40>, x, gamma, beta, y, rows, wait_cnt, wait_target, sig_cnt);
+  return (int)cudaGetLastError();
+}
 
 int layernorm_f32_to_f16(const float* x, const float* gamma, const float* beta, __half* y, int rows, int dim,
                          int ld_in, int ld_out, cudaStream_t stream) {

@@ -321,6 +321,33 @@ def test_full_width_parity(name, fold):
     assert frac == 1.0  # every decision of B and C is decidable at the measured error levels
 
 
+def test_backbone_row_block_chain_is_bitwise_neutral():
+    """The row-block dependency chain (dart_set_chain: fc1 -> fc2 -> next LN1 -> QKV launched into their
+    producer's last wave, synchronised per 128-row block by counters) changes only when each row block
+    is computed, never the arithmetic: the full ViT-H/14 features are bitwise equal with and without
+    it, over several calls (cumulative counters) and a 2-image batch."""
+    from paper_2603_11441_b200 import _native
+
+    g = load_golden("C")
+    model = model_for(g)
+    image = scene_for("C", model.config)
+    img2 = D.generate_scene(D.SceneSpec(seed=7, image_size=1008, num_classes=4))[0]
+    lib = _native.load()
+    ref = D.backbone_forward(model, image).levels
+    ref2, _ = D.model.backbone_forward_batch(model, np.stack([image, img2]))
+    lib.dart_set_chain(1)
+    try:
+        for _ in range(3):
+            got = D.backbone_forward(model, image).levels
+            for a, b in zip(got, ref):
+                np.testing.assert_array_equal(a, b)
+        got2, _ = D.model.backbone_forward_batch(model, np.stack([image, img2]))
+        for a, b in zip(got2, ref2):
+            assert torch.equal(a, b)
+    finally:
+        lib.dart_set_chain(0)
+
+
 @pytest.mark.parametrize("ks", [2, 3])
 def test_decoder_cross_attention_split_kv(ks):
     """Split-KV decoder cross-attention (dart_attention_kv_split: each item's 5184 keys on ks CTAs,
