@@ -267,9 +267,10 @@ class Detector:
         # attention CTAs fill the first one's last waves (N=4: +3-4% over n = 1; n = 3, 4 no
         # better).  DART_PIPE_BB overrides n (A/B measurement).
         nbb = max(1, int(os.environ.get("DART_PIPE_BB", "2")))
-        # DART_PIPE_PRIORITY=1: the backbone stream (the pipeline's critical path) gets the
-        # higher CUDA stream priority (A/B measurement)
-        prio = -1 if os.environ.get("DART_PIPE_PRIORITY") else 0
+        # DART_PIPE_PRIORITY=1: the backbone streams get the higher CUDA stream priority, =2: the
+        # decode stream does (A/B measurement)
+        prio_mode = int(os.environ.get("DART_PIPE_PRIORITY", "0") or 0)
+        prio = -1 if prio_mode == 1 else 0
         s_bbs = [torch.cuda.Stream(device=self.device, priority=prio) for _ in range(nbb)]
         p = {
             "B": B,
@@ -279,7 +280,7 @@ class Detector:
             "h_bb": [self.handle] + [self.handle.fork() for _ in range(nbb - 1)],
             "s_bbs": s_bbs,
             "s_bb": s_bbs[0],
-            "s_dec": torch.cuda.Stream(device=self.device),
+            "s_dec": torch.cuda.Stream(device=self.device, priority=-1 if prio_mode == 2 else 0),
             "slots": [self._alloc_slot(B) for _ in range(nbb + 1)],
             "ev_bb": [torch.cuda.Event() for _ in range(nbb + 1)],
             "ev_dec": [None] * (nbb + 1),
