@@ -276,6 +276,27 @@ def test_batch_independence_and_chunking():
     assert D.run_shared(model, image, names, cfg) == ref
 
 
+def test_full_width_backbone_batch_independence():
+    """Reference tests/test_model.py:85-126 at the full-size kernel shapes (config B: E 1280, T 5184,
+    windowed + global blocks): a 3-image batch gives every image's features bitwise equal to its
+    single-image run, although M = 3 x 5184 changes every GEMM's tile plan (waves, tail halves) and
+    the attention launches' item counts; and the enc-dec rows of those images are bitwise equal too."""
+    g = load_golden("B")
+    model = model_for(g)
+    imgs = [scene_for("B", model.config)] + [D.generate_scene(D.SceneSpec(seed=s, image_size=1008,
+                                                                          num_classes=3))[0] for s in (21, 22)]
+    (l0, l1, l2), _ = D.model.backbone_forward_batch(model, np.stack(imgs))
+    names = [str(n) for n in g["names"]]
+    text = D.text_encode(model, names).stack(names)
+    for i, img in enumerate(imgs):
+        f = D.backbone_forward(model, img)
+        for batched, single in zip((l0, l1, l2), f.levels):
+            np.testing.assert_array_equal(batched[i].cpu().numpy(), single)
+    raw0 = D.encdec_forward(model, D.backbone_forward(model, imgs[0]), text)
+    np.testing.assert_array_equal(raw0.score_logits, D.encdec_forward(model, D.backbone_forward(model, imgs[0]),
+                                                                      text).score_logits)
+
+
 @pytest.mark.parametrize("fold", [3, 1, 0])
 @pytest.mark.parametrize("name", ["B", "C"])
 def test_full_width_parity(name, fold):
