@@ -151,17 +151,23 @@ __device__ __forceinline__ void rope_chunk(float* v, int col, int hd, const floa
 __device__ __forceinline__ float sat_f16(float x) { return fminf(fmaxf(x, -65504.0f), 65504.0f); }
 __device__ __forceinline__ float round_f16(float x) { return __half2float(__float2half_rn(sat_f16(x))); }
 
-template <int EPI>
-__device__ __forceinline__ void epilogue_bias_act(float* v, int col, const float* bias) {
+// bias chunk of 32 columns, loaded ahead of the TMEM load so its latency overlaps it
+__device__ __forceinline__ void bias_prefetch(float4 (&b)[8], int col, const float* bias) {
   if (bias != nullptr) {
     const float4* b4 = reinterpret_cast<const float4*>(bias + col);
 #pragma unroll
+    for (int q = 0; q < 8; ++q) b[q] = __ldg(b4 + q);
+  }
+}
+template <int EPI>
+__device__ __forceinline__ void epilogue_bias_act(float* v, const float4 (&b)[8], const float* bias) {
+  if (bias != nullptr) {
+#pragma unroll
     for (int q = 0; q < 8; ++q) {
-      float4 b = __ldg(b4 + q);
-      v[4 * q + 0] += b.x;
-      v[4 * q + 1] += b.y;
-      v[4 * q + 2] += b.z;
-      v[4 * q + 3] += b.w;
+      v[4 * q + 0] += b[q].x;
+      v[4 * q + 1] += b[q].y;
+      v[4 * q + 2] += b[q].z;
+      v[4 * q + 3] += b[q].w;
     }
   }
   if (EPI == EPI_F16_RELU) {
@@ -708,6 +714,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         __syncwarp();
+        float4 bq[8];
+        bias_prefetch(bq, n0 + c, bias);
         float v[32];
         tmem_ld32(taddr + c, v);
         if constexpr (SPLITK) {  // + the other K half's partial (commutative: same bits either way)
@@ -755,7 +763,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
-        epilogue_bias_act<EPI>(v, n0 + c, bias);
+        epilogue_bias_act<EPI>(v, bq, bias);
         if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) rope_chunk(v, n0 + c, rope_hd, rt, ct);
         if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
 #pragma unroll
