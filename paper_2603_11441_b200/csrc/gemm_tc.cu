@@ -147,6 +147,36 @@ __device__ __forceinline__ void rope_chunk(float* v, int col, int hd, const floa
   }
 }
 
+// rope_chunk for hd 80 (ViT-H/14) with the chunk's first pair index P0 = (col % 80) / 2 known at
+// compile time: the row / column angle choice and the wrap at 40 pairs fold away, and the tables
+// are read with ld.shared (the generic-pointer form above costs ~300 extra instructions per chunk
+// in index arithmetic and generic loads).  rt_s / ct_s: shared addresses of this token's rows.
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+  float2 r;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(addr));
+  return r;
+}
+template <int P0>
+__device__ __forceinline__ void rope_chunk80(float* v, uint32_t rt_s, uint32_t ct_s) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = (P0 + j) % 40;
+    const float2 cs = p < 20 ? lds_f2(rt_s + p * 8) : lds_f2(ct_s + (p - 20) * 8);
+    const float ev = v[2 * j], od = v[2 * j + 1];
+    v[2 * j] = ev * cs.x - od * cs.y;
+    v[2 * j + 1] = ev * cs.y + od * cs.x;
+  }
+}
+__device__ __forceinline__ void rope_chunk_hd80(float* v, int col, uint32_t rt_s, uint32_t ct_s) {
+  switch ((col % 80) >> 1) {  // col is a multiple of 32
+    case 0: rope_chunk80<0>(v, rt_s, ct_s); break;
+    case 8: rope_chunk80<8>(v, rt_s, ct_s); break;
+    case 16: rope_chunk80<16>(v, rt_s, ct_s); break;
+    case 24: rope_chunk80<24>(v, rt_s, ct_s); break;
+    default: rope_chunk80<32>(v, rt_s, ct_s); break;
+  }
+}
+
 // fp16 storage rounding, saturating at +-65504 like the reference's half_round (tensors.py:99-109)
 __device__ __forceinline__ float sat_f16(float x) { return fminf(fmaxf(x, -65504.0f), 65504.0f); }
 __device__ __forceinline__ float round_f16(float x) { return __half2float(__float2half_rn(sat_f16(x))); }
@@ -714,8 +744,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         __syncwarp();
-        float4 bq[8];
-        bias_prefetch(bq, n0 + c, bias);
+        float4 bq[8];  // (the RoPE epilogue loads its bias after the TMEM wait: register budget)
+        if constexpr (EPI != EPI_QKV_ROPE) bias_prefetch(bq, n0 + c, bias);
         float v[32];
         tmem_ld32(taddr + c, v);
         if constexpr (SPLITK) {  // + the other K half's partial (commutative: same bits either way)
@@ -763,8 +793,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+        if constexpr (EPI == EPI_QKV_ROPE) bias_prefetch(bq, n0 + c, bias);
         epilogue_bias_act<EPI>(v, bq, bias);
-        if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) rope_chunk(v, n0 + c, rope_hd, rt, ct);
+        if (EPI == EPI_QKV_ROPE && n0 + c < rope_cols) {
+          if (rope_hd == 80)  // ViT-H/14: compile-time pair indices, ld.shared
+            rope_chunk_hd80(v, n0 + c, (uint32_t)__cvta_generic_to_shared(rt), (uint32_t)__cvta_generic_to_shared(ct));
+          else
+            rope_chunk(v, n0 + c, rope_hd, rt, ct);
+        }
         if ((PREC && epi.round_f16)) {  // fp16 storage: fp32 outputs rounded, fp16 outputs saturated
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = (EPI == EPI_F32 || EPI == EPI_F32_F16) ? round_f16(v[j]) : sat_f16(v[j]);
