@@ -679,6 +679,10 @@ int fa_variant() {
   X(5, 16, 80, 4, 2, 2, 1, 6, 16, 0, 1)  \
   X(7, 16, 64, 4, 1, 1, 1, 6, 16, 0, 4)  \
   X(8, 16, 96, 4, 1, 1, 1, 6, 16, 0, 3)
+// hd 80 with polynomial exponentials (hook-free NPOLY 2 / 4 / 6 of 16, interleaved A/B,
+// profiles/r02/attn_hd80_poly_share_ab.log): global 168 -> 175 / 177 / 178 us, windowed 27.4-28.3
+// -> 27.2-27.7 us (noise): the hd-80 tile is co-bound by MUFU (512 clk per 128 x 64 tile) and the
+// tensor pipe (352 clk), so the FMA-pipe polynomial only lengthens the softmax instruction stream.
 // Variant 0 issues MMAs from the converged warp 1 (warp-collective umma_*_w, one elected lane):
 // the per-MMA issue path shrank from ~77 to ~40 clk (no per-lane R2UR waterfall), which took hd 80
 // global attention 217 -> 193 us and windowed 36.5 -> 33.2 us (scripts/ab_attn.py); with it the
