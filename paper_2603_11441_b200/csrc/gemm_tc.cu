@@ -958,6 +958,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // The MMA order fc1(0) fc1(1) fc2(0) fc1(2) fc2(1) ... fc1(7) fc2(6) fc2(7) lets the conversion of
 // slice e overlap fc1(e+1); an in-order tensor pipe guarantees fc2(e) has read P(e) before
 // fc1(e+2) overwrites the region.
+// MLP_PROBE (timing probes only, separate builds): bit 0 skips the residual epilogue, bit 1 the
+// slice conversion (outputs are garbage; scripts/gpu_mlp_probe.sh)
+#ifndef MLP_PROBE
+#define MLP_PROBE 0
+#endif
 namespace mlpf {
 constexpr int D = 256, HID = 1024, SL = 128, NSL = HID / SL;  // model dims, hidden slice, slices
 constexpr int A_BYTES = BM * D * 2;                            // resident h rows of this CTA (64 KB)
@@ -1153,7 +1158,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         const uint32_t rb = lane_base + (e & 1) * SL;
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {  // this warp: hidden units [64 * half, 64 * half + 64) of the slice
+        for (int c = 0; c < ((MLP_PROBE & 2) ? 0 : 2); ++c) {  // this warp: hidden units [64 * half, 64 * half + 64) of the slice
           const int col = half * 64 + c * 32;
           float v[32];
           tmem_ld32(rb + col, v);
@@ -1176,6 +1181,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // residual epilogue: x += acc2 + b2 (this warp: 32-column chunks half, half + 2, ...)
       mbar_wait(o_full, it & 1);
       tc_fence_after();
+      if constexpr ((MLP_PROBE & 1) != 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(o_empty);
+        continue;
+      }
       const bool lno = ln_g != nullptr;
       float ln_sum = 0.f;
 #pragma unroll 1
