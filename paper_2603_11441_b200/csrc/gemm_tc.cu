@@ -17,6 +17,8 @@
 // 25-33% lower than the 1-SM form; both CTAs' TMA loads complete on the leader's full barrier,
 // MMA completion is multicast to both CTAs' empty / accumulator-full barriers, and both CTAs'
 // epilogue warps release the accumulator on the leader's barrier.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -963,6 +965,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #ifndef MLP_PROBE
 #define MLP_PROBE 0
 #endif
+// MLP_DEFER 1: the epilogue warps copy the fc2 accumulator into registers and release it at once
+// (setmaxnreg: 80 registers for the TMA / MMA warp group, 208 for the two epilogue warp groups);
+// the residual add, stores and LayerNorm of unit u then run in pieces between the slice conversions
+// of unit u+1, so the next unit's fc2 never waits for them.  0: the accumulator is held through
+// the residual / LayerNorm epilogue (A/B builds).
+#ifndef MLP_DEFER
+#define MLP_DEFER 1
+#endif
 namespace mlpf {
 constexpr int D = 256, HID = 1024, SL = 128, NSL = HID / SL;  // model dims, hidden slice, slices
 constexpr int A_BYTES = BM * D * 2;                            // resident h rows of this CTA (64 KB)
@@ -1029,10 +1039,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
+  // MLP_DEFER register split: every warp of a warp group executes the same setmaxnreg, at the top
+  // of its role branch (warps 2 / 3 of the first group have no role after the TMEM allocation)
+  auto regs_dec = [] {
+    if constexpr (MLP_DEFER) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+  };
 
   // Ring sequence per unit: W1(0) W1(1) W2(0) W1(2) W2(1) ... W1(7) W2(6) W2(7); W1(e) = 4 k-blocks
   // (K = 256), W2(e) = 2 k-blocks (K = 128 hidden units of slice e).
   if (warp == 0) {
+    regs_dec();
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -1066,6 +1082,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
+    regs_dec();
     if (rank == 0) {  // converged warp, one elected lane issues
       constexpr uint32_t idesc1 = umma_idesc_f16(BM * CG, SL);
       constexpr uint32_t idesc2 = umma_idesc_f16(BM * CG, D);
@@ -1132,6 +1149,200 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fc2(NSL - 1);
       }
     }
+  } else if (MLP_DEFER && warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    float* bufs = reinterpret_cast<float*>(smem + OFF_EPI) + (warp - 4) * 2048;
+    uint64_t* rbar = rfull + (warp - 4) * 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float* const bias1 = b1;  // hoisted kernel parameters (no reloads after asm clobbers)
+    const float* const bias2 = b2;
+    const float* const lng = ln_g;
+    const float* const lnb = ln_b;
+    const bool lno = lng != nullptr;
+    float* const red = reinterpret_cast<float*>(smem + OFF_RED) + quarter * 64;
+    // deferred unit: its fc2 accumulator, then x + acc + b2, chunk i (columns (2 i + half) * 32 + k)
+    // at st[32 i + k]; drow0: its first row for this warp
+    float st[128];
+    int drow0 = 0, g = 0;  // g: residual chunks loaded by this warp (buffer g & 1, phase (g >> 1) & 1)
+    bool have = false;
+    float ln_sum = 0.f, mu = 0.f, rstd = 0.f;
+    auto resid_load = [&](int chunk, int gg) {
+      mbar_arrive_expect_tx(&rbar[gg & 1], 32 * 32 * 4);
+      tma_load_2d(bufs + (gg & 1) * 1024, &tmX, &rbar[gg & 1], (chunk * 2 + half) * 32, drow0);
+    };
+    // piece `step` of the deferred epilogue: 0..3 residual chunk `step`, 4 LN statistics, 5 / 6 LN
+    // output chunks 0-1 / 2-3 (the same IEEE-pinned arithmetic as ln_rows_epilogue)
+    auto defer_step = [&](auto step_c) {
+      constexpr int c = decltype(step_c)::value;
+      if constexpr (c < 4) {
+        const int col = (c * 2 + half) * 32;
+        float* buf = bufs + (g & 1) * 1024;
+        if (lane == 0 && c < 3) {  // chunk c + 1 into the other buffer (chunk c - 1's store has read it)
+          bulk_wait_read0();
+          resid_load(c + 1, g + 1);
+        }
+        __syncwarp();
+        const float4* bb = reinterpret_cast<const float4*>(bias2 + col);
+        mbar_wait(&rbar[g & 1], (g >> 1) & 1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 bq = __ldg(bb + q);
+          float4* sp = slot32(buf, lane, q);
+          float4 x = *sp;
+          x.x += st[32 * c + 4 * q] + bq.x;
+          x.y += st[32 * c + 4 * q + 1] + bq.y;
+          x.z += st[32 * c + 4 * q + 2] + bq.z;
+          x.w += st[32 * c + 4 * q + 3] + bq.w;
+          *sp = x;
+          st[32 * c + 4 * q] = x.x;
+          st[32 * c + 4 * q + 1] = x.y;
+          st[32 * c + 4 * q + 2] = x.z;
+          st[32 * c + 4 * q + 3] = x.w;
+        }
+        if (lno) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) ln_sum = __fadd_rn(ln_sum, st[32 * c + k]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmX, buf, col, drow0);
+          tma_store_commit();
+        }
+        ++g;
+      } else if constexpr (c == 4) {
+        if (lno) {
+          red[half * 32 + lane] = ln_sum;
+          named_bar_sync(2 + quarter, 64);
+          mu = __fmul_rn(__fadd_rn(red[lane], red[32 + lane]), 1.0f / 256.0f);
+          named_bar_sync(2 + quarter, 64);  // both partners have read the sums before `red` is reused
+          float q = 0.f;
+#pragma unroll
+          for (int k = 0; k < 128; ++k) {
+            const float d = __fsub_rn(st[k], mu);
+            q = __fmaf_rn(d, d, q);
+          }
+          red[half * 32 + lane] = q;
+          named_bar_sync(2 + quarter, 64);
+          const float var = __fmul_rn(__fadd_rn(red[lane], red[32 + lane]), 1.0f / 256.0f);
+          named_bar_sync(2 + quarter, 64);
+          rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-6f)));
+        }
+      } else {
+        if (lno) {
+#pragma unroll
+          for (int i = (c - 5) * 2; i < (c - 5) * 2 + 2; ++i) {
+            const int cc = half * 32 + 64 * i;
+            const float4* g4 = reinterpret_cast<const float4*>(lng + cc);
+            const float4* b4 = reinterpret_cast<const float4*>(lnb + cc);
+            float y[32];
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) {
+              const float4 gg = __ldg(g4 + qq), bb = __ldg(b4 + qq);
+              y[4 * qq] = __fmaf_rn(__fmul_rn(__fsub_rn(st[32 * i + 4 * qq], mu), rstd), gg.x, bb.x);
+              y[4 * qq + 1] = __fmaf_rn(__fmul_rn(__fsub_rn(st[32 * i + 4 * qq + 1], mu), rstd), gg.y, bb.y);
+              y[4 * qq + 2] = __fmaf_rn(__fmul_rn(__fsub_rn(st[32 * i + 4 * qq + 2], mu), rstd), gg.z, bb.z);
+              y[4 * qq + 3] = __fmaf_rn(__fmul_rn(__fsub_rn(st[32 * i + 4 * qq + 3], mu), rstd), gg.w, bb.w);
+            }
+            float* lb = bufs + (i & 1) * 1024;
+            if (lane == 0) {  // the stores that last used this staging chunk have read it
+              if (i == 0)
+                bulk_wait_read0();
+              else
+                bulk_wait_read1();
+            }
+            __syncwarp();
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              uint4 u;
+              u.x = pack_half2(y[8 * qq + 0], y[8 * qq + 1]);
+              u.y = pack_half2(y[8 * qq + 2], y[8 * qq + 3]);
+              u.z = pack_half2(y[8 * qq + 4], y[8 * qq + 5]);
+              u.w = pack_half2(y[8 * qq + 6], y[8 * qq + 7]);
+              *slot16_sw64(lb, lane, qq) = u;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmLN, lb, cc, drow0);
+              tma_store_commit();
+            }
+          }
+        }
+      }
+    };
+    // slice e of the current unit: relu(acc + b1) -> fp16 pairs over the slice's first half (own
+    // columns), then piece e of the previous unit's epilogue
+    auto slice = [&](auto e_c, int it) {
+      constexpr int e = decltype(e_c)::value;
+      const int use = it * (NSL / 2) + (e >> 1);
+      mbar_wait(&s_full[e & 1], use & 1);
+      tc_fence_after();
+      const uint32_t rb = lane_base + (e & 1) * SL;
+#pragma unroll 1
+      for (int c = 0; c < ((MLP_PROBE & 2) ? 0 : 2); ++c) {
+        const int col = half * 64 + c * 32;
+        float v[32];
+        tmem_ld32(rb + col, v);
+        tmem_ld_wait();
+        const float4* bb = reinterpret_cast<const float4*>(bias1 + e * SL + col);
+        uint32_t pk[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 bq = __ldg(bb + q);
+          pk[2 * q] = pack_half2(fmaxf(v[4 * q] + bq.x, 0.f), fmaxf(v[4 * q + 1] + bq.y, 0.f));
+          pk[2 * q + 1] = pack_half2(fmaxf(v[4 * q + 2] + bq.z, 0.f), fmaxf(v[4 * q + 3] + bq.w, 0.f));
+        }
+        tmem_st16(rb + half * 64 + c * 16, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&p_full[e & 1]);
+      if constexpr (e < 7) {
+        if (have) defer_step(e_c);
+      }
+    };
+    int it = 0;
+    for (int unit = cl; unit < num_units; unit += ncl, ++it) {
+      const int row0 = unit * BM * CG + rank * BM + quarter * 32;
+      slice(std::integral_constant<int, 0>{}, it);
+      slice(std::integral_constant<int, 1>{}, it);
+      slice(std::integral_constant<int, 2>{}, it);
+      slice(std::integral_constant<int, 3>{}, it);
+      slice(std::integral_constant<int, 4>{}, it);
+      slice(std::integral_constant<int, 5>{}, it);
+      slice(std::integral_constant<int, 6>{}, it);
+      slice(std::integral_constant<int, 7>{}, it);
+      // the fc2 accumulator into registers, released before any of its epilogue runs
+      mbar_wait(o_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(lane_base + 256 + (c * 2 + half) * 32, st + 32 * c);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(o_empty);
+      if constexpr ((MLP_PROBE & 1) != 0) continue;
+      drow0 = row0;
+      have = true;
+      ln_sum = 0.f;
+      if (lane == 0) {
+        bulk_wait_read0();
+        resid_load(0, g);
+      }
+    }
+    if (have) {
+      defer_step(std::integral_constant<int, 0>{});
+      defer_step(std::integral_constant<int, 1>{});
+      defer_step(std::integral_constant<int, 2>{});
+      defer_step(std::integral_constant<int, 3>{});
+      defer_step(std::integral_constant<int, 4>{});
+      defer_step(std::integral_constant<int, 5>{});
+      defer_step(std::integral_constant<int, 6>{});
+    }
+    if (lane == 0) bulk_wait_all();
   } else if (warp >= 4) {
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     float* bufs = reinterpret_cast<float*>(smem + OFF_EPI) + (warp - 4) * 2048;
@@ -1245,6 +1456,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_all();
+  } else if (warp < 4) {
+    regs_dec();  // warps 2 / 3: no role
   }
   pdl_launch_dependents();
   tc_fence_before();
