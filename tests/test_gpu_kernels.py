@@ -452,7 +452,7 @@ def test_mlp_fused(lib, M):
     assert rel_err(out, ref) < 2e-3
 
 
-@pytest.mark.parametrize("M", [300, 20736, 41472])
+@pytest.mark.parametrize("M", [300, 20736, 41472, 75776 + 77])  # last: several units per CTA pair, ragged tail
 def test_mlp_fused_layernorm_equals_gemm_path(lib, M):
     """The fused MLP kernel's LN epilogue and the GEMM path (fc1 GEMM + fc2 GEMM with the
     EPI_F32_RESID_LN epilogue) give identical bits for x and h = LN(x): the enc-dec picks one or
