@@ -40,6 +40,18 @@ for name, (B, H, L, hd) in {"att16": (4, 16, 5184, 16), "att80": (1, 16, 5184, 8
     o = torch.empty(B * L, E, device="cuda", dtype=torch.float16)
     calls.append((name, lambda qkv=qkv, o=o, B=B, H=H, L=L, hd=hd: _native.check(
         lib.dart_attention_qkv(qkv.data_ptr(), o.data_ptr(), B, H, L, hd, None, st))))
+if "mlp80" in which:  # fused enc-dec MLP with the next LayerNorm at the N=80 row count
+    M = 414720
+    h = torch.randn(M, 256, device="cuda").half()
+    w1 = (torch.randn(1024, 256, device="cuda") / 16).half()
+    w2 = (torch.randn(256, 1024, device="cuda") / 32).half()
+    b1, b2 = torch.zeros(1024, device="cuda"), torch.zeros(256, device="cuda")
+    lg, lb = torch.ones(256, device="cuda"), torch.zeros(256, device="cuda")
+    x = torch.randn(M, 256, device="cuda")
+    ho = torch.empty(M, 256, device="cuda").half()
+    calls.append(("mlp80", lambda: _native.check(lib.dart_mlp_fused_ln(
+        h.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), x.data_ptr(), ho.data_ptr(),
+        lg.data_ptr(), lb.data_ptr(), M, st))))
 for _, f in calls:
     f()
 torch.cuda.synchronize()
